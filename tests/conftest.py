@@ -1,0 +1,58 @@
+"""Shared test configuration.
+
+Markers: ``gpu`` = needs a B200 (run on the GPU box with ``-m gpu``); all other
+tests run on the CPU-only build container.  The CPU oracle (``oracle/``) is test
+infrastructure: tests use it only as the checker.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 device (run with -m gpu)")
+
+
+def load_golden(name):
+    return dict(np.load(os.path.join(GOLDEN, f"{name}.npz")))
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle import cgs_oracle
+
+    cgs_oracle.build_loops()
+    return cgs_oracle
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def grads_close(a, b, rtol, floor_frac):
+    """Per-parameter-column relative L2 with an absolute floor.
+
+    Column j passes when ||a_j - b_j|| <= rtol * max(||b_j||, floor_frac * ||b||).
+    The floor matters only for columns that are analytically zero (e.g. quaternion
+    gradients of isotropic Gaussians, which the reference returns as ~1e-18
+    rounding noise).  Returns the list of worst relative errors per column.
+    """
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    floor = floor_frac * np.linalg.norm(b)
+    errs = []
+    for j in range(b.shape[1]):
+        den = max(np.linalg.norm(b[:, j]), floor)
+        errs.append(float(np.linalg.norm(a[:, j] - b[:, j]) / den))
+    assert max(errs) <= rtol, errs
+    return errs

@@ -1,0 +1,244 @@
+"""Generate the golden fixtures in tests/golden/ by RUNNING THE REFERENCE.
+
+Run in the build container only (it imports the reference package from
+/root/reference, which does not exist on the GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+The fixtures pin the CPU oracle (oracle/cgs_oracle.py): tests/test_oracle_golden.py
+checks the oracle against them, and the GPU parity tests check the CUDA path
+against the oracle.  Every input below is generated with the reference's own
+seeded generators (init_random, sample_pose, make_phantom, random_mixture of
+the reference conftest), so the oracle can regenerate the inputs bit-exactly.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import cryosplat as cs  # noqa: E402
+from cryosplat import _kernels  # noqa: E402
+from cryosplat.gmm import PARAMS_PER_GAUSSIAN, inverse_activate  # noqa: E402
+from cryosplat.simulate import sample_pose  # noqa: E402
+from cryosplat.splat import CLAMP_EVENTS, _Projection  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def random_mixture(rng, n, grid, scale_px=(1.0, 3.0), mean_range=0.2, amp_range=(0.3, 2.0)):
+    """Same draws as the reference tests' conftest.random_mixture (conftest.py:48-62)."""
+    params = np.zeros((n, PARAMS_PER_GAUSSIAN))
+    params[:, 0:3] = rng.uniform(-mean_range, mean_range, (n, 3))
+    params[:, 3:6] = inverse_activate(rng.uniform(*scale_px, (n, 3)) * grid.pixel_width)
+    params[:, 6:10] = rng.standard_normal((n, 4))
+    params[:, 10] = inverse_activate(rng.uniform(*amp_range, n))
+    return cs.GaussianMixture(params)
+
+
+def random_pose(rng, translation_range=0.0):
+    """conftest.random_pose (conftest.py:65-67)."""
+    t = rng.uniform(-translation_range, translation_range, 2) if translation_range else np.zeros(2)
+    return cs.Pose.from_quaternion(rng.standard_normal(4), t)
+
+
+def observed_stack(truth, poses, grid, ctfs, snr, noise_seed0):
+    clean = []
+    for pose, ctf in zip(poses, ctfs):
+        img = cs.rasterize(truth, pose, grid)
+        if ctf is not None:
+            img = cs.apply_ctf(img, ctf)
+        clean.append(img.pixels)
+    clean = np.stack(clean)
+    sigma = float(np.sqrt(clean.var() / snr))
+    obs = np.stack([
+        clean[i] + np.random.default_rng(noise_seed0 + i).normal(0.0, sigma, clean[i].shape)
+        for i in range(len(poses))
+    ]).astype(np.float32)
+    return obs
+
+
+def per_image(mix, pose, grid, H, obs, tile=16):
+    proj = _Projection(mix, pose, grid)
+    ntx = -(-grid.size // tile)
+    ids, starts = _kernels.build_tile_work(proj.bbox, tile, ntx, ntx)
+    rendered = cs.rasterize(mix, pose, grid).pixels
+    model = rendered if H is None else cs.apply_ctf(cs.RenderedImage(grid, rendered), H).pixels
+    loss = cs.loss_mse(model, obs)
+    d = grid.size
+    dL = (2.0 / (d * d)) * (model - obs)
+    up = dL if H is None else cs.apply_ctf(cs.RenderedImage(grid, dL), H).pixels
+    sums = np.zeros((len(mix), 6))
+    _kernels.backward_pixels(up, proj.mean2, proj.prec, proj.bbox, grid.pixel_width,
+                             grid.origin_index, 42.25, float(np.exp(-21.125)), sums)
+    grads = cs.rasterize_backward(mix, pose, grid, up)
+    return dict(bbox=proj.bbox, ids=ids.astype(np.int32), starts=starts, rendered=rendered,
+                model=model, loss=loss, upstream=up, sums=sums, grads=grads, n_clamped=proj.n_clamped)
+
+
+def stack_case(name, n, D, B, with_ctf, seed_obs=11, light=False):
+    grid = cs.GridSpec(D, 0.5, 1.5)
+    mix = cs.init_random(n, 0, grid)
+    poses = [sample_pose(np.random.default_rng(1000 + i)) for i in range(B)]
+    ctfs = []
+    for i in range(B):
+        if with_ctf:
+            d = float(np.random.default_rng(3000 + i).uniform(1e4, 2.5e4))
+            ctfs.append(cs.CtfParams(defocus_u=d, defocus_v=d))
+        else:
+            ctfs.append(None)
+    truth = cs.make_phantom("helix", 50, 0)
+    obs = observed_stack(truth, poses, grid, ctfs, 0.1, seed_obs)
+    out = {"D": D, "n": n, "B": B}
+    rendered, models, ups, sums, losses, grads = [], [], [], [], [], []
+    ids_all, starts_all, bbox_all, clamped = [], [], [], []
+    for i in range(B):
+        H = None if ctfs[i] is None else cs.ctf_evaluate(ctfs[i], grid)
+        r = per_image(mix, poses[i], grid, H, obs[i])
+        rendered.append(r["rendered"]); models.append(r["model"]); ups.append(r["upstream"])
+        sums.append(r["sums"]); losses.append(r["loss"]); grads.append(r["grads"])
+        ids_all.append(r["ids"]); starts_all.append(r["starts"]); bbox_all.append(r["bbox"])
+        clamped.append(r["n_clamped"])
+    out["observed"] = obs
+    out["rendered"] = np.stack(rendered)
+    out["model"] = np.stack(models)
+    out["upstream"] = np.stack(ups)
+    out["losses"] = np.array(losses)
+    out["grads_mean"] = np.mean(grads, axis=0)
+    if not light:
+        out["grads_first"] = grads[0]
+        out["sums_first"] = sums[0]
+    out["bbox"] = np.stack(bbox_all).astype(np.int32)
+    out["tile_ids"] = np.concatenate(ids_all)
+    out["tile_starts"] = np.stack(starts_all)
+    out["n_clamped"] = np.array(clamped)
+    out["defocus"] = np.array([np.nan if c is None else c.defocus_u for c in ctfs])
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
+    print(name, {k: getattr(v, "shape", v) for k, v in out.items()})
+
+
+def kat_cases():
+    out = {}
+    grid64 = cs.GridSpec(64, 0.5, 3.0)
+    # test_splat.py:298-304 dense-oracle mixture, plus tile-size variants (:317-324)
+    rng = np.random.default_rng(6)
+    mix = random_mixture(rng, 64, grid64)
+    pose = random_pose(rng, translation_range=0.03)
+    out["dense_params"] = mix.params
+    out["dense_W"] = pose.rotation
+    out["dense_t"] = pose.translation
+    for tile in (8, 16, 32):
+        out[f"dense_render_tile{tile}"] = cs.rasterize(mix, pose, grid64, tile_size=tile).pixels
+        proj = _Projection(mix, pose, grid64)
+        ntx = -(-64 // tile)
+        ids, starts = _kernels.build_tile_work(proj.bbox, tile, ntx, ntx)
+        out[f"dense_ids_tile{tile}"] = ids
+        out[f"dense_starts_tile{tile}"] = starts
+    up = np.random.default_rng(77).standard_normal((64, 64))
+    out["dense_upstream"] = up
+    out["dense_grads"] = cs.rasterize_backward(mix, pose, grid64, up)
+    # eigenvalue floor (test_splat.py:347-358)
+    params = np.zeros((1, PARAMS_PER_GAUSSIAN))
+    params[0, 3:6] = inverse_activate(1e-6)
+    params[0, 6] = 1.0
+    params[0, 10] = inverse_activate(1.0)
+    CLAMP_EVENTS.reset()
+    out["clamp_render"] = cs.rasterize(cs.GaussianMixture(params), cs.Pose.identity(), grid64).pixels
+    out["clamp_count"] = np.array(CLAMP_EVENTS.count)
+    # anisotropic clamped Gaussians under random poses (needle-like)
+    rng = np.random.default_rng(21)
+    p = np.zeros((16, PARAMS_PER_GAUSSIAN))
+    p[:, 0:3] = rng.uniform(-0.2, 0.2, (16, 3))
+    p[:, 3] = inverse_activate(rng.uniform(2, 4, 16) * grid64.pixel_width)
+    p[:, 4] = inverse_activate(rng.uniform(0.01, 0.05, 16) * grid64.pixel_width)
+    p[:, 5] = inverse_activate(rng.uniform(0.01, 0.05, 16) * grid64.pixel_width)
+    p[:, 6:10] = rng.standard_normal((16, 4))
+    p[:, 10] = inverse_activate(rng.uniform(0.5, 1.5, 16))
+    pose = cs.Pose(np.eye(3))
+    CLAMP_EVENTS.reset()
+    out["needle_params"] = p
+    out["needle_render"] = cs.rasterize(cs.GaussianMixture(p), pose, grid64).pixels
+    out["needle_clamp_count"] = np.array(CLAMP_EVENTS.count)
+    up = np.random.default_rng(78).standard_normal((64, 64))
+    out["needle_upstream"] = up
+    out["needle_grads"] = cs.rasterize_backward(cs.GaussianMixture(p), pose, grid64, up)
+    # softplus / Adam KATs (test_gmm.py:118-122, test_train.py:71-79)
+    out["inv_act_5e-5"] = np.array(inverse_activate(5e-5))
+    st = cs.AdamState(1)
+    prm = np.zeros((1, 11))
+    rng = np.random.default_rng(3)
+    g1 = rng.standard_normal((1, 11))
+    g2 = rng.standard_normal((1, 11))
+    st.update(prm, g1, lr=0.01, config=cs.TrainConfig())
+    st.update(prm, g2, lr=0.01, config=cs.TrainConfig())
+    out["adam_g1"], out["adam_g2"], out["adam_params"] = g1, g2, prm.copy()
+    np.savez_compressed(os.path.join(OUT, "kat.npz"), **out)
+    print("kat", sorted(out))
+
+
+def ctf_cases():
+    out = {}
+    specs = [
+        (64, cs.CtfParams(defocus_u=15000.0, defocus_v=15000.0)),
+        (64, cs.CtfParams(defocus_u=18000.0, defocus_v=14000.0, astigmatism_angle=0.7)),
+        (33, cs.CtfParams(defocus_u=21000.0, defocus_v=12000.0, astigmatism_angle=2.1,
+                          phase_shift=0.3, b_factor=40.0, amplitude_contrast=0.07)),
+        (128, cs.CtfParams(defocus_u=24000.0, defocus_v=19000.0, astigmatism_angle=1.1,
+                           voltage=200.0, spherical_aberration=2.0)),
+    ]
+    rng = np.random.default_rng(5)
+    for i, (D, p) in enumerate(specs):
+        grid = cs.GridSpec(D, 0.5, 1.5)
+        H = cs.ctf_evaluate(p, grid)
+        img = rng.standard_normal((D, D))
+        out[f"ctf{i}_D"] = np.array(D)
+        out[f"ctf{i}_params"] = np.array([p.defocus_u, p.defocus_v, p.astigmatism_angle, p.voltage,
+                                          p.spherical_aberration, p.amplitude_contrast,
+                                          p.phase_shift, p.b_factor])
+        out[f"ctf{i}_H"] = H
+        out[f"ctf{i}_img"] = img
+        out[f"ctf{i}_applied"] = cs.apply_ctf(cs.RenderedImage(grid, img), H).pixels
+    out["lambda_300"] = np.array(cs.electron_wavelength(300.0))
+    np.savez_compressed(os.path.join(OUT, "ctf.npz"), **out)
+    print("ctf", sorted(out))
+
+
+def train_case():
+    """A tiny deterministic train() run (train.py:194-264) with B = 1 semantics."""
+    import tempfile
+
+    grid = cs.GridSpec(32, 0.5, 3.0)
+    rng = np.random.default_rng(7)
+    truth = random_mixture(rng, 6, grid, amp_range=(0.5, 1.5))
+    records = []
+    for _ in range(3):
+        pose = random_pose(rng)
+        ctf = cs.CtfParams(defocus_u=15000.0, defocus_v=15000.0)
+        img = cs.apply_ctf(cs.rasterize(truth, pose, grid), ctf).pixels
+        records.append(cs.ParticleRecord(image=img, pose=pose, ctf=ctf))
+    ds = cs.Dataset(records=records, grid=grid)
+    with tempfile.TemporaryDirectory() as d:
+        mix, losses = cs.train(ds, cs.TrainConfig(epochs=3, seed=0), n_gaussians=8, out_dir=d)
+        trace = open(os.path.join(d, "loss_trace.txt")).read()
+    out = {
+        "images": np.stack([r.image for r in records]),
+        "rotations": np.stack([r.pose.rotation for r in records]),
+        "final_params": mix.params,
+        "losses": np.stack(losses),
+        "trace": np.array(trace),
+    }
+    np.savez_compressed(os.path.join(OUT, "train_small.npz"), **out)
+    print("train_small", {k: getattr(v, "shape", v) for k, v in out.items()})
+
+
+if __name__ == "__main__":
+    stack_case("c1_step", 5000, 64, 4, with_ctf=False)
+    stack_case("c2_slice", 50000, 128, 2, with_ctf=True, light=True)
+    kat_cases()
+    ctf_cases()
+    train_case()
