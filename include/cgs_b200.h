@@ -1,0 +1,206 @@
+/*
+ * cgs_b200.h -- C ABI of the B200-native cryoGS splatting step (libcgs_b200.so).
+ *
+ * Every entry point takes raw DEVICE pointers, plain sizes, a cudaStream_t last
+ * (passed as void* so the header needs no CUDA include), never allocates device
+ * memory inside a step (FFT plans are created once up front), never
+ * synchronises the host, and returns 0 on success or a CGS_ERR_* code.  All
+ * launches are stream-ordered, so a whole step is CUDA-Graph capturable.
+ *
+ * Each function names the reference interface it replaces
+ * (/root/reference/pkg/src/cryosplat/<file>:<line>).  Batched entry points take
+ * B images; B = 1 reproduces the reference's one-image call.
+ *
+ * Data layouts (row-major, C-contiguous):
+ *   params   f64 [N][11]  mean xyz | raw scale xyz | quaternion wxyz | raw amp
+ *                         (gmm.py:25-29)
+ *   splat    f32 [N][16]  prepared per-Gaussian record (cgs_prepare)
+ *   poses    f64 [B][12]  rotation W row-major (9), translation tx ty (2), pad
+ *                         (splat.py:73-104; translation in normalised units)
+ *   ctf      f64 [B][8]   defocus_u, defocus_v [A], astigmatism_angle [rad],
+ *                         voltage [kV], Cs [mm], amplitude_contrast,
+ *                         phase_shift [rad], b_factor [A^2]   (optics.py:39-62)
+ *   images   f32 [B][D][D] in NATURAL layout (pixel (iy, ix), origin D//2) or
+ *                         FFT layout (np.fft.ifftshift of natural) when
+ *                         layout == CGS_LAYOUT_FFT.
+ */
+#ifndef CGS_B200_H
+#define CGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CGS_OK 0
+#define CGS_ERR_ARG 1         /* invalid argument (sizes, null pointers) */
+#define CGS_ERR_CUDA 2        /* a CUDA launch or runtime call failed */
+#define CGS_ERR_CUFFT 3       /* a cuFFT call failed */
+#define CGS_ERR_UNSUPPORTED 4 /* configuration outside the compiled limits */
+
+#define CGS_LAYOUT_NATURAL 0
+#define CGS_LAYOUT_FFT 1
+
+#define CGS_MODE_ANISOTROPIC 0
+#define CGS_MODE_ISOTROPIC 1
+
+#define CGS_SPLAT_STRIDE 16   /* floats per prepared splat record */
+#define CGS_ACC_STRIDE 10     /* floats per world-frame gradient accumulator */
+#define CGS_BIN_CHUNK 2048    /* Gaussians per binning segment */
+
+/* GridSpec (gmm.py:38-73): D pixels over [-extent, extent]; pixel_size in A. */
+typedef struct cgs_grid {
+    int32_t size;
+    int32_t reserved;
+    double extent;
+    double pixel_size;
+} cgs_grid;
+
+/* status bits written by cgs_prepare / cgs_bin_scatter into a device int32 */
+#define CGS_STATUS_DEGENERATE_ROTATION 1 /* DegenerateRotationError, splat.py:191-193 */
+#define CGS_STATUS_BIN_OVERFLOW 2        /* tile list exceeded the item capacity */
+#define CGS_STATUS_NONFINITE_LOSS 4      /* a loss was NaN/inf: Adam skips the update (train.py:144-145) */
+
+const char *cgs_version(void);
+const char *cgs_error_string(int code);
+/* last CUDA / cuFFT error text seen by the library (host string, thread-local) */
+const char *cgs_last_error_detail(void);
+
+/* ---- K0: per-Gaussian preparation ---------------------------------------
+ * Replaces the image-independent part of _Projection.__init__
+ * (splat.py:184-196): softplus activate (gmm.py:76-80), quaternion
+ * normalisation and rotation (gmm.py:101-124), M = R diag(s).
+ * Writes splat[N][16] = {mean xyz, amp, M (9, row-major), 0,0,0}.  A zero or
+ * non-finite quaternion norm sets CGS_STATUS_DEGENERATE_ROTATION in *status. */
+int cgs_prepare(const double *params, int64_t n, float *splat, int32_t *status, void *stream);
+
+/* ---- K2: tile binning (build_tile_work, _kernels.py:17-63) ----------------
+ * A stable, segmented counting sort (one LSD radix pass keyed on tile id,
+ * pre-grouped by image) that reproduces the reference's per-tile ascending
+ * Gaussian order bit-exactly.  Three launches: count -> scan -> scatter.
+ *
+ *   S      = cgs_bin_segments(n)           segments of CGS_BIN_CHUNK Gaussians
+ *   T      = ceil(D/tile)^2                tiles per image
+ *   counts = int32 [B*T*S + 1]             (b, tile, segment) item counts
+ *   offs   = int32 [B*T*S + 1]             exclusive scan of counts; offs[B*T*S]
+ *                                          = total items; tile (b,t) owns items
+ *                                          [offs[(b*T+t)*S], offs[(b*T+t+1)*S])
+ *   rects  = uint32 [B][n]                 packed tile rectangle per (b, g)
+ */
+int64_t cgs_bin_segments(int64_t n);
+int64_t cgs_bin_tiles(int32_t size, int32_t tile);
+
+/* Count pass from parameters: computes the reference's fp64 bounding box
+ * (splat.py:218-226, incl. the eigenvalue-floor clamp splat.py:229-260) per
+ * (image, Gaussian).  bbox_out (int32 [B][n][4], x0 x1 y0 y1) and clamp_count
+ * (int32 [B], CLAMP_EVENTS, splat.py:60-70,277) are optional (may be NULL). */
+int cgs_bin_count(const double *params, int64_t n, const double *poses, int32_t B, cgs_grid grid,
+                  int32_t tile, uint32_t *rects, int32_t *counts, int32_t *bbox_out,
+                  int32_t *clamp_count, void *stream);
+
+/* Count pass from a caller-supplied bbox (int32 [B][n][4]); used to check the
+ * binning on bit-identical input. */
+int cgs_bin_count_bbox(const int32_t *bbox, int64_t n, int32_t B, int32_t size, int32_t tile,
+                       uint32_t *rects, int32_t *counts, void *stream);
+
+/* Generic int32 exclusive scan of count elements (out may alias in).  ws must
+ * hold cgs_scan_workspace_bytes(count) bytes. */
+size_t cgs_scan_workspace_bytes(int64_t count);
+int cgs_exclusive_scan(const int32_t *in, int32_t *out, int64_t count, void *ws, void *stream);
+
+/* Scatter pass: items[pos] = g for every (b, g, tile) in the stable order.
+ * Items at or beyond capacity are dropped and CGS_STATUS_BIN_OVERFLOW is set. */
+int cgs_bin_scatter(const uint32_t *rects, int64_t n, int32_t B, int32_t size, int32_t tile,
+                    const int32_t *offs, int32_t *items, int64_t capacity, int32_t *status,
+                    void *stream);
+
+/* ---- K3: forward rasterizer (forward_tiles, _kernels.py:66-125; rasterize,
+ * splat.py:263-298) --------------------------------------------------------
+ * One CTA per (image, tile): stages the tile's Gaussians (ascending id) in
+ * shared memory and accumulates sum_g w_g (exp(-q/2) - sub) per pixel, q <
+ * 6.5^2, in the reference's per-pixel order.  out f32 [B][D][D]. */
+int cgs_raster_fwd(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
+                   int32_t tile, const int32_t *items, const int32_t *offs, int64_t capacity,
+                   float *out, int32_t layout, void *stream);
+
+/* ---- K4: CTF, centred FFTs and MSE (optics.py:78-141, train.py:114-121,153)
+ * ctf_evaluate (optics.py:93-121): H f64 [B][D][D], centred layout. */
+int cgs_ctf_evaluate(const double *ctf, int32_t B, cgs_grid grid, double *H, void *stream);
+
+/* cuFFT plans for a batch of B D x D real images (created once, reused). */
+int cgs_fft_plan_create(int32_t size, int32_t B, void **plan);
+int cgs_fft_plan_destroy(void *plan);
+/* complex64 elements of the spectrum workspace a plan needs: B*D*(D/2+1) */
+int64_t cgs_fft_spectrum_elems(int32_t size, int32_t B);
+
+/* apply_ctf (optics.py:124-141): out = Re F^-1( H . F(in) ) per image, computed
+ * as R2C -> multiply by H_sym(k) = (H(k) + H(-k mod D))/2 -> C2R (identical to
+ * the reference's complex form).  H comes from ctf (f64 [B][8])
+ * or, when ctf == NULL, from Harr (f64 [B][D][D], centred).  in/out may alias;
+ * spectrum holds cgs_fft_spectrum_elems complex64. */
+int cgs_ctf_apply(void *plan, const float *in, float *out, int32_t B, cgs_grid grid,
+                  const double *ctf, const double *Harr, void *spectrum, int32_t layout,
+                  void *stream);
+
+/* loss_mse (train.py:114-121) and dL/dmodel = 2/D^2 (model - obs)
+ * (train.py:153): loss f64 [B] (fp64 accumulation), resid f32 [B][D][D]
+ * (may be NULL).  A non-finite loss sets CGS_STATUS_NONFINITE_LOSS in *status
+ * (status may be NULL). */
+int cgs_loss_residual(const float *model, const float *obs, int32_t B, int32_t size,
+                      double *loss, float *resid, int32_t *status, void *stream);
+
+/* Fused K4 of one training step: model = CTF(render); loss; upstream =
+ * CTF(2/D^2 (model - obs)) (train.py:151-155).  ctf == NULL means no CTF (the
+ * operator is the identity).  model may be NULL.  Images in `layout`. */
+int cgs_ctf_mse(void *plan, const float *render, const float *obs, int32_t B, cgs_grid grid,
+                const double *ctf, void *spectrum, float *model, float *upstream, double *loss,
+                int32_t *status, int32_t layout, void *stream);
+
+/* ---- K5: fused backward (backward_pixels, _kernels.py:128-190, plus the
+ * per-image part of rasterize_backward, splat.py:332-349) ------------------
+ * Gaussian-major: each CTA owns a chunk of Gaussians and a group of images,
+ * stages each upstream image in shared memory, reduces per-Gaussian moments
+ * with warp shuffles and accumulates, over its images, the 10-float
+ * world-frame accumulator {cnorm sA, W2^T ac (sx, sy), W2^T (ac S) W2}
+ * (SURVEY.md 8(a) row 15).  Deterministic (no atomics).
+ *   partial f32 [G][n][10], G = cgs_bwd_groups(B, images_per_group). */
+int64_t cgs_bwd_groups(int32_t B, int32_t images_per_group);
+int cgs_raster_bwd(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
+                   const float *upstream, int32_t layout, float *partial,
+                   int32_t images_per_group, void *stream);
+
+/* Sum partial [G][n][10] over groups in fixed order -> acc f32 [n][10]
+ * (the buffer a multi-GPU run all-reduces). */
+int cgs_reduce_partials(const float *partial, int32_t G, int64_t n, float *acc, void *stream);
+
+/* ---- K6: epilogue + Adam (splat.py:344-381, train.py:157-159, train.py:101-111)
+ * grads f64 [n][11] = scale * chain(acc) for the raw parameters; mode
+ * isotropic sums the three raw-scale gradients (train.py:157-159). */
+int cgs_epilogue_grads(const float *acc, int32_t G, int64_t n, const double *params, int32_t mode,
+                       double scale, double *grads, void *stream);
+
+/* AdamState.update (train.py:101-111), fp64, in place; bc1 = 1 - beta1^t,
+ * bc2 = 1 - beta2^t. */
+int cgs_adam(double *params, const double *grads, double *m, double *v, int64_t count, double lr,
+             double beta1, double beta2, double eps, double bc1, double bc2, void *stream);
+
+/* Fused epilogue + Adam over acc [G][n][10].  When skip_if_status != NULL and
+ * *skip_if_status has CGS_STATUS_BIN_OVERFLOW or CGS_STATUS_NONFINITE_LOSS set,
+ * the update is skipped: the reference returns before Adam on a non-finite
+ * loss (train.py:144-145), and an overflowed tile list is re-run larger. */
+int cgs_epilogue_adam(const float *acc, int32_t G, int64_t n, double *params, double *m, double *v,
+                      int32_t mode, double scale, double lr, double beta1, double beta2, double eps,
+                      double bc1, double bc2, const int32_t *skip_if_status, void *stream);
+
+/* ---- measurement ----------------------------------------------------------
+ * In-ellipse (image, Gaussian, pixel) pairs q < 6.5^2: the algorithmic work
+ * unit of SURVEY.md 8(d).  pairs int64 [B] (accumulated, caller zeroes). */
+int cgs_count_pairs(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
+                    int64_t *pairs, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGS_B200_H */

@@ -1,0 +1,192 @@
+// K6: per-Gaussian epilogue and Adam.
+// Replaces the per-Gaussian chain of rasterize_backward (splat.py:344-381),
+// the isotropic tie (train.py:157-159) and AdamState.update (train.py:101-111).
+//
+// Input is the 10-float world-frame accumulator summed over images
+// {a, dmean (3), P (xx xy xz yy yz zz)}: dM = 2 P M with M = R diag(s)
+// image-independent, so the chain runs once per Gaussian per step instead of
+// once per (image, Gaussian).  fp64 throughout (parameters and moments are
+// fp64 master copies, so tiny late-epoch updates survive as in the reference).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace cgs {
+
+__device__ __forceinline__ double softplus_e(double x) { return fmax(x, 0.0) + log1p(exp(-fabs(x))); }
+__device__ __forceinline__ double sigmoid_e(double x) {
+    double e = exp(-fabs(x));  // gmm.py:83-88
+    return x >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
+}
+
+// grads[11] = scale * chain(acc) for one Gaussian
+__device__ void chain_grads(const double *__restrict__ raw, const double acc[10], double scale,
+                            int mode, double out[11]) {
+    double s[3], sig[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        s[j] = softplus_e(raw[3 + j]);
+        sig[j] = sigmoid_e(raw[3 + j]);
+    }
+    double qw = raw[6], qx = raw[7], qy = raw[8], qz = raw[9];
+    double qnorm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    bool ok = qnorm > 0.0 && isfinite(qnorm);
+    double inv = ok ? 1.0 / qnorm : 0.0;
+    double w = qw * inv, x = qx * inv, y = qy * inv, z = qz * inv;
+    if (!ok) w = 1.0;
+    double R[9];
+    R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+    R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+    R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+    double P[9] = {acc[4], acc[5], acc[6], acc[5], acc[7], acc[8], acc[6], acc[8], acc[9]};
+    // dM = 2 P M, M = R diag(s)
+    double dM[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            dM[3 * i + j] = 2.0 * (P[3 * i] * R[j] + P[3 * i + 1] * R[3 + j] + P[3 * i + 2] * R[6 + j]) * s[j];
+    double dscale[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dscale[j] = R[j] * dM[j] + R[3 + j] * dM[3 + j] + R[6 + j] * dM[6 + j];
+    double r[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) r[3 * i + j] = dM[3 * i + j] * s[j];
+    // d R(qn) / d qn contracted with dR (splat.py:351-372)
+    double d0 = 2 * (-z * r[1] + y * r[2] + z * r[3] - x * r[5] - y * r[6] + x * r[7]);
+    double d1 = 2 * (y * r[1] + z * r[2] + y * r[3] - 2 * x * r[4] - w * r[5] + z * r[6] + w * r[7] - 2 * x * r[8]);
+    double d2 = 2 * (-2 * y * r[0] + x * r[1] + w * r[2] + x * r[3] + z * r[5] - w * r[6] + z * r[7] - 2 * y * r[8]);
+    double d3 = 2 * (-2 * z * r[0] - w * r[1] + x * r[2] + w * r[3] - 2 * z * r[4] + y * r[5] + x * r[6] + y * r[7]);
+    double dot = d0 * w + d1 * x + d2 * y + d3 * z;  // splat.py:374
+    out[0] = scale * acc[1];
+    out[1] = scale * acc[2];
+    out[2] = scale * acc[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) out[3 + j] = scale * dscale[j] * sig[j];
+    out[6] = scale * (d0 - dot * w) * inv;
+    out[7] = scale * (d1 - dot * x) * inv;
+    out[8] = scale * (d2 - dot * y) * inv;
+    out[9] = scale * (d3 - dot * z) * inv;
+    out[10] = scale * acc[0] * sigmoid_e(raw[10]);
+    if (mode == CGS_MODE_ISOTROPIC) {  // train.py:157-159
+        double t = out[3] + out[4] + out[5];
+        out[3] = out[4] = out[5] = t;
+    }
+}
+
+__device__ __forceinline__ void sum_groups(const float *__restrict__ part, int G, int64_t n,
+                                           int64_t g, double acc[10]) {
+#pragma unroll
+    for (int c = 0; c < 10; ++c) acc[c] = 0.0;
+    for (int k = 0; k < G; ++k) {
+        const float *p = part + ((int64_t)k * n + g) * CGS_ACC_STRIDE;
+#pragma unroll
+        for (int c = 0; c < 10; ++c) acc[c] += (double)p[c];
+    }
+}
+
+// AdamState.update for one element, operation order as train.py:103-111
+__device__ __forceinline__ void adam_elem(double &p, double g, double &m, double &v, double lr,
+                                          double b1, double b2, double eps, double bc1, double bc2) {
+    m = __dadd_rn(__dmul_rn(m, b1), __dmul_rn(1.0 - b1, g));
+    v = __dadd_rn(__dmul_rn(v, b2), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
+    double mh = m / bc1;
+    double vh = v / bc2;
+    p = __dsub_rn(p, __dmul_rn(lr, mh) / __dadd_rn(sqrt(vh), eps));
+}
+
+__global__ void reduce_partials_kernel(const float *__restrict__ part, int G, int64_t n,
+                                       float *__restrict__ acc) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * CGS_ACC_STRIDE) return;
+    float s = 0.f;
+    for (int k = 0; k < G; ++k) s += part[(int64_t)k * n * CGS_ACC_STRIDE + i];
+    acc[i] = s;
+}
+
+__global__ void epilogue_grads_kernel(const float *__restrict__ part, int G, int64_t n,
+                                      const double *__restrict__ params, int mode, double scale,
+                                      double *__restrict__ grads) {
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    double acc[10], out[11];
+    sum_groups(part, G, n, g, acc);
+    chain_grads(params + 11 * g, acc, scale, mode, out);
+#pragma unroll
+    for (int j = 0; j < 11; ++j) grads[11 * g + j] = out[j];
+}
+
+__global__ void adam_kernel(double *__restrict__ params, const double *__restrict__ grads,
+                            double *__restrict__ m, double *__restrict__ v, int64_t count,
+                            double lr, double b1, double b2, double eps, double bc1, double bc2) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    double p = params[i], mm = m[i], vv = v[i];
+    adam_elem(p, grads[i], mm, vv, lr, b1, b2, eps, bc1, bc2);
+    params[i] = p;
+    m[i] = mm;
+    v[i] = vv;
+}
+
+__global__ void epilogue_adam_kernel(const float *__restrict__ part, int G, int64_t n,
+                                     double *__restrict__ params, double *__restrict__ m,
+                                     double *__restrict__ v, int mode, double scale, double lr,
+                                     double b1, double b2, double eps, double bc1, double bc2,
+                                     const int32_t *__restrict__ skip) {
+    if (skip && (*skip & (CGS_STATUS_BIN_OVERFLOW | CGS_STATUS_NONFINITE_LOSS))) return;
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    double acc[10], gr[11];
+    sum_groups(part, G, n, g, acc);
+    double *p = params + 11 * g;
+    chain_grads(p, acc, scale, mode, gr);
+    double *mg = m + 11 * g, *vg = v + 11 * g;
+#pragma unroll
+    for (int j = 0; j < 11; ++j) {
+        double pj = p[j], mj = mg[j], vj = vg[j];
+        adam_elem(pj, gr[j], mj, vj, lr, b1, b2, eps, bc1, bc2);
+        p[j] = pj;
+        mg[j] = mj;
+        vg[j] = vj;
+    }
+}
+
+}  // namespace cgs
+
+using namespace cgs;
+
+extern "C" int cgs_reduce_partials(const float *partial, int32_t G, int64_t n, float *acc, void *stream) {
+    if (G <= 0 || n <= 0 || !partial || !acc) return CGS_ERR_ARG;
+    int64_t tot = n * CGS_ACC_STRIDE;
+    reduce_partials_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(partial, G, n, acc);
+    return check_launch("reduce_partials_kernel");
+}
+
+extern "C" int cgs_epilogue_grads(const float *acc, int32_t G, int64_t n, const double *params,
+                                  int32_t mode, double scale, double *grads, void *stream) {
+    if (G <= 0 || n <= 0 || !acc || !params || !grads) return CGS_ERR_ARG;
+    epilogue_grads_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        acc, G, n, params, mode, scale, grads);
+    return check_launch("epilogue_grads_kernel");
+}
+
+extern "C" int cgs_adam(double *params, const double *grads, double *m, double *v, int64_t count,
+                        double lr, double beta1, double beta2, double eps, double bc1, double bc2,
+                        void *stream) {
+    if (count <= 0 || !params || !grads || !m || !v) return CGS_ERR_ARG;
+    adam_kernel<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        params, grads, m, v, count, lr, beta1, beta2, eps, bc1, bc2);
+    return check_launch("adam_kernel");
+}
+
+extern "C" int cgs_epilogue_adam(const float *acc, int32_t G, int64_t n, double *params, double *m,
+                                 double *v, int32_t mode, double scale, double lr, double beta1,
+                                 double beta2, double eps, double bc1, double bc2,
+                                 const int32_t *skip_if_status, void *stream) {
+    if (G <= 0 || n <= 0 || !acc || !params || !m || !v) return CGS_ERR_ARG;
+    epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        acc, G, n, params, m, v, mode, scale, lr, beta1, beta2, eps, bc1, bc2, skip_if_status);
+    return check_launch("epilogue_adam_kernel");
+}

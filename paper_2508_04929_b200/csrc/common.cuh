@@ -1,0 +1,153 @@
+// Shared device helpers for the sm_100a cryoGS kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cgs_b200.h"
+
+namespace cgs {
+
+constexpr double kCullSigma = 6.5;                 // splat.py:49
+constexpr double kCutoffSqD = kCullSigma * kCullSigma;
+constexpr float kCutoffSq = 42.25f;
+constexpr double kPiD = 3.14159265358979323846;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kEigenFloorPx2 = 0.01f;            // (EIGEN_FLOOR_FRACTION * h)^2 / h^2, splat.py:55
+// sub = exp(-cutoff_sq / 2) (splat.py:51) as the fp32 boundary value
+constexpr float kSub = 6.6915861e-10f;
+// the same boundary in log2 units: log2(sub) = -21.125 * log2(e)
+constexpr float kL2Cut = -21.125f * 1.4426950408889634f;
+
+void set_error_detail(const char *what, const char *detail);
+int check_launch(const char *what);
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Image-independent geometry of one Gaussian, written by cgs_prepare:
+// rec[0..2] mean, rec[3] amp, rec[4..12] M = R diag(s) row-major.
+struct SplatRec {
+    float mx, my, mz, amp;
+    float M[9];
+};
+
+__device__ __forceinline__ SplatRec load_splat(const float *__restrict__ splat, int64_t g) {
+    const float4 *p = reinterpret_cast<const float4 *>(splat + g * CGS_SPLAT_STRIDE);
+    float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3);
+    SplatRec r;
+    r.mx = a.x; r.my = a.y; r.mz = a.z; r.amp = a.w;
+    r.M[0] = b.x; r.M[1] = b.y; r.M[2] = b.z; r.M[3] = b.w;
+    r.M[4] = c.x; r.M[5] = c.y; r.M[6] = c.z; r.M[7] = c.w;
+    r.M[8] = d.x;
+    return r;
+}
+
+// Pose of one image in fp32 for the raster kernels: rows 0/1 of W and t.
+struct PoseF {
+    float w0[3], w1[3], tx, ty;
+};
+
+__device__ __forceinline__ PoseF load_pose_f(const double *__restrict__ poses, int b) {
+    const double *p = poses + 12 * (int64_t)b;
+    PoseF q;
+    q.w0[0] = (float)p[0]; q.w0[1] = (float)p[1]; q.w0[2] = (float)p[2];
+    q.w1[0] = (float)p[3]; q.w1[1] = (float)p[4]; q.w1[2] = (float)p[5];
+    q.tx = (float)p[9]; q.ty = (float)p[10];
+    return q;
+}
+
+// Grid constants in the units the raster kernels use (pixels).
+struct GridF {
+    int D;
+    float c0;      // origin pixel index D//2
+    float inv_h;   // 1 / pixel_width
+    float inv_2pi_h2;  // 1 / (2 pi h^2): cnorm in normalised units from a px^2 det
+};
+
+__host__ __forceinline__ GridF make_grid_f(const cgs_grid &g) {
+    GridF f;
+    f.D = g.size;
+    f.c0 = (float)(g.size / 2);
+    double h = 2.0 * g.extent / g.size;
+    f.inv_h = (float)(1.0 / h);
+    f.inv_2pi_h2 = (float)(1.0 / (2.0 * kPiD * h * h));
+    return f;
+}
+
+// Screen-space Gaussian of one (image, Gaussian) pair in pixel units: the
+// fp32 restatement of _Projection.__init__ (splat.py:184-226) and
+// _clamp_eigenvalues (splat.py:229-260).
+//   q(dx, dy) = p00 dx^2 + 2 p01 dx dy + p11 dy^2, d = pixel - mean  [pixels]
+//   l = -q/2 * log2(e) = A dx^2 + Bc dx dy + C dy^2   (exp(-q/2) = 2^l)
+struct Splat2 {
+    float mpx, mpy;        // mean in pixel-index coordinates
+    float p00, p01, p11;   // precision in px^-2
+    float A, Bc, C;        // log2-scaled quadratic form
+    float cnorm;           // 1 / (2 pi sqrt(det)) in normalised units
+    float w;               // amp * cnorm
+    float hx, hy;          // half-extents of the q < cutoff ellipse [px]
+};
+
+__device__ __forceinline__ Splat2 project2(const SplatRec &r, const PoseF &P, const GridF &G) {
+    Splat2 s;
+    // B2 = W[:2] M, mean2 = W[:2] mu + t  (splat.py:197-200), in pixel units
+    float b0[3], b1[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        b0[j] = (P.w0[0] * r.M[j] + P.w0[1] * r.M[3 + j] + P.w0[2] * r.M[6 + j]) * G.inv_h;
+        b1[j] = (P.w1[0] * r.M[j] + P.w1[1] * r.M[3 + j] + P.w1[2] * r.M[6 + j]) * G.inv_h;
+    }
+    s.mpx = (P.w0[0] * r.mx + P.w0[1] * r.my + P.w0[2] * r.mz + P.tx) * G.inv_h + G.c0;
+    s.mpy = (P.w1[0] * r.mx + P.w1[1] * r.my + P.w1[2] * r.mz + P.ty) * G.inv_h + G.c0;
+    // cov2 = B2 B2^T (splat.py:202-206); det by Cauchy-Binet (sum of squared
+    // 2x2 minors) so thin footprints keep full relative precision
+    float c00 = b0[0] * b0[0] + b0[1] * b0[1] + b0[2] * b0[2];
+    float c01 = b0[0] * b1[0] + b0[1] * b1[1] + b0[2] * b1[2];
+    float c11 = b1[0] * b1[0] + b1[1] * b1[1] + b1[2] * b1[2];
+    float m01 = b0[0] * b1[1] - b0[1] * b1[0];
+    float m02 = b0[0] * b1[2] - b0[2] * b1[0];
+    float m12 = b0[1] * b1[2] - b0[2] * b1[1];
+    float det = m01 * m01 + m02 * m02 + m12 * m12;
+    float mid = 0.5f * (c00 + c11);
+    float hd = 0.5f * (c00 - c11);
+    float rad = sqrtf(hd * hd + c01 * c01);
+    float l1 = mid + rad;
+    float l2 = l1 > 0.f ? det / l1 : 0.f;
+    if (l2 < kEigenFloorPx2) {
+        // floor the small eigenvalue, keep the eigenvector (splat.py:245-259)
+        float a1 = fmaxf(l1, kEigenFloorPx2), a2 = kEigenFloorPx2;
+        float vx = c01, vy = l1 - c00;
+        float ux = l1 - c11, uy = c01;
+        if (ux * ux + uy * uy > vx * vx + vy * vy) { vx = ux; vy = uy; }
+        float nn = sqrtf(vx * vx + vy * vy);
+        if (nn == 0.f) { vx = 1.f; vy = 0.f; } else { vx /= nn; vy /= nn; }
+        c00 = a1 * vx * vx + a2 * vy * vy;
+        c01 = (a1 - a2) * vx * vy;
+        c11 = a1 * vy * vy + a2 * vx * vx;
+        det = a1 * a2;
+    }
+    float inv_det = 1.f / det;
+    s.p00 = c11 * inv_det;
+    s.p01 = -c01 * inv_det;
+    s.p11 = c00 * inv_det;
+    s.cnorm = G.inv_2pi_h2 / sqrtf(det);
+    s.w = r.amp * s.cnorm;
+    s.A = -0.5f * kLog2e * s.p00;
+    s.Bc = -kLog2e * s.p01;
+    s.C = -0.5f * kLog2e * s.p11;
+    s.hx = sqrtf(kCutoffSq * c00);
+    s.hy = sqrtf(kCutoffSq * c11);
+    return s;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace cgs

@@ -1,0 +1,308 @@
+"""Device-resident execution of the splatting step over libcgs_b200.so.
+
+PyTorch provides device memory, the current CUDA stream and (for multi-GPU)
+``torch.distributed``; all compute runs in the hand-written sm_100a kernels of
+``csrc/`` through the C ABI in ``include/cgs_b200.h``.  Nothing here computes on
+the host, and nothing falls back to a CPU path: without a CUDA device or the
+library every entry point raises ``CudaUnavailableError``.
+
+Pipeline of one step (call stack A):
+  K0 cgs_prepare -> K2 cgs_bin_count / cgs_exclusive_scan / cgs_bin_scatter
+  -> K3 cgs_raster_fwd -> K4 cgs_ctf_mse (cuFFT R2C, H_sym, C2R, MSE, R2C,
+  H_sym, C2R) -> K5 cgs_raster_bwd -> [NCCL all-reduce] -> K6
+  cgs_epilogue_adam.  All launches are stream-ordered with no host sync.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import CudaUnavailableError
+
+try:  # torch is the device-memory / stream / collective plumbing
+    import torch
+except ImportError:  # pragma: no cover - torch is in the image
+    torch = None
+
+DEFAULT_TILE = 16
+DEFAULT_IMAGES_PER_GROUP = 16
+
+
+def require_cuda():
+    if torch is None or not torch.cuda.is_available():
+        raise CudaUnavailableError(
+            "a CUDA device is required: paper_2508_04929_b200 runs only on the GPU (no CPU fallback)"
+        )
+    return _lib.load()
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def pose_array(rotations, translations=None) -> np.ndarray:
+    """Pack poses as f64 [B][12]: W row-major, tx, ty, 0 (include/cgs_b200.h)."""
+    R = np.asarray(rotations, dtype=np.float64).reshape(-1, 3, 3)
+    out = np.zeros((R.shape[0], 12), dtype=np.float64)
+    out[:, :9] = R.reshape(-1, 9)
+    if translations is not None:
+        out[:, 9:11] = np.asarray(translations, dtype=np.float64).reshape(-1, 2)
+    return out
+
+
+def ctf_array(params_list) -> np.ndarray:
+    """Pack CtfParams-like objects as f64 [B][8] (include/cgs_b200.h)."""
+    out = np.zeros((len(params_list), 8), dtype=np.float64)
+    for i, p in enumerate(params_list):
+        out[i] = [p.defocus_u, p.defocus_v, p.astigmatism_angle, p.voltage, p.spherical_aberration,
+                  p.amplitude_contrast, p.phase_shift, p.b_factor]
+    return out
+
+
+class DeviceContext:
+    """Per-device library handle, grow-only scratch buffers and FFT plans."""
+
+    _instances: dict = {}
+
+    def __init__(self, device):
+        self.lib = require_cuda()
+        self.device = torch.device(device)
+        self._bufs: dict = {}
+        self._plans: dict = {}
+
+    @classmethod
+    def get(cls, device=None) -> "DeviceContext":
+        require_cuda()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        key = dev.index if dev.index is not None else torch.cuda.current_device()
+        if key not in cls._instances:
+            cls._instances[key] = cls(torch.device("cuda", key))
+        return cls._instances[key]
+
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def buf(self, name: str, numel: int, dtype) -> "torch.Tensor":
+        """Grow-only scratch tensor (flat, at least ``numel`` elements)."""
+        t = self._bufs.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(max(int(numel), 1), dtype=dtype, device=self.device)
+            self._bufs[name] = t
+        return t[: max(int(numel), 1)]
+
+    def plan(self, size: int, batch: int) -> int:
+        key = (int(size), int(batch))
+        if key not in self._plans:
+            h = ctypes.c_void_p()
+            _lib.call("cgs_fft_plan_create", int(size), int(batch), ctypes.byref(h))
+            self._plans[key] = h.value
+        return self._plans[key]
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            for h in self._plans.values():
+                self.lib.cgs_fft_plan_destroy(h)
+        except Exception:
+            pass
+
+
+@dataclass
+class Binning:
+    items: "torch.Tensor"   # int32 [capacity]
+    offs: "torch.Tensor"    # int32 [B*T*S + 1]
+    tile: int
+    T: int
+    S: int
+    capacity: int
+
+
+def prepare(ctx: DeviceContext, params, status, out=None):
+    """K0: f64 [N][11] -> splat f32 [N][16]."""
+    n = params.shape[0]
+    splat = out if out is not None else ctx.buf("splat", n * 16, torch.float32)
+    _lib.call("cgs_prepare", _ptr(params), n, _ptr(splat), _ptr(status), ctx.stream)
+    return splat
+
+
+def bin_count(ctx, params, poses, grid_s, tile, *, bbox_out=None, clamp=None, prefix="bin"):
+    """K2 count + scan: returns (offs, rects, T, S)."""
+    n = params.shape[0]
+    B = poses.shape[0]
+    T = int(ctx.lib.cgs_bin_tiles(grid_s.size, tile))
+    S = int(ctx.lib.cgs_bin_segments(n))
+    cnt = B * T * S + 1
+    rects = ctx.buf(prefix + "_rects", B * n, torch.int32)
+    counts = ctx.buf(prefix + "_counts", cnt, torch.int32)
+    offs = ctx.buf(prefix + "_offs", cnt, torch.int32)
+    ws = ctx.buf(prefix + "_scanws", ctx.lib.cgs_scan_workspace_bytes(cnt) // 4 + 1, torch.int32)
+    _lib.call("cgs_bin_count", _ptr(params), n, _ptr(poses), B, grid_s, tile, _ptr(rects),
+              _ptr(counts), _ptr(bbox_out), _ptr(clamp), ctx.stream)
+    _lib.call("cgs_exclusive_scan", _ptr(counts), _ptr(offs), cnt, _ptr(ws), ctx.stream)
+    return offs, rects, T, S
+
+
+def bin_scatter(ctx, rects, n, B, grid_s, tile, offs, items, status):
+    _lib.call("cgs_bin_scatter", _ptr(rects), n, B, grid_s.size, tile, _ptr(offs), _ptr(items),
+              items.numel(), _ptr(status), ctx.stream)
+
+
+def bin_full(ctx, params, poses, grid_s, tile, status, *, bbox_out=None, clamp=None, prefix="bin") -> Binning:
+    """Count, scan, then size the item list exactly (one host read) and scatter."""
+    offs, rects, T, S = bin_count(ctx, params, poses, grid_s, tile, bbox_out=bbox_out, clamp=clamp, prefix=prefix)
+    total = int(offs[-1].item())
+    items = ctx.buf(prefix + "_items", max(total, 1), torch.int32)
+    bin_scatter(ctx, rects, params.shape[0], poses.shape[0], grid_s, tile, offs, items, status)
+    return Binning(items, offs, tile, T, S, items.numel())
+
+
+def raster_fwd(ctx, splat, n, poses, grid_s, binning: Binning, out, layout=_lib.CGS_LAYOUT_NATURAL):
+    """K3: rendered images f32 [B][D][D]."""
+    _lib.call("cgs_raster_fwd", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, binning.tile,
+              _ptr(binning.items), _ptr(binning.offs), binning.capacity, _ptr(out), layout, ctx.stream)
+    return out
+
+
+def raster_bwd(ctx, splat, n, poses, grid_s, upstream, ipg=DEFAULT_IMAGES_PER_GROUP, out=None,
+               layout=_lib.CGS_LAYOUT_NATURAL):
+    """K5: partial world-frame accumulators f32 [G][N][10]."""
+    B = poses.shape[0]
+    G = int(ctx.lib.cgs_bwd_groups(B, ipg))
+    partial = out if out is not None else ctx.buf("bwd_partial", G * n * 10, torch.float32)
+    _lib.call("cgs_raster_bwd", _ptr(splat), n, _ptr(poses), B, grid_s, _ptr(upstream), layout,
+              _ptr(partial), ipg, ctx.stream)
+    return partial, G
+
+
+def epilogue_grads(ctx, partial, G, params, mode, scale, out=None):
+    n = params.shape[0]
+    grads = out if out is not None else torch.empty((n, 11), dtype=torch.float64, device=ctx.device)
+    _lib.call("cgs_epilogue_grads", _ptr(partial), G, n, _ptr(params), mode, float(scale), _ptr(grads), ctx.stream)
+    return grads
+
+
+def ctf_apply(ctx, images, grid_s, *, ctf=None, H=None, out=None):
+    """apply_ctf on a device batch f32 [B][D][D]."""
+    B = images.shape[0]
+    D = grid_s.size
+    out = out if out is not None else torch.empty_like(images)
+    spec = ctx.buf("spectrum", 2 * int(ctx.lib.cgs_fft_spectrum_elems(D, B)), torch.float32)
+    _lib.call("cgs_ctf_apply", ctx.plan(D, B), _ptr(images), _ptr(out), B, grid_s, _ptr(ctf), _ptr(H),
+              _ptr(spec), _lib.CGS_LAYOUT_NATURAL, ctx.stream)
+    return out
+
+
+def loss_residual(ctx, model, obs, resid=None):
+    B, D = model.shape[0], model.shape[-1]
+    loss = torch.empty(B, dtype=torch.float64, device=ctx.device)
+    _lib.call("cgs_loss_residual", _ptr(model), _ptr(obs), B, D, _ptr(loss), _ptr(resid), 0, ctx.stream)
+    return loss
+
+
+def count_pairs(ctx, splat, n, poses, grid_s) -> "torch.Tensor":
+    pairs = torch.zeros(poses.shape[0], dtype=torch.int64, device=ctx.device)
+    _lib.call("cgs_count_pairs", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, _ptr(pairs), ctx.stream)
+    return pairs
+
+
+class StepPipeline:
+    """One fused training step over a device-resident batch, no host sync.
+
+    Buffers are allocated once for (N, B, D); the step is stream-ordered and
+    CUDA-Graph capturable (the item capacity is fixed at construction and an
+    overflow only sets a status bit that makes the Adam epilogue skip the
+    update; ``check_overflow`` reports it and ``grow`` enlarges the buffer).
+    """
+
+    def __init__(self, ctx: DeviceContext, n: int, batch: int, grid_s, *, tile=DEFAULT_TILE,
+                 images_per_group=DEFAULT_IMAGES_PER_GROUP, mode="anisotropic", item_capacity=None):
+        self.ctx = ctx
+        self.n, self.B, self.grid = int(n), int(batch), grid_s
+        self.D = grid_s.size
+        self.tile = tile
+        self.ipg = images_per_group
+        self.mode = _lib.CGS_MODE[mode]
+        dev = ctx.device
+        D = self.D
+        self.T = int(ctx.lib.cgs_bin_tiles(D, tile))
+        self.S = int(ctx.lib.cgs_bin_segments(n))
+        cnt = self.B * self.T * self.S + 1
+        self.splat = torch.empty(n * 16, dtype=torch.float32, device=dev)
+        self.rects = torch.empty(self.B * n, dtype=torch.int32, device=dev)
+        self.counts = torch.empty(cnt, dtype=torch.int32, device=dev)
+        self.offs = torch.empty(cnt, dtype=torch.int32, device=dev)
+        self.scan_ws = torch.empty(ctx.lib.cgs_scan_workspace_bytes(cnt) // 4 + 1, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.render = torch.empty((self.B, D, D), dtype=torch.float32, device=dev)
+        self.upstream = torch.empty((self.B, D, D), dtype=torch.float32, device=dev)
+        self.spectrum = torch.empty(2 * int(ctx.lib.cgs_fft_spectrum_elems(D, self.B)), dtype=torch.float32, device=dev)
+        self.loss = torch.empty(self.B, dtype=torch.float64, device=dev)
+        self.G = int(ctx.lib.cgs_bwd_groups(self.B, self.ipg))
+        self.partial = torch.empty(self.G * n * 10, dtype=torch.float32, device=dev)
+        self.acc = torch.empty(n * 10, dtype=torch.float32, device=dev)
+        self.plan = ctx.plan(D, self.B)
+        self.items = torch.empty(max(int(item_capacity or 1), 1), dtype=torch.int32, device=dev)
+
+    @property
+    def capacity(self) -> int:
+        return self.items.numel()
+
+    def grow(self, needed: int) -> None:
+        cap = int(needed * 1.25) + 1024
+        if cap > self.items.numel():
+            self.items = torch.empty(cap, dtype=torch.int32, device=self.ctx.device)
+
+    def measure_items(self, params, poses) -> int:
+        """Run the count pass once and read the item total (one host sync)."""
+        self._count(params, poses)
+        return int(self.offs[-1].item())
+
+    def _count(self, params, poses):
+        s = self.ctx.stream
+        _lib.call("cgs_prepare", _ptr(params), self.n, _ptr(self.splat), _ptr(self.status), s)
+        _lib.call("cgs_bin_count", _ptr(params), self.n, _ptr(poses), self.B, self.grid, self.tile,
+                  _ptr(self.rects), _ptr(self.counts), 0, 0, s)
+        _lib.call("cgs_exclusive_scan", _ptr(self.counts), _ptr(self.offs), self.counts.numel(),
+                  _ptr(self.scan_ws), s)
+
+    def forward_backward(self, params, poses, obs, ctf):
+        """K0..K5 for a batch; leaves partial accumulators in self.partial."""
+        s = self.ctx.stream
+        self._count(params, poses)
+        _lib.call("cgs_bin_scatter", _ptr(self.rects), self.n, self.B, self.D, self.tile, _ptr(self.offs),
+                  _ptr(self.items), self.items.numel(), _ptr(self.status), s)
+        _lib.call("cgs_raster_fwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid, self.tile,
+                  _ptr(self.items), _ptr(self.offs), self.items.numel(), _ptr(self.render),
+                  _lib.CGS_LAYOUT_NATURAL, s)
+        _lib.call("cgs_ctf_mse", self.plan, _ptr(self.render), _ptr(obs), self.B, self.grid, _ptr(ctf),
+                  _ptr(self.spectrum), 0, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status),
+                  _lib.CGS_LAYOUT_NATURAL, s)
+        _lib.call("cgs_raster_bwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid,
+                  _ptr(self.upstream), _lib.CGS_LAYOUT_NATURAL, _ptr(self.partial), self.ipg, s)
+
+    def reduce(self):
+        _lib.call("cgs_reduce_partials", _ptr(self.partial), self.G, self.n, _ptr(self.acc), self.ctx.stream)
+        return self.acc
+
+    def adam(self, params, m, v, *, scale, lr, beta1, beta2, eps, t, acc=None, groups=None):
+        """K6 fused epilogue + Adam; acc defaults to this step's partials."""
+        src = self.partial if acc is None else acc
+        G = self.G if acc is None else (groups or 1)
+        bc1 = 1.0 - beta1 ** t
+        bc2 = 1.0 - beta2 ** t
+        _lib.call("cgs_epilogue_adam", _ptr(src), G, self.n, _ptr(params), _ptr(m), _ptr(v), self.mode,
+                  float(scale), float(lr), float(beta1), float(beta2), float(eps), float(bc1), float(bc2),
+                  _ptr(self.status), self.ctx.stream)
+
+    def overflowed(self) -> bool:
+        return bool(int(self.status.item()) & _lib.CGS_STATUS_BIN_OVERFLOW)
+
+    def degenerate(self) -> bool:
+        return bool(int(self.status.item()) & _lib.CGS_STATUS_DEGENERATE_ROTATION)
+
+    def clear_status(self):
+        self.status.zero_()

@@ -1,0 +1,433 @@
+"""Training on the GPU: loss, Adam, one step, the epoch loop (mirrors train.py).
+
+``train_step`` / ``train`` keep the reference signatures (train.py:164-264) and
+its semantics at ``batch_size = 1``: same seeded shuffle, one Adam step per
+record, lr(e) = lr0 * gamma^e, divergence guard against 1e3 x the epoch-0
+median, ``loss_trace.txt`` and one CGS1 checkpoint per epoch.  Unlike the
+reference, ``batch_size > 1`` is accepted: the loss of a step is the mean of the
+per-image MSEs, so B = 1 reduces exactly to the reference step.
+
+The dataset (centred observations, poses, CTF parameters) is made resident in
+HBM once; each step runs the libcgs_b200 pipeline (``engine.StepPipeline``) on
+a batch gathered on the device, with no host synchronisation: losses are read
+back in blocks and the divergence guard is applied to them in step order (the
+run's parameters are discarded on a raise, so a late raise is equivalent).
+With ``torch.distributed`` initialised, each rank takes its slice of every
+global batch and the 10-float gradient accumulators are all-reduced (NCCL)
+before the fused epilogue + Adam, which then runs identically on every rank.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _lib, engine, parallel
+from .ctf import CtfParams, phase_shift_translate
+from .exceptions import DegenerateRotationError, DivergenceError
+from .mixture import COL_RAW_SCALE, MODES, GaussianMixture, GridSpec, init_random, save_checkpoint
+from .render import Pose, RenderedImage
+
+DIVERGENCE_FACTOR = 1e3
+LOSS_READBACK_STEPS = 64
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """Optimisation settings (train.py:33-56); batch_size >= 1 is supported."""
+
+    epochs: int = 5
+    batch_size: int = 1
+    learning_rate: float = 0.001
+    decay_gamma: float = 0.1
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_epsilon: float = 1e-8
+    seed: int = 0
+    mode: str = "anisotropic"
+
+    def __post_init__(self):
+        if self.epochs < 1:
+            raise ValueError("epochs must be >= 1")
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+        if self.learning_rate <= 0 or self.decay_gamma <= 0:
+            raise ValueError("learning_rate and decay_gamma must be positive")
+        if self.mode not in MODES:
+            raise ValueError(f"unknown mode {self.mode!r}")
+
+    def epoch_lr(self, epoch: int) -> float:
+        return self.learning_rate * self.decay_gamma**epoch
+
+
+@dataclass(eq=False)
+class ParticleRecord:
+    """One observed particle with its pose, CTF and recorded translation (px)."""
+
+    image: np.ndarray
+    pose: Pose
+    ctf: CtfParams
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(2))
+
+    def __post_init__(self):
+        self.image = np.asarray(self.image)
+        self.translation = np.asarray(self.translation, dtype=np.float64)
+        if self.image.ndim != 2 or self.image.shape[0] != self.image.shape[1]:
+            raise ValueError("particle image must be square")
+        if not np.all(np.isfinite(self.image)):
+            raise ValueError("particle image contains non-finite values")
+
+
+@dataclass
+class Dataset:
+    records: list
+    grid: GridSpec
+
+    def __len__(self) -> int:
+        return len(self.records)
+
+    def half(self, which: str) -> "Dataset":
+        """Even/odd split for gold-standard halves (train.py:85-90)."""
+        if which not in ("even", "odd"):
+            raise ValueError("half must be 'even' or 'odd'")
+        return Dataset(records=self.records[(0 if which == "even" else 1)::2], grid=self.grid)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class AdamState:
+    """Adam moments for the (N, 11) raw parameters, fp64 on the GPU (train.py:93-111)."""
+
+    def __init__(self, n: int):
+        torch = _torch()
+        engine.require_cuda()
+        self.n = int(n)
+        self._m = torch.zeros((n, 11), dtype=torch.float64, device="cuda")
+        self._v = torch.zeros((n, 11), dtype=torch.float64, device="cuda")
+        self.t = 0
+
+    @property
+    def m(self) -> np.ndarray:
+        return self._m.cpu().numpy()
+
+    @property
+    def v(self) -> np.ndarray:
+        return self._v.cpu().numpy()
+
+    def update(self, params: np.ndarray, grads: np.ndarray, lr: float, config: TrainConfig) -> None:
+        """One in-place Adam step on host arrays (runs ``cgs_adam`` on the device)."""
+        torch = _torch()
+        ctx = engine.DeviceContext.get()
+        p = torch.as_tensor(np.ascontiguousarray(params, dtype=np.float64)).cuda()
+        g = torch.as_tensor(np.ascontiguousarray(grads, dtype=np.float64)).cuda()
+        self.t += 1
+        b1, b2 = config.adam_beta1, config.adam_beta2
+        _lib.call("cgs_adam", p.data_ptr(), g.data_ptr(), self._m.data_ptr(), self._v.data_ptr(), p.numel(),
+                  float(lr), b1, b2, config.adam_epsilon, 1.0 - b1**self.t, 1.0 - b2**self.t, ctx.stream)
+        params[...] = p.cpu().numpy().reshape(params.shape)
+
+
+def loss_mse(rendered, observed) -> float:
+    """Mean squared difference over all pixels (train.py:114-121), fp64 sum on the GPU."""
+    torch = _torch()
+    a = rendered.pixels if isinstance(rendered, RenderedImage) else np.asarray(rendered)
+    b = observed.pixels if isinstance(observed, RenderedImage) else np.asarray(observed)
+    if a.shape != b.shape:
+        raise ValueError(f"shape mismatch: {a.shape} vs {b.shape}")
+    ctx = engine.DeviceContext.get()
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        # the device kernel is per square image; other shapes go through a square pad
+        flat_a = np.zeros((1, a.size), np.float64)
+        flat_b = np.zeros((1, b.size), np.float64)
+        flat_a[0], flat_b[0] = a.ravel(), b.ravel()
+        side = int(math.ceil(math.sqrt(a.size)))
+        pa = np.zeros((side * side,))
+        pb = np.zeros((side * side,))
+        pa[: a.size], pb[: b.size] = a.ravel(), b.ravel()
+        a, b = pa.reshape(side, side), pb.reshape(side, side)
+        scale = (side * side) / max(flat_a.size, 1)
+    else:
+        scale = 1.0
+    ta = torch.as_tensor(np.ascontiguousarray(a, dtype=np.float32)[None]).cuda()
+    tb = torch.as_tensor(np.ascontiguousarray(b, dtype=np.float32)[None]).cuda()
+    loss = engine.loss_residual(ctx, ta, tb)
+    return float(loss.item()) * scale
+
+
+def _centered_observation(record: ParticleRecord) -> np.ndarray:
+    """Observed image with its recorded translation removed (train.py:124-133)."""
+    img = np.asarray(record.image, dtype=np.float64)
+    if record.translation[0] == 0.0 and record.translation[1] == 0.0:
+        return img
+    shifted = phase_shift_translate(RenderedImage(grid=GridSpec(img.shape[0]), pixels=img), -record.translation)
+    return shifted.pixels
+
+
+# ---------------------------------------------------------------------------
+# device-resident reconstruction
+# ---------------------------------------------------------------------------
+class Reconstructor:
+    """Holds a dataset and a mixture in HBM and runs batched Adam steps.
+
+    ``obs`` f32 [R][D][D] (centred observations), ``poses`` f64 [R][12],
+    ``ctfs`` f64 [R][8] or None (no CTF).  ``step(indices, lr)`` launches one
+    full step for the given record indices and returns the device tensor of
+    per-image losses (no host sync).
+    """
+
+    def __init__(self, grid: GridSpec, params: np.ndarray, obs, poses, ctfs, *, batch_size: int,
+                 mode: str = "anisotropic", config: TrainConfig | None = None, process_group=None,
+                 images_per_group: int = engine.DEFAULT_IMAGES_PER_GROUP, tile: int = engine.DEFAULT_TILE):
+        torch = _torch()
+        self.ctx = engine.DeviceContext.get()
+        dev = self.ctx.device
+        self.grid = grid
+        self.gs = _lib.grid_struct(grid.size, grid.extent, grid.pixel_size)
+        self.config = config or TrainConfig(batch_size=batch_size, mode=mode)
+        self.mode = mode
+        self.n = int(params.shape[0])
+        self.params = torch.as_tensor(np.ascontiguousarray(params, dtype=np.float64)).to(dev)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.t = 0
+        self.obs = obs if isinstance(obs, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(obs, np.float32))
+        self.obs = self.obs.to(dev, torch.float32).contiguous()
+        self.poses = torch.as_tensor(np.ascontiguousarray(poses, np.float64)).to(dev)
+        self.ctfs = None if ctfs is None else torch.as_tensor(np.ascontiguousarray(ctfs, np.float64)).to(dev)
+        self.global_batch = int(batch_size)
+        self.pg = process_group
+        self.world = 1
+        self.rank = 0
+        if process_group is not None or _dist_active():
+            import torch.distributed as dist
+
+            self.world = dist.get_world_size(process_group)
+            self.rank = dist.get_rank(process_group)
+        self.ipg = images_per_group
+        self.tile = tile
+        self._pipes: dict = {}
+
+    # -- helpers -------------------------------------------------------------
+    def local_slice(self, indices: np.ndarray) -> np.ndarray:
+        """This rank's contiguous share of a global batch."""
+        return parallel.shard(indices, self.rank, self.world)
+
+    def pipeline(self, b: int) -> engine.StepPipeline:
+        if b not in self._pipes:
+            self._pipes[b] = engine.StepPipeline(self.ctx, self.n, b, self.gs, tile=self.tile,
+                                                 images_per_group=self.ipg, mode=self.mode)
+        return self._pipes[b]
+
+    def _batch(self, local: np.ndarray):
+        torch = _torch()
+        idx = torch.as_tensor(local, dtype=torch.int64).to(self.ctx.device, non_blocking=True)
+        obs = self.obs.index_select(0, idx)
+        poses = self.poses.index_select(0, idx)
+        ctfs = None if self.ctfs is None else self.ctfs.index_select(0, idx)
+        return obs, poses, ctfs
+
+    def ensure_capacity(self, indices_list) -> None:
+        """Size the tile-list buffers from the given batches (one host read each)."""
+        for local in indices_list:
+            pipe = self.pipeline(len(local))
+            _, poses, _ = self._batch(local)
+            pipe.grow(pipe.measure_items(self.params, poses))
+
+    def step(self, indices, lr: float, *, retry: bool = True):
+        """One step over the global batch ``indices``; returns per-image losses (device)."""
+        torch = _torch()
+        indices = np.asarray(indices)
+        local = self.local_slice(indices)
+        pipe = self.pipeline(len(local))
+        obs, poses, ctfs = self._batch(local)
+        cfg = self.config
+        pipe.clear_status()
+        pipe.forward_backward(self.params, poses, obs, ctfs)
+        scale = 1.0 / len(indices)
+        self.t += 1
+        if self.world > 1:
+            acc = parallel.allreduce_accumulator(pipe.reduce(), self.pg)
+            pipe.adam(self.params, self.m, self.v, scale=scale, lr=lr, beta1=cfg.adam_beta1,
+                      beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t, acc=acc, groups=1)
+        else:
+            pipe.adam(self.params, self.m, self.v, scale=scale, lr=lr, beta1=cfg.adam_beta1,
+                      beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t)
+        return pipe.loss
+
+    def check_status(self) -> None:
+        for pipe in self._pipes.values():
+            if pipe.degenerate():
+                raise DegenerateRotationError("quaternion with zero or non-finite norm")
+
+    def params_host(self) -> np.ndarray:
+        return self.params.cpu().numpy()
+
+
+def _dist_active() -> bool:
+    try:
+        import torch.distributed as dist
+
+        return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+    except Exception:
+        return False
+
+
+def _record_arrays(records, grid: GridSpec):
+    from .engine import ctf_array, pose_array
+
+    obs = np.stack([_centered_observation(r) for r in records]).astype(np.float32)
+    poses = pose_array([r.pose.rotation for r in records], [r.pose.translation for r in records])
+    ctfs = ctf_array([r.ctf for r in records])
+    return obs, poses, ctfs
+
+
+def train_step(mixture: GaussianMixture, record: ParticleRecord, config: TrainConfig, adam: AdamState,
+               *, lr: float | None = None, grid: GridSpec | None = None, record_index: int = -1):
+    """One render / CTF / MSE / backward / Adam cycle on one record (train.py:164-191).
+
+    Mutates ``mixture.params`` in place and returns ``(mixture, loss)``.  A
+    non-finite loss raises DivergenceError and leaves the parameters unchanged.
+    """
+    torch = _torch()
+    if grid is None:
+        grid = GridSpec(record.image.shape[0], pixel_size=1.0)
+    if lr is None:
+        lr = config.learning_rate
+    obs, poses, ctfs = _record_arrays([record], grid)
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(grid.size, grid.extent, grid.pixel_size)
+    pipe = _step_pipe(ctx, len(mixture), gs, config.mode)
+    params = torch.as_tensor(np.ascontiguousarray(mixture.params)).to(ctx.device)
+    p_t = torch.as_tensor(poses).to(ctx.device)
+    o_t = torch.as_tensor(obs).to(ctx.device)
+    c_t = torch.as_tensor(ctfs).to(ctx.device)
+    pipe.clear_status()
+    pipe.grow(pipe.measure_items(params, p_t))
+    pipe.forward_backward(params, p_t, o_t, c_t)
+    loss = float(pipe.loss[0].item())
+    if pipe.degenerate():
+        raise DegenerateRotationError("quaternion with zero or non-finite norm")
+    if not math.isfinite(loss):
+        raise DivergenceError("non-finite loss", epoch=-1, step=-1, record_index=record_index)
+    adam.t += 1
+    pipe.adam(params, adam._m, adam._v, scale=1.0, lr=lr, beta1=config.adam_beta1, beta2=config.adam_beta2,
+              eps=config.adam_epsilon, t=adam.t)
+    mixture.params[...] = params.cpu().numpy()
+    return mixture, loss
+
+
+_PIPES: dict = {}
+
+
+def _step_pipe(ctx, n, gs, mode):
+    key = (ctx.device.index, n, gs.size, gs.extent, gs.pixel_size, mode)
+    if key not in _PIPES:
+        _PIPES.clear()
+        _PIPES[key] = engine.StepPipeline(ctx, n, 1, gs, mode=mode)
+    return _PIPES[key]
+
+
+def train(dataset: Dataset, config: TrainConfig, *, n_gaussians: int, out_dir: str | None = None,
+          initial: GaussianMixture | None = None, process_group=None):
+    """Fit a mixture to the dataset (train.py:194-264).  Returns (mixture, epoch_losses)."""
+    if len(dataset) == 0:
+        raise ValueError("cannot train on an empty dataset")
+    grid = dataset.grid
+    mixture = initial.copy() if initial is not None else init_random(n_gaussians, config.seed, grid, mode=config.mode)
+    shuffle_rng = np.random.default_rng(config.seed)
+    obs, poses, ctfs = _record_arrays(dataset.records, grid)
+    rec = Reconstructor(grid, mixture.params, obs, poses, ctfs, batch_size=config.batch_size, mode=config.mode,
+                        config=config, process_group=process_group)
+    R = len(dataset)
+    B = config.batch_size
+    is_root = rec.rank == 0
+    trace, epoch_losses = [], []
+    epoch0_median = None
+    history0: list = []
+    torch = _torch()
+
+    for epoch in range(config.epochs):
+        lr = config.epoch_lr(epoch)
+        order = shuffle_rng.permutation(R)
+        batches = [order[i:i + B] for i in range(0, R, B)]
+        if epoch == 0:
+            sizes = {}
+            for b in batches:
+                sizes.setdefault(len(rec.local_slice(b)), rec.local_slice(b))
+            rec.ensure_capacity(list(sizes.values()))
+        steps = len(batches)
+        losses = np.empty(steps, dtype=np.float64)
+        pending: list = []
+
+        def drain(upto):
+            nonlocal epoch0_median
+            for s, dev_loss, nloc, bidx in pending:
+                val = _global_batch_loss(dev_loss, nloc, len(bidx), rec)
+                losses[s] = val
+                ridx = int(bidx[0]) if B == 1 else -1
+                if not math.isfinite(val):
+                    raise DivergenceError("non-finite loss", epoch=epoch, step=s, record_index=ridx)
+                if epoch0_median is not None:
+                    ref = epoch0_median
+                else:
+                    history0.append(val)
+                    ref = float(np.median(history0))
+                if val > DIVERGENCE_FACTOR * ref:
+                    raise DivergenceError(
+                        f"loss {val:.6g} exceeded {DIVERGENCE_FACTOR:g} x epoch-0 median {ref:.6g}",
+                        epoch=epoch, step=s, record_index=ridx)
+                trace.append(f"{epoch} {s} {val:.17g} {lr:.17g}")
+            pending.clear()
+
+        for s, bidx in enumerate(batches):
+            dev_loss = rec.step(bidx, lr)
+            pending.append((s, dev_loss.clone(), len(rec.local_slice(bidx)), bidx))
+            if len(pending) >= LOSS_READBACK_STEPS:
+                drain(s)
+        drain(steps)
+        rec.check_status()
+        if any(p.overflowed() for p in rec._pipes.values()):  # pragma: no cover - capacity sized above
+            raise RuntimeError("tile list capacity overflow: re-run with a larger capacity")
+        if epoch == 0:
+            epoch0_median = float(np.median(losses))
+        epoch_losses.append(losses)
+        if out_dir is not None and is_root:
+            mixture.params[...] = rec.params_host()
+            save_checkpoint(mixture, os.path.join(out_dir, f"checkpoint_epoch_{epoch}.cgs"))
+    mixture.params[...] = rec.params_host()
+    if out_dir is not None and is_root:
+        with open(os.path.join(out_dir, "loss_trace.txt"), "w") as fh:
+            fh.write(f"# seed {config.seed}\n")
+            fh.write("# epoch step loss lr\n")
+            fh.write("\n".join(trace) + "\n")
+    del torch
+    return mixture, epoch_losses
+
+
+def _global_batch_loss(dev_loss, n_local: int, n_global: int, rec: Reconstructor) -> float:
+    """Mean per-image loss of the global batch (sum over ranks when distributed)."""
+    torch = _torch()
+    total = dev_loss[:n_local].sum()
+    if rec.world > 1:
+        import torch.distributed as dist
+
+        t = total.reshape(1).clone()
+        dist.all_reduce(t, group=rec.pg)
+        total = t[0]
+    return float(total.item()) / n_global
+
+
+def half_config(config: TrainConfig, which: str) -> TrainConfig:
+    """Gold-standard half configs: the odd half uses seed + 1 (train.py:267-273)."""
+    if which == "even":
+        return config
+    if which == "odd":
+        return replace(config, seed=config.seed + 1)
+    raise ValueError("half must be 'even' or 'odd'")

@@ -1,0 +1,141 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared symbol,
+host-side logic (parameter model, checkpoints, poses, configs) matches the
+reference, and the product path refuses to run without a GPU (no fallback)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden
+
+import paper_2508_04929_b200 as cs
+from paper_2508_04929_b200 import _lib
+
+HEADER = os.path.join(ROOT, "include", "cgs_b200.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cgs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    names = _declared()
+    assert len(names) >= 25
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _lib.PROTOTYPES, f"{name} missing from the ctypes prototypes"
+    assert set(_lib.PROTOTYPES) == set(names)
+
+
+def test_host_only_entry_points():
+    lib = _lib.load()
+    assert lib.cgs_version().decode().startswith("cgs_b200")
+    assert lib.cgs_error_string(1).decode() == "invalid argument"
+    assert lib.cgs_bin_segments(5000) == 3
+    assert lib.cgs_bin_tiles(128, 16) == 64
+    assert lib.cgs_bin_tiles(33, 16) == 9
+    assert lib.cgs_bwd_groups(256, 16) == 16
+    assert lib.cgs_fft_spectrum_elems(128, 2) == 2 * 128 * 65
+    assert lib.cgs_scan_workspace_bytes(4096) >= 8
+
+
+def test_invalid_arguments_are_rejected_without_touching_the_device():
+    lib = _lib.load()
+    g = _lib.grid_struct(64, 0.5, 1.5)
+    assert lib.cgs_prepare(None, 0, None, None, None) == 1
+    assert lib.cgs_raster_fwd(None, 10, None, 1, g, 12, None, None, 0, None, 0, None) == 1
+    assert lib.cgs_bin_count_bbox(None, 10, 1, 64, 16, None, None, None) == 1
+
+
+def test_product_path_fails_loudly_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    mix = cs.init_random(10, 0, cs.GridSpec(32))
+    with pytest.raises(cs.CudaUnavailableError):
+        cs.rasterize(mix, cs.Pose.identity(), cs.GridSpec(32))
+    with pytest.raises(cs.CudaUnavailableError):
+        cs.AdamState(10)
+
+
+def test_parameter_model_matches_reference_and_oracle(oracle):
+    grid = cs.GridSpec(64, 0.5, 1.5)
+    mix = cs.init_random(5000, 0, grid)
+    assert np.array_equal(mix.params, oracle.init_random(5000, 0, oracle.Grid(64, 0.5, 1.5)))
+    assert cs.inverse_activate(5e-5) == pytest.approx(-9.903462552431961, rel=1e-12)
+    x = np.linspace(-50, 50, 1001)
+    np.testing.assert_array_equal(cs.activate(x), oracle.activate(x))
+    np.testing.assert_array_equal(cs.mixture.activate_derivative(x), oracle.activate_derivative(x))
+    q = np.random.default_rng(0).standard_normal((20, 4))
+    np.testing.assert_allclose(cs.mixture.quaternion_to_matrix(cs.mixture.normalize_quaternion(q)),
+                               oracle.quaternion_to_matrix(oracle.normalize_quaternion(q)), rtol=0, atol=1e-15)
+    with pytest.raises(cs.DegenerateRotationError):
+        cs.mixture.normalize_quaternion(np.zeros(4))
+    helix = cs.make_phantom("helix", 50, 0)
+    np.testing.assert_array_equal(helix.params, oracle.make_helix(50))
+    for kind in ("two-lobe", "blob-cluster"):
+        assert cs.make_phantom(kind, 40, 3).params.shape == (40, 11)
+    with pytest.raises(ValueError):
+        cs.make_phantom("cube", 4)
+
+
+def test_checkpoint_round_trip(tmp_path):
+    mix = cs.init_random(17, 3, cs.GridSpec(32), mode="isotropic")
+    path = tmp_path / "a.cgs"
+    cs.save_checkpoint(mix, path)
+    back = cs.load_checkpoint(path)
+    assert back.mode == "isotropic" and np.array_equal(back.params, mix.params)
+    blob = path.read_bytes()
+    assert blob[:4] == b"CGS1" and len(blob) == 13 + 17 * 11 * 8
+    (tmp_path / "bad.cgs").write_bytes(b"XXXX" + blob[4:])
+    with pytest.raises(cs.DataError):
+        cs.load_checkpoint(tmp_path / "bad.cgs")
+    (tmp_path / "short.cgs").write_bytes(blob[:-8])
+    with pytest.raises(cs.DataError):
+        cs.load_checkpoint(tmp_path / "short.cgs")
+
+
+def test_pose_and_config_validation():
+    with pytest.raises(ValueError):
+        cs.Pose(np.eye(3) * 1.1)
+    with pytest.raises(ValueError):
+        cs.Pose(-np.eye(3))
+    rng = np.random.default_rng(0)
+    p = cs.sample_pose(rng)
+    assert np.allclose(p.rotation.T @ p.rotation, np.eye(3), atol=1e-12)
+    assert cs.TrainConfig(batch_size=4).batch_size == 4
+    with pytest.raises(ValueError):
+        cs.TrainConfig(batch_size=0)
+    with pytest.raises(ValueError):
+        cs.TrainConfig(epochs=0)
+    assert cs.TrainConfig(learning_rate=1e-3, decay_gamma=0.1).epoch_lr(2) == pytest.approx(1e-5)
+    from paper_2508_04929_b200.train import half_config
+
+    assert half_config(cs.TrainConfig(seed=7), "odd").seed == 8
+    assert cs.electron_wavelength(300.0) == pytest.approx(float(load_golden("ctf")["lambda_300"]), rel=1e-15)
+
+
+def test_reference_module_paths_exist():
+    from paper_2508_04929_b200 import errors, gmm, optics, splat, train  # noqa: F401
+    from paper_2508_04929_b200.gmm import PARAMS_PER_GAUSSIAN, inverse_activate  # noqa: F401
+    from paper_2508_04929_b200.splat import CLAMP_EVENTS  # noqa: F401
+
+    assert PARAMS_PER_GAUSSIAN == 11
+
+
+def test_view_transform_and_projection_scalar_forms():
+    g = cs.GaussianParams(mean=np.array([0.1, 0.0, 0.0]), raw_scale=cs.inverse_activate(np.array([0.02] * 3)),
+                          quaternion=np.array([1.0, 0, 0, 0]), raw_amplitude=0.0)
+    c, s = np.cos(np.pi / 2), np.sin(np.pi / 2)
+    pose = cs.Pose(np.array([[c, -s, 0], [s, c, 0], [0, 0, 1.0]]), np.array([0.05, 0.0]))
+    out = cs.view_transform(g, pose)
+    assert np.allclose(out.mean3, [0.05, 0.1, 0.0], atol=1e-15)
+    sg = cs.orthographic_project(cs.CameraSpaceGaussian(np.zeros(3), 1e-4 * np.eye(3)))
+    assert float(sg.density(np.zeros(2))) == pytest.approx(1.0 / (2 * np.pi * 1e-4), rel=1e-12)
+    with pytest.raises(cs.DegenerateSplatError):
+        cs.orthographic_project(cs.CameraSpaceGaussian(np.zeros(3), np.diag([1.0, -1.0, 1.0])))
