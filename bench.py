@@ -1,0 +1,367 @@
+"""Benchmark: particle images/s for the fwd+bwd(+Adam) splatting step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the metric's configuration): 50k Gaussians
+(init_random(50000, 0)), 128x128 particles, batch 256 per GPU, known poses +
+per-particle CTF, one full training step per "step": project, bin, render,
+CTF, MSE, CTF^T, backward, all-reduce (N>1), epilogue + Adam.  Synthetic
+particles (helix-50 phantom, 300 kV, defocus U(1e4, 2.5e4) A, SNR 0.1) are
+generated on the device; a dataset of 2048 particles per rank (134 MB, larger
+than the 126 MB L2) is cycled, so consecutive steps read different inputs.
+
+One JSON line on rank 0: value = images/s over all ranks (device time, CUDA
+events, max over ranks); e2e = the same through the public host-buffer API
+(pinned H2D of each step's batch + D2H of its losses inside the timed region);
+roofline for the dominant kernel (raster_bwd) against the FP32/SFU issue
+roofline of SURVEY.md 8(d); cpu_baseline = the CPU oracle (fp64 NumPy + C
+restatement of the reference, "port") on the host cores.  --impl reference
+times that CPU path alone (the reference arm).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("MKL_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle images/sec (fwd+bwd step, 128² px, 50k Gaussians)"
+N_GAUSS, D, BATCH, DATASET = 50000, 128, 256, 2048
+PIXEL_A = 1.5
+WORKLOAD = "C2: 50k init_random Gaussians, 128x128 particles, batch 256/GPU, known poses + CTF, fwd+bwd+Adam"
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (test infrastructure used as the baseline, never product)
+# ---------------------------------------------------------------------------
+_W = {}
+
+
+def _cpu_worker_init():
+    from oracle import cgs_oracle as oracle
+
+    oracle.build_loops()
+    grid = oracle.Grid(D, 0.5, PIXEL_A)
+    _W["oracle"] = oracle
+    _W["grid"] = grid
+    _W["params"] = oracle.init_random(N_GAUSS, 0, grid)
+    _W["helix"] = oracle.make_helix(50)
+
+
+def _cpu_one_image(i: int) -> float:
+    """The reference bench frame + loss for image i (bench.py:50-58, train.py:136-156), fp64."""
+    oracle = _W["oracle"]
+    grid = _W["grid"]
+    W, t = oracle.sample_pose(np.random.default_rng(1000 + i))
+    d = float(np.random.default_rng(3000 + i).uniform(1e4, 2.5e4))
+    t0 = time.perf_counter()
+    H = oracle.ctf_evaluate(oracle.Ctf(d, d), grid)
+    obs = np.zeros((D, D))
+    oracle.image_step(_W["params"], W, t, grid, H, obs)
+    return time.perf_counter() - t0
+
+
+def _cpu_sample(i0: int, seconds: float):
+    """Worker: images i0, i0+1, ... until `seconds` of measured work (first one is warm-up)."""
+    _cpu_one_image(i0)
+    done, spent, i = 0, 0.0, i0 + 1
+    while spent < seconds:
+        spent += _cpu_one_image(i)
+        done += 1
+        i += 1
+    return done, spent
+
+
+def cpu_baseline(seconds: float = 12.0):
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_cpu_worker_init) as pool:
+        res = pool.starmap(_cpu_sample, [(100000 + 1000 * k, seconds) for k in range(cores)])
+    images = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    per_img_ms = 1e3 * statistics.median(r[1] / max(r[0], 1) for r in res)
+    return {
+        "value": images / wall,
+        "unit": "images/s",
+        "cores": cores,
+        "kind": "port",
+        "sample": (f"{images} C2 images (50k Gaussians, 128^2, CTF, fp64 project+bin+forward+CTF+MSE+CTF^T+"
+                   f"backward+chain) over {cores} fork workers x ~{seconds:.0f}s; median {per_img_ms:.0f} ms/image/core"),
+        "cpu_model": _cpu_model(),
+    }
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank: int, world: int):
+    """The reference arm: the CPU path on all host cores, K timed steps of P images."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_cpu_worker_init) as pool:
+        idx = iter(range(10**7))
+        for _ in range(args.warmup):
+            pool.map(_cpu_one_image, [next(idx) for _ in range(cores)])
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_cpu_one_image, [next(idx) for _ in range(cores)])
+        dt = time.perf_counter() - t0
+    value = cores * args.steps / dt
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD + " (CPU oracle port, one image per core per step)",
+                   "n_gaussians": N_GAUSS, "image_px": D, "images_per_step": cores},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} steps x {cores} images (one per core), fp64 oracle",
+                         "cpu_model": _cpu_model()},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for row in out.strip().splitlines():
+            parts = [p.strip() for p in row.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dataset(rank: int):
+    import paper_2508_04929_b200 as cs
+    from paper_2508_04929_b200.synth import synthetic_stack
+
+    grid = cs.GridSpec(D, 0.5, PIXEL_A)
+    base = rank * DATASET
+    poses = [cs.sample_pose(np.random.default_rng(1000 + base + i)) for i in range(DATASET)]
+    defocus = [float(np.random.default_rng(3000 + base + i).uniform(1e4, 2.5e4)) for i in range(DATASET)]
+    rot = np.stack([p.rotation for p in poses])
+    truth = cs.make_phantom("helix", 50, 0)
+    obs, ctfs, sigma = synthetic_stack(truth, rot, grid, defocus=defocus, snr=0.1, noise_seed=11 + rank)
+    from paper_2508_04929_b200.engine import pose_array
+
+    return grid, obs, pose_array(rot), ctfs
+
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+
+    import paper_2508_04929_b200 as cs
+    from paper_2508_04929_b200 import engine
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_seconds)
+
+    grid, obs, poses, ctfs = _dataset(rank)
+    mix = cs.init_random(N_GAUSS, 0, grid)
+    global_batch = BATCH * world
+    rec = Reconstructor(grid, mix.params, obs, poses, ctfs, batch_size=global_batch)
+    dev = rec.ctx.device
+    nb = DATASET // BATCH
+    batches = [np.arange(k * BATCH, (k + 1) * BATCH) for k in range(nb)]
+    dev_batches = []
+    for b in batches:
+        idx = torch.as_tensor(b, device=dev)
+        dev_batches.append((rec.obs.index_select(0, idx).contiguous(), rec.poses.index_select(0, idx).contiguous(),
+                            rec.ctfs.index_select(0, idx).contiguous()))
+    # size the tile lists once (one host read per batch shape) with 25% headroom
+    pipe = rec.pipeline(BATCH)
+    need = max(pipe.measure_items(rec.params, p) for _, p, _ in dev_batches)
+    pipe.grow(need)
+    # algorithmic work: in-ellipse (image, Gaussian, pixel) pairs of every batch
+    splat = engine.prepare(rec.ctx, rec.params, pipe.status)
+    pairs = [int(engine.count_pairs(rec.ctx, splat, N_GAUSS, p, rec.gs).sum().item()) for _, p, _ in dev_batches]
+    lr = 1e-3
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timing (value) ----
+    for k in range(args.warmup):
+        o, p, c = dev_batches[k % nb]
+        rec.step_batch(o, p, c, lr, global_batch=global_batch)
+    barrier()
+    sampler = ClockSampler(local_rank)
+    stage = {n: [] for n in ("bin", "fwd", "ctf", "bwd")}
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_pairs = 0
+    start.record()
+    for k in range(args.steps):
+        o, p, c = dev_batches[k % nb]
+        ev = {n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for n in stage}
+        rec.step_batch(o, p, c, lr, global_batch=global_batch, events=ev)
+        for n in stage:
+            stage[n].append(ev[n])
+        step_pairs += pairs[k % nb]
+    end.record()
+    barrier()
+    clocks = sampler.stop()
+    ms = start.elapsed_time(end)
+    stage_ms = {n: sum(a.elapsed_time(b) for a, b in v) / args.steps for n, v in stage.items()}
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = global_batch * args.steps / (ms_max / 1e3)
+    overflow = pipe.overflowed()
+
+    # ---- end-to-end through the public API with pinned host buffers (e2e) ----
+    host = [(o.cpu().pin_memory(), p.cpu().pin_memory(), c.cpu().pin_memory()) for o, p, c in dev_batches]
+    loss_host = torch.empty(BATCH, dtype=torch.float64).pin_memory()
+    for k in range(args.warmup):
+        o, p, c = host[k % nb]
+        rec.step_host(o, p, c, lr, global_batch=global_batch, loss_out=loss_host)
+    barrier()
+    start.record()
+    for k in range(args.steps):
+        o, p, c = host[k % nb]
+        rec.step_host(o, p, c, lr, global_batch=global_batch, loss_out=loss_host)
+    end.record()
+    barrier()
+    ms_e2e = start.elapsed_time(end)
+    if dist is not None:
+        t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = global_batch * args.steps / (ms_e2e / 1e3)
+    h2d = BATCH * D * D * 4 + BATCH * 12 * 8 + BATCH * 8 * 8
+    d2h = BATCH * 8
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    f_mhz = clocks.get("sm_mhz") or 1965.0
+    pairs_per_launch = step_pairs / args.steps
+    bwd_achieved = pairs_per_launch / (stage_ms["bwd"] / 1e3) / 1e9
+    bwd_peak = 8.0 * 148 * f_mhz * 1e6 / 1e9            # 128 lanes/clk/SM / 16 issue slots per pair
+    step_peak = 148 * f_mhz * 1e6 / 0.164 / 1e9          # 0.164 SM-clk per pair fwd+bwd
+    step_achieved = pairs_per_launch / (ms / args.steps / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "raster_bwd_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 binning bbox, fp64 Adam master params)", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_gaussians": N_GAUSS, "image_px": D, "batch_per_gpu": BATCH,
+                   "global_batch": global_batch, "parallelism": f"dp{world}", "ctf": True,
+                   "l2": f"inputs larger than L2: {DATASET}-particle dataset ({DATASET * D * D * 4 >> 20} MiB) cycled"},
+        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": engine.StepPipeline.OWN_LAUNCHES_PER_STEP * args.steps + (args.steps if world > 1 else 0),
+        "roofline": {"bound": "fp32_sfu_issue", "kernel": "raster_bwd", "achieved": bwd_achieved, "peak": bwd_peak,
+                     "unit": "Gpair/s", "frac": bwd_achieved / bwd_peak, "traffic": traffic,
+                     "peak_basis": (f"SURVEY.md 8(d): 1 EX2 + 15 FP32 per in-ellipse pair, 128 FP32 lanes/clk/SM "
+                                    f"x 148 SMs at the sampled {f_mhz:.0f} MHz"),
+                     "units_per_launch": pairs_per_launch, "launch_ms": stage_ms["bwd"]},
+        "roofline_step": {"achieved": step_achieved, "peak": step_peak, "unit": "Gpair/s",
+                          "frac": step_achieved / step_peak,
+                          "peak_basis": "0.164 SM-clk per in-ellipse pair (fwd+bwd issue), SURVEY.md 8(d)"},
+        "stage_ms": stage_ms,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    if overflow:
+        line["warning"] = "tile-list overflow during timing"
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -269,20 +269,43 @@ class StepPipeline:
         _lib.call("cgs_exclusive_scan", _ptr(self.counts), _ptr(self.offs), self.counts.numel(),
                   _ptr(self.scan_ws), s)
 
-    def forward_backward(self, params, poses, obs, ctf):
-        """K0..K5 for a batch; leaves partial accumulators in self.partial."""
+    # kernels of libcgs_b200 launched by one forward_backward + adam (bench accounting):
+    # prepare, bin_count, scan x3, bin_scatter, raster_fwd, ctf_multiply x2, loss_resid,
+    # raster_bwd, epilogue_adam  (cuFFT's own R2C/C2R kernels are library launches)
+    OWN_LAUNCHES_PER_STEP = 12
+
+    def forward_backward(self, params, poses, obs, ctf, events=None):
+        """K0..K5 for a batch; leaves partial accumulators in self.partial.
+
+        ``events`` (optional dict of name -> (start, end) torch.cuda.Event
+        lists) records CUDA events around the bin / fwd / ctf / bwd stages on
+        the launching stream, for per-kernel timing inside the bench.
+        """
         s = self.ctx.stream
+
+        def mark(name, which):
+            if events is not None and name in events:
+                events[name][which].record()
+
+        mark("bin", 0)
         self._count(params, poses)
         _lib.call("cgs_bin_scatter", _ptr(self.rects), self.n, self.B, self.D, self.tile, _ptr(self.offs),
                   _ptr(self.items), self.items.numel(), _ptr(self.status), s)
+        mark("bin", 1)
+        mark("fwd", 0)
         _lib.call("cgs_raster_fwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid, self.tile,
                   _ptr(self.items), _ptr(self.offs), self.items.numel(), _ptr(self.render),
                   _lib.CGS_LAYOUT_NATURAL, s)
+        mark("fwd", 1)
+        mark("ctf", 0)
         _lib.call("cgs_ctf_mse", self.plan, _ptr(self.render), _ptr(obs), self.B, self.grid, _ptr(ctf),
                   _ptr(self.spectrum), 0, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status),
                   _lib.CGS_LAYOUT_NATURAL, s)
+        mark("ctf", 1)
+        mark("bwd", 0)
         _lib.call("cgs_raster_bwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid,
                   _ptr(self.upstream), _lib.CGS_LAYOUT_NATURAL, _ptr(self.partial), self.ipg, s)
+        mark("bwd", 1)
 
     def reduce(self):
         _lib.call("cgs_reduce_partials", _ptr(self.partial), self.G, self.n, _ptr(self.acc), self.ctx.stream)

@@ -240,17 +240,40 @@ class Reconstructor:
             _, poses, _ = self._batch(local)
             pipe.grow(pipe.measure_items(self.params, poses))
 
-    def step(self, indices, lr: float, *, retry: bool = True):
+    def step(self, indices, lr: float):
         """One step over the global batch ``indices``; returns per-image losses (device)."""
-        torch = _torch()
         indices = np.asarray(indices)
         local = self.local_slice(indices)
-        pipe = self.pipeline(len(local))
         obs, poses, ctfs = self._batch(local)
+        return self.step_batch(obs, poses, ctfs, lr, global_batch=len(indices))
+
+    def step_host(self, obs, poses, ctfs, lr: float, *, global_batch: int, loss_out=None):
+        """Public end-to-end step from (pinned) HOST buffers of this rank's batch.
+
+        Copies the batch host->device on the current stream, runs the step and
+        copies the per-image losses device->host into ``loss_out`` (pinned), all
+        stream-ordered; the caller synchronises when it needs the numbers.
+        """
+        torch = _torch()
+        dev = self.ctx.device
+        o = obs.to(dev, non_blocking=True)
+        p = poses.to(dev, non_blocking=True)
+        c = None if ctfs is None else ctfs.to(dev, non_blocking=True)
+        loss = self.step_batch(o, p, c, lr, global_batch=global_batch)
+        if loss_out is not None:
+            loss_out.copy_(loss, non_blocking=True)
+        del torch
+        return loss
+
+    def step_batch(self, obs, poses, ctfs, lr: float, *, global_batch: int, events=None):
+        """One step on device tensors of this rank's batch (obs f32 [b][D][D],
+        poses f64 [b][12], ctfs f64 [b][8] or None); ``global_batch`` sets the
+        1/B loss scale.  Returns the device tensor of per-image losses."""
+        pipe = self.pipeline(obs.shape[0])
         cfg = self.config
         pipe.clear_status()
-        pipe.forward_backward(self.params, poses, obs, ctfs)
-        scale = 1.0 / len(indices)
+        pipe.forward_backward(self.params, poses, obs, ctfs, events=events)
+        scale = 1.0 / global_batch
         self.t += 1
         if self.world > 1:
             acc = parallel.allreduce_accumulator(pipe.reduce(), self.pg)
