@@ -253,7 +253,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         rec.step_batch(o, p, c, lr, global_batch=global_batch)
     barrier()
     sampler = ClockSampler(local_rank)
-    stage = {n: [] for n in ("bin", "fwd", "ctf", "bwd")}
+    stage = {n: [] for n in ("fwd", "ctf", "bwd")}
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_pairs = 0
     start.record()

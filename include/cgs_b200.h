@@ -14,7 +14,8 @@
  * Data layouts (row-major, C-contiguous):
  *   params   f64 [N][11]  mean xyz | raw scale xyz | quaternion wxyz | raw amp
  *                         (gmm.py:25-29)
- *   splat    f32 [N][16]  prepared per-Gaussian record (cgs_prepare)
+ *   splat    f32 [N][16]  prepared per-Gaussian record (cgs_prepare):
+ *                         mean xyz, amp, M = R diag(s) (9, row-major), s xyz
  *   poses    f64 [B][12]  rotation W row-major (9), translation tx ty (2), pad
  *                         (splat.py:73-104; translation in normalised units)
  *   ctf      f64 [B][8]   defocus_u, defocus_v [A], astigmatism_angle [rad],
@@ -124,6 +125,18 @@ int cgs_bin_scatter(const uint32_t *rects, int64_t n, int32_t B, int32_t size, i
 int cgs_raster_fwd(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
                    int32_t tile, const int32_t *items, const int32_t *offs, int64_t capacity,
                    float *out, int32_t layout, void *stream);
+
+/* ---- K3 (training path): binning-free render -------------------------------
+ * Same image as cgs_raster_fwd without tile lists: one lane per (image,
+ * Gaussian) walks its footprint and adds w (e - sub) into a shared-memory
+ * image as int32 fixed point (scale 2^30 / sum of view-independent weight
+ * bounds, so sums cannot overflow and the result is bitwise deterministic).
+ * out f32 [B][D][D] natural layout (used as int32 scratch first); ws holds
+ * cgs_render_workspace_bytes(n) bytes.  Replaces rasterize (splat.py:263-298)
+ * inside the training step. */
+size_t cgs_render_workspace_bytes(int64_t n);
+int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
+               void *ws, void *stream);
 
 /* ---- K4: CTF, centred FFTs and MSE (optics.py:78-141, train.py:114-121,153)
  * ctf_evaluate (optics.py:93-121): H f64 [B][D][D], centred layout. */

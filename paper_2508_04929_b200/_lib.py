@@ -61,6 +61,8 @@ PROTOTYPES = {
     "cgs_exclusive_scan": (ctypes.c_int, [P, P, I64, P, P]),
     "cgs_bin_scatter": (ctypes.c_int, [P, I64, I32, I32, I32, P, P, I64, P, P]),
     "cgs_raster_fwd": (ctypes.c_int, [P, I64, P, I32, G, I32, P, P, I64, P, I32, P]),
+    "cgs_render_workspace_bytes": (ctypes.c_size_t, [I64]),
+    "cgs_render": (ctypes.c_int, [P, I64, P, I32, G, P, P, P]),
     "cgs_ctf_evaluate": (ctypes.c_int, [P, I32, G, P, P]),
     "cgs_fft_plan_create": (ctypes.c_int, [I32, I32, ctypes.POINTER(ctypes.c_void_p)]),
     "cgs_fft_plan_destroy": (ctypes.c_int, [P]),

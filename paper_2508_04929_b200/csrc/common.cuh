@@ -83,10 +83,19 @@ __host__ __forceinline__ GridF make_grid_f(const cgs_grid &g) {
 // _clamp_eigenvalues (splat.py:229-260).
 //   q(dx, dy) = p00 dx^2 + 2 p01 dx dy + p11 dy^2, d = pixel - mean  [pixels]
 //   l = -q/2 * log2(e) = A dx^2 + Bc dx dy + C dy^2   (exp(-q/2) = 2^l)
+//
+// Rows are walked in row-conditional coordinates: on pixel row dy the
+// ellipse is centred at x_c(dy) = mpx - (p01/p00) dy and, with dx' = x - x_c,
+//   q = p00 dx'^2 + k dy^2,   k = p11 - p01^2/p00 = 1/c11,
+// a sum of two non-negative terms.  Expanding (p00 dx + p01 dy)^2 instead
+// cancels catastrophically in fp32 for thin diagonal footprints.
 struct Splat2 {
     float mpx, mpy;        // mean in pixel-index coordinates
     float p00, p01, p11;   // precision in px^-2
-    float A, Bc, C;        // log2-scaled quadratic form
+    float A, Bc, C;        // log2-scaled quadratic form: l = A dx^2 + Bc dx dy + C dy^2
+    float slope;           // p01 / p00: x_c(dy) = mpx - slope * dy
+    float k, Ck;           // k = 1/c11 [px^-2]; Ck = -log2(e)/2 * k
+    float inv_sqrt_p00;    // row half-span = sqrt((cut - k dy^2) / p00)
     float cnorm;           // 1 / (2 pi sqrt(det)) in normalised units
     float w;               // amp * cnorm
     float hx, hy;          // half-extents of the q < cutoff ellipse [px]
@@ -141,7 +150,25 @@ __device__ __forceinline__ Splat2 project2(const SplatRec &r, const PoseF &P, co
     s.C = -0.5f * kLog2e * s.p11;
     s.hx = sqrtf(kCutoffSq * c00);
     s.hy = sqrtf(kCutoffSq * c11);
+    s.slope = s.p01 / s.p00;
+    s.k = 1.f / c11;
+    s.Ck = -0.5f * kLog2e * s.k;
+    s.inv_sqrt_p00 = rsqrtf(s.p00);
     return s;
+}
+
+// Pixel span [xa, xb] of row dy (clipped to [xlo, xhi]) inside q < cutoff,
+// and the row-conditional offset dx' of xa.  Returns false for an empty row.
+__device__ __forceinline__ bool row_span(const Splat2 &s, float dy, int xlo, int xhi, int &xa, int &xb,
+                                         float &dxa) {
+    const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
+    if (rem <= 0.f) return false;
+    const float half = sqrtf(rem) * s.inv_sqrt_p00;
+    const float xc = fmaf(-s.slope, dy, s.mpx);
+    xa = max((int)ceilf(xc - half), xlo);
+    xb = min((int)floorf(xc + half), xhi);
+    dxa = (float)xa - xc;
+    return xa <= xb;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

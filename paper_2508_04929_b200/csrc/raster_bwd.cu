@@ -2,167 +2,168 @@
 // (_kernels.py:128-190) plus the per-image part of rasterize_backward
 // (splat.py:332-349), batched over images.
 //
-// Gaussian-major and atomic-free: a CTA owns kGPC Gaussians and a group of
-// images.  For each image it stages the upstream gradient (natural layout,
-// padded rows) in shared memory; each Gaussian is handled by kLPG lanes, lane
-// i walking rows i, i+kLPG, ... of the footprint along the exact q < 6.5^2
-// row span.  Per pixel it accumulates seven moments of g*e in pixel units
-// (sum ge, sum g, sum ge dx, ge dx^2 and per row ge dy, ge dx dy, ge dy^2),
-// which carry the reference's six raw sums exactly:
-//   sA = sum ge - sub sum g,  s_ab = 1/(2h^2) (sum ge pd_a pd_b - p_ab sA), ...
-// The kLPG lanes reduce them with xor shuffles, convert them to the
-// image-summable 10-float world-frame accumulator
-//   {cnorm sA, W2^T ac (sx, sy), W2^T (ac S) W2}
-// and add it to a per-CTA shared accumulator that exactly one lane group owns.
-// The CTA writes its image group's partial once; cgs_epilogue_* sums groups in
-// a fixed order, so the gradient is bitwise reproducible.
+// Gaussian-major, one lane per (image, Gaussian), atomic-free.  A CTA owns
+// kGPC Gaussians (one per thread) and a group of images; for each image it
+// stages the upstream gradient in shared memory, and every thread walks its
+// own Gaussian's footprint row by row along the exact q < 6.5^2 span.  Same-
+// size footprints keep the warp's lanes in near lockstep, so no lane sits idle
+// on another lane's rows and no cross-lane reduction is needed.  Per pixel it
+// accumulates moments of ge = g e in pixel units:
+//   per row:   sum ge, sum g, sum ge dx, sum ge dx^2
+//   per image: + dy-weighted row sums -> 7 moments
+// which carry the reference's six raw sums exactly
+//   sA = sum ge - sub sum g,   s_ab = 1/(2 h^2) (sum ge pd_a pd_b - p_ab sA),
+// then converts them, in registers, to the image-summable 10-float world-frame
+// accumulator {cnorm sA, W2^T ac (sx, sy), W2^T (ac S) W2} (SURVEY.md 8(a)
+// row 15) and keeps summing that over the CTA's images.  The CTA writes its
+// image group's partial once; the epilogue sums groups in fixed order, so the
+// gradient is bitwise reproducible.
 #include "common.cuh"
 
 namespace cgs {
 
-constexpr int kLPG = 8;                  // lanes per Gaussian
-constexpr int kGPW = 32 / kLPG;          // Gaussians per warp per pass
 constexpr int kBwdThreads = 256;
-constexpr int kGPC = 256;                // Gaussians per CTA
+constexpr int kGPC = kBwdThreads;        // Gaussians per CTA, one per thread
 constexpr int kBandBytes = 96 * 1024;    // upstream rows staged per band
 
 __device__ __forceinline__ void stage_rows(float *__restrict__ img, const float *__restrict__ up,
                                            int b, int D, int r0, int r1, int layout) {
-    const int ld = D + 1, c0 = D / 2;
-    const int total = (r1 - r0) * D;
     const float *src = up + (int64_t)b * D * D;
+    const int total = (r1 - r0) * D;
+    if (layout == CGS_LAYOUT_NATURAL && (D & 3) == 0) {
+        const float4 *s4 = reinterpret_cast<const float4 *>(src + (int64_t)r0 * D);
+        float4 *d4 = reinterpret_cast<float4 *>(img);
+        for (int i = threadIdx.x; i < (total >> 2); i += blockDim.x) d4[i] = __ldg(s4 + i);
+        return;
+    }
+    const int c0 = D / 2;
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
         int r = idx / D, x = idx - r * D;
-        int iy = r0 + r;
-        int sy = iy, sx = x;
+        int sy = r0 + r, sx = x;
         if (layout == CGS_LAYOUT_FFT) {
-            sy = iy - c0; if (sy < 0) sy += D;
-            sx = x - c0; if (sx < 0) sx += D;
+            sy -= c0; if (sy < 0) sy += D;
+            sx -= c0; if (sx < 0) sx += D;
         }
-        img[r * ld + x] = src[(int64_t)sy * D + sx];
+        img[idx] = src[(int64_t)sy * D + sx];
     }
 }
 
-__global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(
+struct Moments {
+    float e, g, x, y, xx, xy, yy;
+};
+
+// one pixel of the row walk in row-conditional coordinates (common.cuh):
+// e = 2^l, l = A dx'^2 + Ck dy^2
+__device__ __forceinline__ void bwd_pixel(float gp, float dx, float A, float Ckdy2,
+                                          float &rE, float &rG, float &rX, float &rXX) {
+    const float e = ex2_approx(fmaf(A * dx, dx, Ckdy2));
+    const float ge = gp * e;
+    rE += ge;
+    rG += gp;
+    const float t = ge * dx;
+    rX += t;
+    rXX = fmaf(t, dx, rXX);
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 2) raster_bwd_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, int layout, float *__restrict__ partial, int ipg, int HB) {
-    extern __shared__ float sm[];
-    const int D = G.D, ld = D + 1;
-    float *img = sm;
-    float *acc = sm + HB * ld;
-    const int64_t g0 = (int64_t)blockIdx.x * kGPC;
+    extern __shared__ float img[];
+    const int D = G.D;
+    const int64_t g = (int64_t)blockIdx.x * kGPC + threadIdx.x;
+    const bool valid = g < n;
     const int grp = blockIdx.y;
     const int b_begin = grp * ipg, b_end = min(B, b_begin + ipg);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sub = lane / kLPG, li = lane % kLPG;
-    for (int i = threadIdx.x; i < kGPC * CGS_ACC_STRIDE; i += blockDim.x) acc[i] = 0.f;
+    SplatRec rec{};
+    if (valid) rec = load_splat(splat, g);
+    float acc[CGS_ACC_STRIDE];
+#pragma unroll
+    for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = 0.f;
 
     for (int b = b_begin; b < b_end; ++b) {
         const PoseF P = load_pose_f(poses, b);
+        Splat2 s{};
+        int ylo = 1, yhi = 0;
+        if (valid) {
+            s = project2(rec, P, G);
+            if (s.w > 0.f) {
+                ylo = max((int)ceilf(s.mpy - s.hy), 0);
+                yhi = min((int)floorf(s.mpy + s.hy), D - 1);
+            }
+        }
+        Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int r0 = 0; r0 < D; r0 += HB) {
             const int r1 = min(D, r0 + HB);
             __syncthreads();
             stage_rows(img, upstream, b, D, r0, r1, layout);
             __syncthreads();
-            for (int k = warp * kGPW + sub; k < kGPC; k += (kBwdThreads / 32) * kGPW) {
-                const int64_t g = g0 + k;
-                Splat2 s{};
-                int ylo = 1, yhi = 0;
-                if (g < n) {
-                    s = project2(load_splat(splat, g), P, G);
-                    if (s.w > 0.f) {
-                        ylo = max(max((int)ceilf(s.mpy - s.hy), r0), 0);
-                        yhi = min(min((int)floorf(s.mpy + s.hy), r1 - 1), D - 1);
-                    }
+            const int ya = max(ylo, r0), yb = min(yhi, r1 - 1);
+            for (int iy = ya; iy <= yb; ++iy) {
+                const float dy = (float)iy - s.mpy;
+                int xa, xb;
+                float dx;
+                if (!row_span(s, dy, 0, D - 1, xa, xb, dx)) continue;
+                const float Ckdy2 = s.Ck * dy * dy;
+                const float *row = img + (iy - r0) * D;
+                float rE = 0.f, rG = 0.f, rX = 0.f, rXX = 0.f, rE2 = 0.f, rG2 = 0.f, rX2 = 0.f, rXX2 = 0.f;
+                int x = xa;
+                for (; x < xb; x += 2) {  // two independent chains per iteration
+                    bwd_pixel(row[x], dx, s.A, Ckdy2, rE, rG, rX, rXX);
+                    bwd_pixel(row[x + 1], dx + 1.f, s.A, Ckdy2, rE2, rG2, rX2, rXX2);
+                    dx += 2.f;
                 }
-                float Me = 0.f, Mg = 0.f, Mx = 0.f, My = 0.f, Mxx = 0.f, Mxy = 0.f, Myy = 0.f;
-                for (int iy = ylo + li; iy <= yhi; iy += kLPG) {
-                    const float dy = (float)iy - s.mpy;
-                    // exact span of q < cutoff on this row:
-                    // p00 dx^2 + 2 (p01 dy) dx + (p11 dy^2 - cut) < 0
-                    const float bq = s.p01 * dy;
-                    const float cq = fmaf(s.p11 * dy, dy, -kCutoffSq);
-                    const float disc = fmaf(bq, bq, -s.p00 * cq);
-                    if (disc <= 0.f) continue;
-                    const float root = sqrtf(disc);
-                    const float inv = 1.f / s.p00;
-                    const int xa = max((int)ceilf(s.mpx + (-bq - root) * inv), 0);
-                    const int xb = min((int)floorf(s.mpx + (-bq + root) * inv), D - 1);
-                    const float Bdy = s.Bc * dy, Cdy2 = s.C * dy * dy;
-                    const float *row = img + (iy - r0) * ld;
-                    float rE = 0.f, rG = 0.f, rX = 0.f;
-                    float dx = (float)xa - s.mpx;
-                    for (int x = xa; x <= xb; ++x) {
-                        const float e = ex2_approx(fmaf(fmaf(s.A, dx, Bdy), dx, Cdy2));
-                        const float gp = row[x];
-                        const float ge = gp * e;
-                        rE += ge;
-                        rG += gp;
-                        const float tq = ge * dx;
-                        rX += tq;
-                        Mxx = fmaf(tq, dx, Mxx);
-                        dx += 1.f;
-                    }
-                    Me += rE;
-                    Mg += rG;
-                    Mx += rX;
-                    My = fmaf(dy, rE, My);
-                    Mxy = fmaf(dy, rX, Mxy);
-                    Myy = fmaf(dy * dy, rE, Myy);
-                }
-#pragma unroll
-                for (int o = kLPG / 2; o > 0; o >>= 1) {
-                    Me += __shfl_xor_sync(0xffffffffu, Me, o);
-                    Mg += __shfl_xor_sync(0xffffffffu, Mg, o);
-                    Mx += __shfl_xor_sync(0xffffffffu, Mx, o);
-                    My += __shfl_xor_sync(0xffffffffu, My, o);
-                    Mxx += __shfl_xor_sync(0xffffffffu, Mxx, o);
-                    Mxy += __shfl_xor_sync(0xffffffffu, Mxy, o);
-                    Myy += __shfl_xor_sync(0xffffffffu, Myy, o);
-                }
-                if (ylo <= yhi) {
-                    // moments -> the reference's raw sums (normalised units)
-                    const float ih2 = 0.5f * G.inv_h * G.inv_h;
-                    const float p00 = s.p00, p01 = s.p01, p11 = s.p11;
-                    const float sA = Me - kSub * Mg;
-                    const float sx = (p00 * Mx + p01 * My) * G.inv_h;
-                    const float sy = (p01 * Mx + p11 * My) * G.inv_h;
-                    const float Sxx = p00 * p00 * Mxx + 2.f * p00 * p01 * Mxy + p01 * p01 * Myy;
-                    const float Sxy = p00 * p01 * Mxx + (p00 * p11 + p01 * p01) * Mxy + p01 * p11 * Myy;
-                    const float Syy = p01 * p01 * Mxx + 2.f * p01 * p11 * Mxy + p11 * p11 * Myy;
-                    const float ac = s.w;
-                    const float S00 = ac * ih2 * (Sxx - p00 * sA);
-                    const float S01 = ac * ih2 * (Sxy - p01 * sA);
-                    const float S11 = ac * ih2 * (Syy - p11 * sA);
-                    const float d0 = ac * sx, d1 = ac * sy;
-                    float *a = acc + k * CGS_ACC_STRIDE;
-#pragma unroll
-                    for (int c = li; c < CGS_ACC_STRIDE; c += kLPG) {
-                        float v;
-                        switch (c) {
-                            case 0: v = s.cnorm * sA; break;
-                            case 1: v = d0 * P.w0[0] + d1 * P.w1[0]; break;
-                            case 2: v = d0 * P.w0[1] + d1 * P.w1[1]; break;
-                            case 3: v = d0 * P.w0[2] + d1 * P.w1[2]; break;
-                            default: {
-                                // P3_kl = sum_ab W_ak S_ab W_bl for (k,l) in xx xy xz yy yz zz
-                                const int kk = (c == 4 || c == 5 || c == 6) ? 0 : (c == 9 ? 2 : 1);
-                                const int ll = (c == 4) ? 0 : (c == 5 || c == 7) ? 1 : 2;
-                                v = S00 * P.w0[kk] * P.w0[ll] +
-                                    S01 * (P.w0[kk] * P.w1[ll] + P.w1[kk] * P.w0[ll]) +
-                                    S11 * P.w1[kk] * P.w1[ll];
-                            }
-                        }
-                        a[c] += v;
-                    }
-                }
+                if (x == xb) bwd_pixel(row[x], dx, s.A, Ckdy2, rE, rG, rX, rXX);
+                M.xx += rXX + rXX2;
+                rE += rE2;
+                rG += rG2;
+                rX += rX2;
+                M.e += rE;
+                M.g += rG;
+                M.x += rX;
+                M.y = fmaf(dy, rE, M.y);
+                M.xy = fmaf(dy, rX, M.xy);
+                M.yy = fmaf(dy * dy, rE, M.yy);
             }
         }
+        if (ylo <= yhi) {
+            // moments -> the reference's raw sums (normalised units), then the
+            // world-frame accumulator for this image
+            const float ih2 = 0.5f * G.inv_h * G.inv_h;
+            const float p00 = s.p00, p01 = s.p01, p11 = s.p11;
+            // row-conditional moments: (P d)_x = p00 dx', (P d)_y = p01 dx' + k dy
+            const float k = s.k;
+            const float sA = M.e - kSub * M.g;
+            const float sx = (p00 * M.x) * G.inv_h;
+            const float sy = (p01 * M.x + k * M.y) * G.inv_h;
+            const float Sxx = p00 * p00 * M.xx;
+            const float Sxy = p00 * (p01 * M.xx + k * M.xy);
+            const float Syy = p01 * p01 * M.xx + 2.f * p01 * k * M.xy + k * k * M.yy;
+            const float ac = s.w;
+            const float S00 = ac * ih2 * (Sxx - p00 * sA);
+            const float S01 = ac * ih2 * (Sxy - p01 * sA);
+            const float S11 = ac * ih2 * (Syy - p11 * sA);
+            const float d0 = ac * sx, d1 = ac * sy;
+            acc[0] += s.cnorm * sA;
+            acc[1] += d0 * P.w0[0] + d1 * P.w1[0];
+            acc[2] += d0 * P.w0[1] + d1 * P.w1[1];
+            acc[3] += d0 * P.w0[2] + d1 * P.w1[2];
+            // P3_kl = sum_ab W_ak S_ab W_bl, (k,l) in xx xy xz yy yz zz
+            const float u0 = S00 * P.w0[0] + S01 * P.w1[0], v0 = S01 * P.w0[0] + S11 * P.w1[0];
+            const float u1 = S00 * P.w0[1] + S01 * P.w1[1], v1 = S01 * P.w0[1] + S11 * P.w1[1];
+            const float u2 = S00 * P.w0[2] + S01 * P.w1[2], v2 = S01 * P.w0[2] + S11 * P.w1[2];
+            acc[4] += u0 * P.w0[0] + v0 * P.w1[0];
+            acc[5] += u0 * P.w0[1] + v0 * P.w1[1];
+            acc[6] += u0 * P.w0[2] + v0 * P.w1[2];
+            acc[7] += u1 * P.w0[1] + v1 * P.w1[1];
+            acc[8] += u1 * P.w0[2] + v1 * P.w1[2];
+            acc[9] += u2 * P.w0[2] + v2 * P.w1[2];
+        }
     }
-    __syncthreads();
-    const int64_t cnt = min((int64_t)kGPC, n - g0);
-    float *dst = partial + ((int64_t)grp * n + g0) * CGS_ACC_STRIDE;
-    for (int64_t i = threadIdx.x; i < cnt * CGS_ACC_STRIDE; i += blockDim.x) dst[i] = acc[i];
+    if (valid) {
+        float *dst = partial + ((int64_t)grp * n + g) * CGS_ACC_STRIDE;
+#pragma unroll
+        for (int c = 0; c < CGS_ACC_STRIDE; ++c) dst[c] = acc[c];
+    }
 }
 
 // In-ellipse pair count per image (same row spans as the backward).
@@ -179,15 +180,9 @@ __global__ void __launch_bounds__(256) count_pairs_kernel(const float *__restric
         int ylo = max((int)ceilf(s.mpy - s.hy), 0), yhi = min((int)floorf(s.mpy + s.hy), D - 1);
         if (s.w > 0.f) {
             for (int iy = ylo; iy <= yhi; ++iy) {
-                const float dy = (float)iy - s.mpy;
-                const float bq = s.p01 * dy;
-                const float cq = fmaf(s.p11 * dy, dy, -kCutoffSq);
-                const float disc = fmaf(bq, bq, -s.p00 * cq);
-                if (disc <= 0.f) continue;
-                const float root = sqrtf(disc), inv = 1.f / s.p00;
-                const int xa = max((int)ceilf(s.mpx + (-bq - root) * inv), 0);
-                const int xb = min((int)floorf(s.mpx + (-bq + root) * inv), D - 1);
-                if (xb >= xa) cnt += xb - xa + 1;
+                int xa, xb;
+                float dx;
+                if (row_span(s, (float)iy - s.mpy, 0, D - 1, xa, xb, dx)) cnt += xb - xa + 1;
             }
         }
     }
@@ -211,10 +206,10 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
         !upstream || !partial)
         return CGS_ERR_ARG;
     const int D = grid.size;
-    int HB = kBandBytes / ((D + 1) * (int)sizeof(float));
+    int HB = kBandBytes / (D * (int)sizeof(float));
     if (HB < 1) return CGS_ERR_UNSUPPORTED;
     HB = HB > D ? D : HB;
-    size_t smem = ((size_t)HB * (D + 1) + (size_t)kGPC * CGS_ACC_STRIDE) * sizeof(float);
+    size_t smem = (size_t)HB * D * sizeof(float);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

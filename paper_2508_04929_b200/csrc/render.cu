@@ -1,0 +1,182 @@
+// K3 (training path): binning-free forward render with deterministic
+// fixed-point shared-memory accumulation.
+//
+// The reference renders tile by tile from per-tile Gaussian lists
+// (build_tile_work + forward_tiles, _kernels.py:17-125).  On B200 the faster
+// schedule for ~1 px footprints is Gaussian-major, like the backward: one
+// lane per (image, Gaussian) walks its own footprint along the exact
+// q < 6.5^2 row spans and adds w (e - sub) into a shared-memory image.  Lanes
+// of a warp hit unrelated pixels, so the adds must be atomic; shared-memory
+// float atomics are CAS loops on sm_100a (3 updates/clk/SM measured), native
+// int32 ATOMS.ADD sustain ~10/clk/SM at random addresses
+// (profiles/microbench_smem_atomics_r01.txt).  Values are therefore added as
+// round-to-nearest int32 fixed point with one scale per step:
+//   scale = 2^30 / sum_g wb_g,   wb_g >= w_g(b) for every view b,
+// so no pixel sum can overflow, and integer addition makes the render
+// bitwise reproducible regardless of scheduling.  One ulp is sum wb / 2^30,
+// ~1e-6 of the image's total peak weight (render tolerance is 1e-4 rel L2).
+//
+// wb_g: by eigenvalue interlacing the projected 2x2 covariance has
+// lambda1 >= s_mid^2 and lambda2 >= s_min^2; with the eigenvalue floor
+// (0.1 px)^2 (splat.py:207-209) det >= max(s_mid^2, f) max(s_min^2, f), so
+// w = amp / (2 pi sqrt(det)) <= amp / (2 pi sqrt(that)).
+//
+// Along a row, e = exp(-q/2) follows e_{k+1} = e_k g_k, g_{k+1} = g_k c with
+// c = 2^(2A): two FMULs per pixel instead of an MUFU.EX2, restarted every 16
+// pixels so the recurrence error stays below 1e-5.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace cgs {
+
+constexpr int kRThreads = 256;
+constexpr int kRChunk = 4096;              // Gaussians per CTA
+constexpr int kRBandBytes = 64 * 1024;     // int32 accumulator rows per CTA
+constexpr int kWbBlock = 1024;
+constexpr float kFixedRange = 1073741824.f;  // 2^30
+
+__global__ void __launch_bounds__(kWbBlock) wbound_partial_kernel(const float *__restrict__ splat, int64_t n,
+                                                                  double h, float *__restrict__ part) {
+    const int64_t g = blockIdx.x * (int64_t)kWbBlock + threadIdx.x;
+    float wb = 0.f;
+    if (g < n) {
+        const float *r = splat + g * CGS_SPLAT_STRIDE;
+        const double s0 = r[13], s1 = r[14], s2 = r[15], amp = r[3];
+        const double lo = fmin(s0, fmin(s1, s2)), hi = fmax(s0, fmax(s1, s2));
+        const double mid = s0 + s1 + s2 - lo - hi;
+        const double fl = (0.1 * h) * (0.1 * h);
+        const double det = fmax(mid * mid, fl) * fmax(lo * lo, fl);
+        // 1.001: headroom for the fp32 evaluation of w inside the kernels
+        wb = (float)(1.001 * amp / (2.0 * kPiD * sqrt(det)));
+    }
+    __shared__ float ws[kWbBlock / 32];
+    float v = warp_sum(wb);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float t = warp_sum(ws[threadIdx.x]);
+        if (threadIdx.x == 0) part[blockIdx.x] = t;
+    }
+}
+
+// scale = 2^30 / sum(part), written to part[nparts]; fixed-order reduction
+__global__ void __launch_bounds__(256) wbound_scale_kernel(float *part, int nparts) {
+    __shared__ double ws[8];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += 256) t += part[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += ws[w];
+        part[nparts] = s > 0.0 ? (float)((double)kFixedRange / s) : 1.f;
+    }
+}
+
+__global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
+    const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, GridF G,
+    const float *__restrict__ scale_ptr, int HB, int *__restrict__ out) {
+    extern __shared__ int band[];
+    const int D = G.D;
+    const int b = blockIdx.y;
+    const int r0 = blockIdx.z * HB, r1 = min(D, r0 + HB);
+    const int npx = (r1 - r0) * D;
+    for (int i = threadIdx.x; i < npx; i += kRThreads) band[i] = 0;
+    const float scale = *scale_ptr;
+    const PoseF P = load_pose_f(poses, b);
+    const int64_t g_begin = (int64_t)blockIdx.x * kRChunk;
+    const int64_t g_end = min(n, g_begin + kRChunk);
+    __syncthreads();
+    for (int64_t g = g_begin + threadIdx.x; g < g_end; g += kRThreads) {
+        const Splat2 s = project2(load_splat(splat, g), P, G);
+        if (!(s.w > 0.f)) continue;
+        const int ylo = max(max((int)ceilf(s.mpy - s.hy), 0), r0);
+        const int yhi = min(min((int)floorf(s.mpy + s.hy), D - 1), r1 - 1);
+        const float wS = s.w * scale, wsubS = s.w * kSub * scale;
+        const float c = exp2f(2.f * s.A);  // g_{k+1} / g_k
+        for (int iy = ylo; iy <= yhi; ++iy) {
+            const float dy = (float)iy - s.mpy;
+            int xa, xb;
+            float dx;
+            if (!row_span(s, dy, 0, D - 1, xa, xb, dx)) continue;
+            const float Ckdy2 = s.Ck * dy * dy;
+            int *row = band + (iy - r0) * D;
+            for (int x0 = xa; x0 <= xb; x0 += 16) {
+                // restart the recurrence from an exact exp every 16 pixels
+                float e = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
+                float gg = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
+                const int xe = min(xb, x0 + 15);
+                for (int x = x0; x <= xe; ++x) {
+                    atomicAdd(row + x, __float2int_rn(fmaf(wS, e, -wsubS)));
+                    e *= gg;
+                    gg *= c;
+                }
+                dx += 16.f;
+            }
+        }
+    }
+    __syncthreads();
+    int *dst = out + (int64_t)b * D * D + (int64_t)r0 * D;
+    for (int i = threadIdx.x; i < npx; i += kRThreads) {
+        const int v = band[i];
+        if (v) atomicAdd(dst + i, v);
+    }
+}
+
+// int32 fixed point -> float, in place
+__global__ void fixed_to_float_kernel(int *__restrict__ buf, int64_t count, const float *__restrict__ scale_ptr) {
+    const float inv = 1.f / *scale_ptr;
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
+    if (i + 3 < count) {
+        int4 v = *reinterpret_cast<int4 *>(buf + i);
+        float4 f = make_float4((float)v.x * inv, (float)v.y * inv, (float)v.z * inv, (float)v.w * inv);
+        *reinterpret_cast<float4 *>(buf + i) = f;
+    } else {
+        for (; i < count; ++i) reinterpret_cast<float *>(buf)[i] = (float)buf[i] * inv;
+    }
+}
+
+}  // namespace cgs
+
+using namespace cgs;
+
+extern "C" size_t cgs_render_workspace_bytes(int64_t n) {
+    int64_t parts = (n + kWbBlock - 1) / kWbBlock;
+    return (size_t)(parts + 1) * sizeof(float);
+}
+
+extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
+                          void *ws, void *stream) {
+    if (n <= 0 || B <= 0 || grid.size < 1 || !splat || !poses || !out || !ws) return CGS_ERR_ARG;
+    const int D = grid.size;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int parts = (int)((n + kWbBlock - 1) / kWbBlock);
+    float *part = (float *)ws;
+    const double h = 2.0 * grid.extent / grid.size;
+    wbound_partial_kernel<<<parts, kWbBlock, 0, st>>>(splat, n, h, part);
+    wbound_scale_kernel<<<1, 256, 0, st>>>(part, parts);
+    int HB = kRBandBytes / (D * (int)sizeof(int));
+    if (HB < 1) return CGS_ERR_UNSUPPORTED;
+    HB = HB > D ? D : HB;
+    const int bands = (D + HB - 1) / HB;
+    const size_t smem = (size_t)HB * D * sizeof(int);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(raster_fwd_atomic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    const int64_t count = (int64_t)B * D * D;
+    cudaMemsetAsync(out, 0, sizeof(int) * count, st);
+    dim3 g((unsigned)((n + kRChunk - 1) / kRChunk), (unsigned)B, (unsigned)bands);
+    raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), part + parts, HB,
+                                                         reinterpret_cast<int *>(out));
+    int rc = check_launch("raster_fwd_atomic_kernel");
+    if (rc) return rc;
+    const int64_t threads = (count + 3) / 4;
+    fixed_to_float_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(reinterpret_cast<int *>(out), count,
+                                                                           part + parts);
+    return check_launch("fixed_to_float_kernel");
+}

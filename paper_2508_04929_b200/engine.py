@@ -7,8 +7,8 @@ the host, and nothing falls back to a CPU path: without a CUDA device or the
 library every entry point raises ``CudaUnavailableError``.
 
 Pipeline of one step (call stack A):
-  K0 cgs_prepare -> K2 cgs_bin_count / cgs_exclusive_scan / cgs_bin_scatter
-  -> K3 cgs_raster_fwd -> K4 cgs_ctf_mse (cuFFT R2C, H_sym, C2R, MSE, R2C,
+  K0 cgs_prepare -> K3 cgs_render (binning-free; or K2 cgs_bin_* + cgs_raster_fwd
+  in tile mode) -> K4 cgs_ctf_mse (cuFFT R2C, H_sym, C2R, MSE, R2C,
   H_sym, C2R) -> K5 cgs_raster_bwd -> [NCCL all-reduce] -> K6
   cgs_epilogue_adam.  All launches are stream-ordered with no host sync.
 """
@@ -28,7 +28,7 @@ try:  # torch is the device-memory / stream / collective plumbing
 except ImportError:  # pragma: no cover - torch is in the image
     torch = None
 
-DEFAULT_TILE = 16
+DEFAULT_TILE = 32
 DEFAULT_IMAGES_PER_GROUP = 16
 
 
@@ -167,6 +167,13 @@ def raster_fwd(ctx, splat, n, poses, grid_s, binning: Binning, out, layout=_lib.
     return out
 
 
+def render_direct(ctx, splat, n, poses, grid_s, out):
+    """K3 binning-free render (cgs_render): images f32 [B][D][D], natural layout."""
+    ws = ctx.buf("render_ws", ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, torch.float32)
+    _lib.call("cgs_render", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, _ptr(out), _ptr(ws), ctx.stream)
+    return out
+
+
 def raster_bwd(ctx, splat, n, poses, grid_s, upstream, ipg=DEFAULT_IMAGES_PER_GROUP, out=None,
                layout=_lib.CGS_LAYOUT_NATURAL):
     """K5: partial world-frame accumulators f32 [G][N][10]."""
@@ -213,29 +220,26 @@ class StepPipeline:
     """One fused training step over a device-resident batch, no host sync.
 
     Buffers are allocated once for (N, B, D); the step is stream-ordered and
-    CUDA-Graph capturable (the item capacity is fixed at construction and an
-    overflow only sets a status bit that makes the Adam epilogue skip the
-    update; ``check_overflow`` reports it and ``grow`` enlarges the buffer).
+    CUDA-Graph capturable.  ``render="direct"`` (default) renders with the
+    binning-free fixed-point kernel (cgs_render); ``render="tiles"`` runs the
+    reference's tile schedule (cgs_bin_* + cgs_raster_fwd), whose item buffer
+    has a fixed capacity: an overflow only sets a status bit that makes the Adam
+    epilogue skip the update (``overflowed``/``grow`` handle it on the host).
     """
 
     def __init__(self, ctx: DeviceContext, n: int, batch: int, grid_s, *, tile=DEFAULT_TILE,
-                 images_per_group=DEFAULT_IMAGES_PER_GROUP, mode="anisotropic", item_capacity=None):
+                 images_per_group=DEFAULT_IMAGES_PER_GROUP, mode="anisotropic", item_capacity=None,
+                 render="direct"):
         self.ctx = ctx
         self.n, self.B, self.grid = int(n), int(batch), grid_s
         self.D = grid_s.size
         self.tile = tile
         self.ipg = images_per_group
         self.mode = _lib.CGS_MODE[mode]
+        self.render_mode = render
         dev = ctx.device
         D = self.D
-        self.T = int(ctx.lib.cgs_bin_tiles(D, tile))
-        self.S = int(ctx.lib.cgs_bin_segments(n))
-        cnt = self.B * self.T * self.S + 1
         self.splat = torch.empty(n * 16, dtype=torch.float32, device=dev)
-        self.rects = torch.empty(self.B * n, dtype=torch.int32, device=dev)
-        self.counts = torch.empty(cnt, dtype=torch.int32, device=dev)
-        self.offs = torch.empty(cnt, dtype=torch.int32, device=dev)
-        self.scan_ws = torch.empty(ctx.lib.cgs_scan_workspace_bytes(cnt) // 4 + 1, dtype=torch.int32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.render = torch.empty((self.B, D, D), dtype=torch.float32, device=dev)
         self.upstream = torch.empty((self.B, D, D), dtype=torch.float32, device=dev)
@@ -245,41 +249,59 @@ class StepPipeline:
         self.partial = torch.empty(self.G * n * 10, dtype=torch.float32, device=dev)
         self.acc = torch.empty(n * 10, dtype=torch.float32, device=dev)
         self.plan = ctx.plan(D, self.B)
-        self.items = torch.empty(max(int(item_capacity or 1), 1), dtype=torch.int32, device=dev)
+        self.render_ws = torch.empty(ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, dtype=torch.float32, device=dev)
+        self.T = int(ctx.lib.cgs_bin_tiles(D, tile))
+        self.S = int(ctx.lib.cgs_bin_segments(n))
+        if render == "tiles":
+            cnt = self.B * self.T * self.S + 1
+            self.rects = torch.empty(self.B * n, dtype=torch.int32, device=dev)
+            self.counts = torch.empty(cnt, dtype=torch.int32, device=dev)
+            self.offs = torch.empty(cnt, dtype=torch.int32, device=dev)
+            self.scan_ws = torch.empty(ctx.lib.cgs_scan_workspace_bytes(cnt) // 4 + 1, dtype=torch.int32, device=dev)
+            self.items = torch.empty(max(int(item_capacity or 1), 1), dtype=torch.int32, device=dev)
+        elif render != "direct":
+            raise ValueError(f"unknown render mode {render!r}")
 
     @property
     def capacity(self) -> int:
-        return self.items.numel()
+        return self.items.numel() if self.render_mode == "tiles" else 0
 
     def grow(self, needed: int) -> None:
+        if self.render_mode != "tiles":
+            return
         cap = int(needed * 1.25) + 1024
         if cap > self.items.numel():
             self.items = torch.empty(cap, dtype=torch.int32, device=self.ctx.device)
 
     def measure_items(self, params, poses) -> int:
-        """Run the count pass once and read the item total (one host sync)."""
+        """Tile mode: run the count pass once and read the item total (one host sync)."""
+        if self.render_mode != "tiles":
+            return 0
+        self._prepare(params)
         self._count(params, poses)
         return int(self.offs[-1].item())
 
+    def _prepare(self, params):
+        _lib.call("cgs_prepare", _ptr(params), self.n, _ptr(self.splat), _ptr(self.status), self.ctx.stream)
+
     def _count(self, params, poses):
         s = self.ctx.stream
-        _lib.call("cgs_prepare", _ptr(params), self.n, _ptr(self.splat), _ptr(self.status), s)
         _lib.call("cgs_bin_count", _ptr(params), self.n, _ptr(poses), self.B, self.grid, self.tile,
                   _ptr(self.rects), _ptr(self.counts), 0, 0, s)
         _lib.call("cgs_exclusive_scan", _ptr(self.counts), _ptr(self.offs), self.counts.numel(),
                   _ptr(self.scan_ws), s)
 
-    # kernels of libcgs_b200 launched by one forward_backward + adam (bench accounting):
-    # prepare, bin_count, scan x3, bin_scatter, raster_fwd, ctf_multiply x2, loss_resid,
-    # raster_bwd, epilogue_adam  (cuFFT's own R2C/C2R kernels are library launches)
-    OWN_LAUNCHES_PER_STEP = 12
+    # kernels of libcgs_b200 launched by one forward_backward + adam (bench accounting), direct mode:
+    # prepare, wbound_partial, wbound_scale, raster_fwd_atomic, fixed_to_float, ctf_multiply x2,
+    # loss_resid, raster_bwd, epilogue_adam  (cuFFT's own R2C/C2R kernels are library launches)
+    OWN_LAUNCHES_PER_STEP = 10
 
     def forward_backward(self, params, poses, obs, ctf, events=None):
         """K0..K5 for a batch; leaves partial accumulators in self.partial.
 
         ``events`` (optional dict of name -> (start, end) torch.cuda.Event
-        lists) records CUDA events around the bin / fwd / ctf / bwd stages on
-        the launching stream, for per-kernel timing inside the bench.
+        lists) records CUDA events around the fwd / ctf / bwd stages on the
+        launching stream, for per-kernel timing inside the bench.
         """
         s = self.ctx.stream
 
@@ -287,15 +309,18 @@ class StepPipeline:
             if events is not None and name in events:
                 events[name][which].record()
 
-        mark("bin", 0)
-        self._count(params, poses)
-        _lib.call("cgs_bin_scatter", _ptr(self.rects), self.n, self.B, self.D, self.tile, _ptr(self.offs),
-                  _ptr(self.items), self.items.numel(), _ptr(self.status), s)
-        mark("bin", 1)
         mark("fwd", 0)
-        _lib.call("cgs_raster_fwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid, self.tile,
-                  _ptr(self.items), _ptr(self.offs), self.items.numel(), _ptr(self.render),
-                  _lib.CGS_LAYOUT_NATURAL, s)
+        self._prepare(params)
+        if self.render_mode == "direct":
+            _lib.call("cgs_render", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid, _ptr(self.render),
+                      _ptr(self.render_ws), s)
+        else:
+            self._count(params, poses)
+            _lib.call("cgs_bin_scatter", _ptr(self.rects), self.n, self.B, self.D, self.tile, _ptr(self.offs),
+                      _ptr(self.items), self.items.numel(), _ptr(self.status), s)
+            _lib.call("cgs_raster_fwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid, self.tile,
+                      _ptr(self.items), _ptr(self.offs), self.items.numel(), _ptr(self.render),
+                      _lib.CGS_LAYOUT_NATURAL, s)
         mark("fwd", 1)
         mark("ctf", 0)
         _lib.call("cgs_ctf_mse", self.plan, _ptr(self.render), _ptr(obs), self.B, self.grid, _ptr(ctf),
@@ -323,6 +348,13 @@ class StepPipeline:
 
     def overflowed(self) -> bool:
         return bool(int(self.status.item()) & _lib.CGS_STATUS_BIN_OVERFLOW)
+
+    def render_only(self, params, poses):
+        """K0 + K3 (direct mode): rendered images in self.render."""
+        self._prepare(params)
+        _lib.call("cgs_render", _ptr(self.splat), self.n, _ptr(poses), poses.shape[0], self.grid, _ptr(self.render),
+                  _ptr(self.render_ws), self.ctx.stream)
+        return self.render
 
     def degenerate(self) -> bool:
         return bool(int(self.status.item()) & _lib.CGS_STATUS_DEGENERATE_ROTATION)

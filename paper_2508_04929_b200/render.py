@@ -143,10 +143,13 @@ def _check_status(status) -> None:
 
 
 def rasterize_batch(mixture: GaussianMixture, rotations, translations, grid: GridSpec, *,
-                    tile_size: int = DEFAULT_TILE_SIZE, device_out: bool = False):
+                    tile_size: int = DEFAULT_TILE_SIZE, device_out: bool = False, method: str = "tiles"):
     """Render B poses at once -> (B, D, D) (float32 device tensor or float64 array).
 
-    Adds the eigenvalue-floor clamp count to CLAMP_EVENTS like the reference.
+    ``method="tiles"`` follows the reference schedule (fp64 bbox, tile lists,
+    tiled forward) and adds the eigenvalue-floor clamp count to CLAMP_EVENTS;
+    ``method="direct"`` uses the binning-free fixed-point render of the
+    training step (no clamp counting).
     """
     import torch
 
@@ -156,13 +159,19 @@ def rasterize_batch(mixture: GaussianMixture, rotations, translations, grid: Gri
     B = poses.shape[0]
     gs = _grid(grid)
     status = torch.zeros(1, dtype=torch.int32, device=ctx.device)
-    clamp = torch.zeros(B, dtype=torch.int32, device=ctx.device)
     splat = engine.prepare(ctx, params, status)
-    binning = engine.bin_full(ctx, params, poses, gs, tile_size, status, clamp=clamp)
     out = torch.empty((B, grid.size, grid.size), dtype=torch.float32, device=ctx.device)
-    engine.raster_fwd(ctx, splat, len(mixture), poses, gs, binning, out)
-    _check_status(status)
-    CLAMP_EVENTS.count += int(clamp.sum().item())
+    if method == "direct":
+        engine.render_direct(ctx, splat, len(mixture), poses, gs, out)
+        _check_status(status)
+    elif method == "tiles":
+        clamp = torch.zeros(B, dtype=torch.int32, device=ctx.device)
+        binning = engine.bin_full(ctx, params, poses, gs, tile_size, status, clamp=clamp)
+        engine.raster_fwd(ctx, splat, len(mixture), poses, gs, binning, out)
+        _check_status(status)
+        CLAMP_EVENTS.count += int(clamp.sum().item())
+    else:
+        raise ValueError(f"unknown method {method!r}")
     return out if device_out else out.double().cpu().numpy()
 
 

@@ -104,7 +104,7 @@ def synthetic_stack(truth: GaussianMixture, rotations, grid: GridSpec, *, defocu
     gs = _lib.grid_struct(grid.size, grid.extent, grid.pixel_size)
     for a in range(0, K, chunk):
         b = min(K, a + chunk)
-        img = rasterize_batch(truth, R[a:b], None, grid, device_out=True)
+        img = rasterize_batch(truth, R[a:b], None, grid, device_out=True, method="direct")
         if ctfs is not None:
             c = torch.as_tensor(ctfs[a:b]).to(ctx.device)
             img = engine.ctf_apply(ctx, img, gs, ctf=c)

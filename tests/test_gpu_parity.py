@@ -121,23 +121,44 @@ def _render(params, poses, grid_o, tile=16):
     return cs.rasterize_batch(mix, Rs, ts, grid, tile_size=tile)
 
 
+@pytest.mark.parametrize("tile", [16, 32])
 @pytest.mark.parametrize("case", ["c1_step", "c2_slice"])
-def test_forward_render_matches_reference(oracle, case):
+def test_forward_render_matches_reference(oracle, case, tile):
     g = load_golden(case)
     grid, params, poses = _stack_inputs(oracle, g)
-    img = _render(params, poses, grid)
+    img = _render(params, poses, grid, tile=tile)
     for i in range(len(poses)):
         assert rel_l2(img[i], g["rendered"][i]) < RENDER_TOL
 
 
-def test_forward_render_full_c1_batch_vs_oracle(oracle):
+@pytest.mark.parametrize("method", ["tiles", "direct"])
+def test_forward_render_full_c1_batch_vs_oracle(oracle, method):
     grid = oracle.Grid(64, 0.5, 1.5)
     params = oracle.init_random(5000, 0, grid)
     poses = [oracle.sample_pose(np.random.default_rng(1000 + i)) for i in range(32)]
-    img = _render(params, poses, grid)
+    mix = cs.GaussianMixture(params)
+    img = cs.rasterize_batch(mix, np.stack([W for W, _ in poses]), np.stack([t for _, t in poses]),
+                             cs.GridSpec(64, 0.5, 1.5), method=method)
     for i, (W, t) in enumerate(poses):
         ref, _ = oracle.rasterize(params, W, t, grid)
         assert rel_l2(img[i], ref) < RENDER_TOL
+
+
+def test_direct_render_kats_and_needles(oracle):
+    k = load_golden("kat")
+    grid = cs.GridSpec(64, 0.5, 3.0)
+    for prm, W, t, ref in [(k["dense_params"], k["dense_W"], k["dense_t"], k["dense_render_tile16"]),
+                           (k["needle_params"], np.eye(3), np.zeros(2), k["needle_render"])]:
+        img = cs.rasterize_batch(cs.GaussianMixture(prm), W[None], t[None], grid, method="direct")[0]
+        assert rel_l2(img, ref) < RENDER_TOL
+        assert np.abs(img - ref).max() <= 1e-4 * ref.max()
+    far = np.zeros((1, 11))
+    far[0, 0] = 5.0
+    far[0, 3:6] = cs.inverse_activate(0.02)
+    far[0, 6] = 1.0
+    far[0, 10] = cs.inverse_activate(1.0)
+    img = cs.rasterize_batch(cs.GaussianMixture(far), np.eye(3)[None], None, grid, method="direct")
+    assert np.all(img == 0.0)
 
 
 @pytest.mark.parametrize("tile", [8, 16, 32])
@@ -260,12 +281,12 @@ def test_ctf_evaluate_and_apply():
         assert rel_l2(out2, c[f"ctf{i}_applied"]) < 1e-5
 
 
-def _full_step_device(params, poses, grid, obs, ctfs):
+def _full_step_device(params, poses, grid, obs, ctfs, render="direct"):
     """Run the engine's fused K0..K5 + epilogue grads for a batch; return (losses, grads)."""
     ctx = engine.DeviceContext.get()
     gs = _lib.grid_struct(grid.size, grid.extent, grid.pixel_size)
     B = len(poses)
-    pipe = engine.StepPipeline(ctx, params.shape[0], B, gs)
+    pipe = engine.StepPipeline(ctx, params.shape[0], B, gs, render=render)
     p = _dev(params, torch.float64)
     P = _dev(engine.pose_array([W for W, _ in poses], [t for _, t in poses]), torch.float64)
     o = _dev(obs, torch.float32)
@@ -276,14 +297,18 @@ def _full_step_device(params, poses, grid, obs, ctfs):
     return pipe.loss.cpu().numpy(), grads.cpu().numpy(), pipe
 
 
+@pytest.mark.parametrize("render", ["direct", "tiles"])
 @pytest.mark.parametrize("case", ["c1_step", "c2_slice"])
-def test_fused_step_matches_reference(oracle, case):
+def test_fused_step_matches_reference(oracle, case, render):
     g = load_golden(case)
     grid, params, poses = _stack_inputs(oracle, g)
     ctfs = None
     if not np.isnan(g["defocus"][0]):
         ctfs = np.stack([oracle.Ctf(d, d).as_array() for d in g["defocus"]])
-    losses, grads, _ = _full_step_device(params, poses, grid, g["observed"], ctfs)
+    losses, grads, pipe = _full_step_device(params, poses, grid, g["observed"], ctfs, render=render)
+    rend = pipe.render.cpu().numpy()
+    for i in range(len(poses)):
+        assert rel_l2(rend[i], g["rendered"][i]) < RENDER_TOL
     np.testing.assert_allclose(losses, g["losses"], rtol=1e-4)
     grads_close(grads, g["grads_mean"], GRAD_TOL, 1e-6)
 
