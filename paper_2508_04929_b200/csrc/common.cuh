@@ -28,6 +28,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Image-independent geometry of one Gaussian, written by cgs_prepare:
 // rec[0..2] mean, rec[3] amp, rec[4..12] M = R diag(s) row-major.
 struct SplatRec {
@@ -163,12 +169,52 @@ __device__ __forceinline__ bool row_span(const Splat2 &s, float dy, int xlo, int
                                          float &dxa) {
     const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
     if (rem <= 0.f) return false;
-    const float half = sqrtf(rem) * s.inv_sqrt_p00;
+    // approximate sqrt: a boundary pixel it might flip carries ~sub of the peak
+    const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
     const float xc = fmaf(-s.slope, dy, s.mpx);
     xa = max((int)ceilf(xc - half), xlo);
     xb = min((int)floorf(xc + half), xhi);
     dxa = (float)xa - xc;
     return xa <= xb;
+}
+
+// float -> nearest int32 on the FMA/ALU pipes (no F2I on the XU pipe):
+// valid for |x| < 2^22; returns round-to-nearest-even(x).
+__device__ __forceinline__ int fast_rint(float x) {
+    return __float_as_int(x + 12582912.0f) - 0x4B400000;
+}
+
+// ---- mbarrier + 1D bulk async copy (TMA engine), CTA scope ----------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, 16B-aligned), completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// order this thread's prior generic-proxy shared accesses before async-proxy writes
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

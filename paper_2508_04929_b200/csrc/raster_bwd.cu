@@ -3,31 +3,182 @@
 // (splat.py:332-349), batched over images.
 //
 // Gaussian-major, one lane per (image, Gaussian), atomic-free.  A CTA owns
-// kGPC Gaussians (one per thread) and a group of images; for each image it
-// stages the upstream gradient in shared memory, and every thread walks its
-// own Gaussian's footprint row by row along the exact q < 6.5^2 span.  Same-
-// size footprints keep the warp's lanes in near lockstep, so no lane sits idle
-// on another lane's rows and no cross-lane reduction is needed.  Per pixel it
-// accumulates moments of ge = g e in pixel units:
-//   per row:   sum ge, sum g, sum ge dx, sum ge dx^2
-//   per image: + dy-weighted row sums -> 7 moments
-// which carry the reference's six raw sums exactly
-//   sA = sum ge - sub sum g,   s_ab = 1/(2 h^2) (sum ge pd_a pd_b - p_ab sA),
-// then converts them, in registers, to the image-summable 10-float world-frame
-// accumulator {cnorm sA, W2^T ac (sx, sy), W2^T (ac S) W2} (SURVEY.md 8(a)
-// row 15) and keeps summing that over the CTA's images.  The CTA writes its
-// image group's partial once; the epilogue sums groups in fixed order, so the
-// gradient is bitwise reproducible.
+// one Gaussian per thread and a group of images; for each image the upstream
+// gradient sits in shared memory and every thread walks its own Gaussian's
+// footprint row by row along the exact q < 6.5^2 span (row-conditional
+// coordinates, common.cuh).  Same-size footprints keep the warp's lanes in
+// near lockstep, so no lane idles on another lane's rows and no cross-lane
+// reduction is needed.  Per pixel it accumulates moments of ge = g e in pixel
+// units (per row: sum ge, sum g, sum ge dx', sum ge dx'^2; per image the
+// dy-weighted row sums), which carry the reference's six raw sums exactly:
+//   sA = sum ge - sub sum g,  s_ab = 1/(2 h^2) (sum ge (Pd)_a (Pd)_b - p_ab sA),
+// with (Pd)_x = p00 dx', (Pd)_y = p01 dx' + k dy.  They are converted in
+// registers to the image-summable 10-float world-frame accumulator
+// {cnorm sA, W2^T ac (sx, sy), W2^T (ac S) W2} and
+// summed over the CTA's images.  The CTA writes its image group's partial
+// once; the epilogue sums groups in a fixed order: bitwise reproducible.
+//
+// Staging: for D <= 160 each CTA double-buffers whole upstream images in
+// shared memory with 1-D bulk async copies (TMA engine, mbarrier completion),
+// so image b+1 streams in while image b is processed; larger D falls back to
+// synchronous row bands.
 #include "common.cuh"
 
 namespace cgs {
 
-constexpr int kBwdThreads = 256;
-constexpr int kGPC = kBwdThreads;        // Gaussians per CTA, one per thread
+constexpr int kBwdThreadsDB = 512;       // double-buffered kernel: Gaussians per CTA
+constexpr int kBwdThreadsBand = 256;     // band kernel
 constexpr int kBandBytes = 96 * 1024;    // upstream rows staged per band
+constexpr int kDBMaxBytes = 200 * 1024;  // two whole images must fit
 
-__device__ __forceinline__ void stage_rows(float *__restrict__ img, const float *__restrict__ up,
-                                           int b, int D, int r0, int r1, int layout) {
+struct Moments {
+    float e, g, x, y, xx, xy, yy;
+};
+
+// Walk rows [ya, yb] of one footprint over upstream rows stored from row r0.
+__device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, int D, int ya, int yb,
+                                         const Splat2 &s, float c2A, Moments &M) {
+    for (int iy = ya; iy <= yb; ++iy) {
+        const float dy = (float)iy - s.mpy;
+        int xa, xb;
+        float dx;
+        if (!row_span(s, dy, 0, D - 1, xa, xb, dx)) continue;
+        const float *row = img + (iy - r0) * D;
+        float rE = 0.f, rG = 0.f, rX = 0.f, rXX = 0.f;
+        // e = 2^(A dx'^2 + Ck dy^2) by the recurrence e_{k+1} = e_k g_k,
+        // g_{k+1} = g_k c (c = 2^(2A)), restarted from an exact exp every 32
+        // pixels (relative error < 2e-5 at the row's peak)
+        for (int x0 = xa; x0 <= xb; x0 += 32) {
+            float e = ex2_approx(fmaf(s.A * dx, dx, s.Ck * dy * dy));
+            float gg = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
+            const int xe = min(xb, x0 + 31);
+#pragma unroll 4
+            for (int x = x0; x <= xe; ++x) {
+                const float gp = row[x];
+                const float ge = gp * e;
+                rE += ge;
+                rG += gp;
+                const float t = ge * dx;
+                rX += t;
+                rXX = fmaf(t, dx, rXX);
+                e *= gg;
+                gg *= c2A;
+                dx += 1.f;
+            }
+        }
+        M.xx += rXX;
+        M.e += rE;
+        M.g += rG;
+        M.x += rX;
+        M.y = fmaf(dy, rE, M.y);
+        M.xy = fmaf(dy, rX, M.xy);
+        M.yy = fmaf(dy * dy, rE, M.yy);
+    }
+}
+
+// moments of one (image, Gaussian) -> += world-frame accumulator
+__device__ __forceinline__ void accumulate_world(const Moments &M, const Splat2 &s, const PoseF &P, float inv_h,
+                                                 float acc[CGS_ACC_STRIDE]) {
+    const float ih2 = 0.5f * inv_h * inv_h;
+    const float p00 = s.p00, p01 = s.p01, p11 = s.p11, k = s.k;
+    const float sA = M.e - kSub * M.g;
+    const float sx = (p00 * M.x) * inv_h;
+    const float sy = (p01 * M.x + k * M.y) * inv_h;
+    const float Sxx = p00 * p00 * M.xx;
+    const float Sxy = p00 * (p01 * M.xx + k * M.xy);
+    const float Syy = p01 * p01 * M.xx + 2.f * p01 * k * M.xy + k * k * M.yy;
+    const float ac = s.w;
+    const float S00 = ac * ih2 * (Sxx - p00 * sA);
+    const float S01 = ac * ih2 * (Sxy - p01 * sA);
+    const float S11 = ac * ih2 * (Syy - p11 * sA);
+    const float d0 = ac * sx, d1 = ac * sy;
+    acc[0] += s.cnorm * sA;
+    acc[1] += d0 * P.w0[0] + d1 * P.w1[0];
+    acc[2] += d0 * P.w0[1] + d1 * P.w1[1];
+    acc[3] += d0 * P.w0[2] + d1 * P.w1[2];
+    // P3_kl = sum_ab W_ak S_ab W_bl, (k,l) in xx xy xz yy yz zz
+    const float u0 = S00 * P.w0[0] + S01 * P.w1[0], v0 = S01 * P.w0[0] + S11 * P.w1[0];
+    const float u1 = S00 * P.w0[1] + S01 * P.w1[1], v1 = S01 * P.w0[1] + S11 * P.w1[1];
+    const float u2 = S00 * P.w0[2] + S01 * P.w1[2], v2 = S01 * P.w0[2] + S11 * P.w1[2];
+    acc[4] += u0 * P.w0[0] + v0 * P.w1[0];
+    acc[5] += u0 * P.w0[1] + v0 * P.w1[1];
+    acc[6] += u0 * P.w0[2] + v0 * P.w1[2];
+    acc[7] += u1 * P.w0[1] + v1 * P.w1[1];
+    acc[8] += u1 * P.w0[2] + v1 * P.w1[2];
+    acc[9] += u2 * P.w0[2] + v2 * P.w1[2];
+}
+
+__device__ __forceinline__ void footprint_rows(const Splat2 &s, int D, int &ylo, int &yhi) {
+    ylo = 1;
+    yhi = 0;
+    if (s.w > 0.f) {
+        ylo = max((int)ceilf(s.mpy - s.hy), 0);
+        yhi = min((int)floorf(s.mpy + s.hy), D - 1);
+    }
+}
+
+__device__ __forceinline__ void store_partial(float *__restrict__ partial, int grp, int64_t n, int64_t g,
+                                              const float acc[CGS_ACC_STRIDE]) {
+    float *dst = partial + ((int64_t)grp * n + g) * CGS_ACC_STRIDE;
+#pragma unroll
+    for (int c = 0; c < CGS_ACC_STRIDE; ++c) dst[c] = acc[c];
+}
+
+// Whole-image double buffering: natural layout only, D*D*4 bytes per buffer.
+__global__ void __launch_bounds__(kBwdThreadsDB, 1) raster_bwd_db_kernel(
+    const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
+    const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
+    extern __shared__ __align__(128) float smem_db[];
+    __shared__ __align__(8) uint64_t bars[2];
+    const int D = G.D;
+    const uint32_t img_bytes = (uint32_t)D * D * sizeof(float);
+    const int64_t g = (int64_t)blockIdx.x * kBwdThreadsDB + threadIdx.x;
+    const bool valid = g < n;
+    const int grp = blockIdx.y;
+    const int b_begin = grp * ipg, b_end = min(B, b_begin + ipg);
+    const int nimg = b_end - b_begin;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 2 && i < nimg; ++i) {
+            mbar_expect_tx(&bars[i], img_bytes);
+            bulk_g2s(smem_db + i * D * D, upstream + (int64_t)(b_begin + i) * D * D, img_bytes, &bars[i]);
+        }
+    }
+    __syncthreads();
+    SplatRec rec{};
+    if (valid) rec = load_splat(splat, g);
+    float acc[CGS_ACC_STRIDE];
+#pragma unroll
+    for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = 0.f;
+
+    for (int i = 0; i < nimg; ++i) {
+        const int b = b_begin + i;
+        const PoseF P = load_pose_f(poses, b);
+        Splat2 s{};
+        int ylo = 1, yhi = 0;
+        if (valid) {
+            s = project2(rec, P, G);
+            footprint_rows(s, D, ylo, yhi);
+        }
+        const float c2A = exp2f(2.f * s.A);
+        mbar_wait(&bars[i & 1], (uint32_t)((i >> 1) & 1));
+        Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        bwd_rows(smem_db + (i & 1) * D * D, 0, D, ylo, yhi, s, c2A, M);
+        if (ylo <= yhi) accumulate_world(M, s, P, G.inv_h, acc);
+        __syncthreads();  // every thread is done reading buf[i & 1]
+        if (threadIdx.x == 0 && i + 2 < nimg) {
+            fence_proxy_async_smem();
+            mbar_expect_tx(&bars[i & 1], img_bytes);
+            bulk_g2s(smem_db + (i & 1) * D * D, upstream + (int64_t)(b + 2) * D * D, img_bytes, &bars[i & 1]);
+        }
+    }
+    if (valid) store_partial(partial, grp, n, g, acc);
+}
+
+__device__ __forceinline__ void stage_rows(float *__restrict__ img, const float *__restrict__ up, int b, int D,
+                                           int r0, int r1, int layout) {
     const float *src = up + (int64_t)b * D * D;
     const int total = (r1 - r0) * D;
     if (layout == CGS_LAYOUT_NATURAL && (D & 3) == 0) {
@@ -48,29 +199,13 @@ __device__ __forceinline__ void stage_rows(float *__restrict__ img, const float 
     }
 }
 
-struct Moments {
-    float e, g, x, y, xx, xy, yy;
-};
-
-// one pixel of the row walk in row-conditional coordinates (common.cuh):
-// e = 2^l, l = A dx'^2 + Ck dy^2
-__device__ __forceinline__ void bwd_pixel(float gp, float dx, float A, float Ckdy2,
-                                          float &rE, float &rG, float &rX, float &rXX) {
-    const float e = ex2_approx(fmaf(A * dx, dx, Ckdy2));
-    const float ge = gp * e;
-    rE += ge;
-    rG += gp;
-    const float t = ge * dx;
-    rX += t;
-    rXX = fmaf(t, dx, rXX);
-}
-
-__global__ void __launch_bounds__(kBwdThreads, 2) raster_bwd_kernel(
+// Synchronous row bands: any D, either layout.
+__global__ void __launch_bounds__(kBwdThreadsBand, 3) raster_bwd_band_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, int layout, float *__restrict__ partial, int ipg, int HB) {
     extern __shared__ float img[];
     const int D = G.D;
-    const int64_t g = (int64_t)blockIdx.x * kGPC + threadIdx.x;
+    const int64_t g = (int64_t)blockIdx.x * kBwdThreadsBand + threadIdx.x;
     const bool valid = g < n;
     const int grp = blockIdx.y;
     const int b_begin = grp * ipg, b_end = min(B, b_begin + ipg);
@@ -79,91 +214,26 @@ __global__ void __launch_bounds__(kBwdThreads, 2) raster_bwd_kernel(
     float acc[CGS_ACC_STRIDE];
 #pragma unroll
     for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = 0.f;
-
     for (int b = b_begin; b < b_end; ++b) {
         const PoseF P = load_pose_f(poses, b);
         Splat2 s{};
         int ylo = 1, yhi = 0;
         if (valid) {
             s = project2(rec, P, G);
-            if (s.w > 0.f) {
-                ylo = max((int)ceilf(s.mpy - s.hy), 0);
-                yhi = min((int)floorf(s.mpy + s.hy), D - 1);
-            }
+            footprint_rows(s, D, ylo, yhi);
         }
+        const float c2A = exp2f(2.f * s.A);
         Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int r0 = 0; r0 < D; r0 += HB) {
             const int r1 = min(D, r0 + HB);
             __syncthreads();
             stage_rows(img, upstream, b, D, r0, r1, layout);
             __syncthreads();
-            const int ya = max(ylo, r0), yb = min(yhi, r1 - 1);
-            for (int iy = ya; iy <= yb; ++iy) {
-                const float dy = (float)iy - s.mpy;
-                int xa, xb;
-                float dx;
-                if (!row_span(s, dy, 0, D - 1, xa, xb, dx)) continue;
-                const float Ckdy2 = s.Ck * dy * dy;
-                const float *row = img + (iy - r0) * D;
-                float rE = 0.f, rG = 0.f, rX = 0.f, rXX = 0.f, rE2 = 0.f, rG2 = 0.f, rX2 = 0.f, rXX2 = 0.f;
-                int x = xa;
-                for (; x < xb; x += 2) {  // two independent chains per iteration
-                    bwd_pixel(row[x], dx, s.A, Ckdy2, rE, rG, rX, rXX);
-                    bwd_pixel(row[x + 1], dx + 1.f, s.A, Ckdy2, rE2, rG2, rX2, rXX2);
-                    dx += 2.f;
-                }
-                if (x == xb) bwd_pixel(row[x], dx, s.A, Ckdy2, rE, rG, rX, rXX);
-                M.xx += rXX + rXX2;
-                rE += rE2;
-                rG += rG2;
-                rX += rX2;
-                M.e += rE;
-                M.g += rG;
-                M.x += rX;
-                M.y = fmaf(dy, rE, M.y);
-                M.xy = fmaf(dy, rX, M.xy);
-                M.yy = fmaf(dy * dy, rE, M.yy);
-            }
+            bwd_rows(img, r0, D, max(ylo, r0), min(yhi, r1 - 1), s, c2A, M);
         }
-        if (ylo <= yhi) {
-            // moments -> the reference's raw sums (normalised units), then the
-            // world-frame accumulator for this image
-            const float ih2 = 0.5f * G.inv_h * G.inv_h;
-            const float p00 = s.p00, p01 = s.p01, p11 = s.p11;
-            // row-conditional moments: (P d)_x = p00 dx', (P d)_y = p01 dx' + k dy
-            const float k = s.k;
-            const float sA = M.e - kSub * M.g;
-            const float sx = (p00 * M.x) * G.inv_h;
-            const float sy = (p01 * M.x + k * M.y) * G.inv_h;
-            const float Sxx = p00 * p00 * M.xx;
-            const float Sxy = p00 * (p01 * M.xx + k * M.xy);
-            const float Syy = p01 * p01 * M.xx + 2.f * p01 * k * M.xy + k * k * M.yy;
-            const float ac = s.w;
-            const float S00 = ac * ih2 * (Sxx - p00 * sA);
-            const float S01 = ac * ih2 * (Sxy - p01 * sA);
-            const float S11 = ac * ih2 * (Syy - p11 * sA);
-            const float d0 = ac * sx, d1 = ac * sy;
-            acc[0] += s.cnorm * sA;
-            acc[1] += d0 * P.w0[0] + d1 * P.w1[0];
-            acc[2] += d0 * P.w0[1] + d1 * P.w1[1];
-            acc[3] += d0 * P.w0[2] + d1 * P.w1[2];
-            // P3_kl = sum_ab W_ak S_ab W_bl, (k,l) in xx xy xz yy yz zz
-            const float u0 = S00 * P.w0[0] + S01 * P.w1[0], v0 = S01 * P.w0[0] + S11 * P.w1[0];
-            const float u1 = S00 * P.w0[1] + S01 * P.w1[1], v1 = S01 * P.w0[1] + S11 * P.w1[1];
-            const float u2 = S00 * P.w0[2] + S01 * P.w1[2], v2 = S01 * P.w0[2] + S11 * P.w1[2];
-            acc[4] += u0 * P.w0[0] + v0 * P.w1[0];
-            acc[5] += u0 * P.w0[1] + v0 * P.w1[1];
-            acc[6] += u0 * P.w0[2] + v0 * P.w1[2];
-            acc[7] += u1 * P.w0[1] + v1 * P.w1[1];
-            acc[8] += u1 * P.w0[2] + v1 * P.w1[2];
-            acc[9] += u2 * P.w0[2] + v2 * P.w1[2];
-        }
+        if (ylo <= yhi) accumulate_world(M, s, P, G.inv_h, acc);
     }
-    if (valid) {
-        float *dst = partial + ((int64_t)grp * n + g) * CGS_ACC_STRIDE;
-#pragma unroll
-        for (int c = 0; c < CGS_ACC_STRIDE; ++c) dst[c] = acc[c];
-    }
+    if (valid) store_partial(partial, grp, n, g, acc);
 }
 
 // In-ellipse pair count per image (same row spans as the backward).
@@ -177,13 +247,12 @@ __global__ void __launch_bounds__(256) count_pairs_kernel(const float *__restric
         const PoseF P = load_pose_f(poses, b);
         Splat2 s = project2(load_splat(splat, g), P, G);
         const int D = G.D;
-        int ylo = max((int)ceilf(s.mpy - s.hy), 0), yhi = min((int)floorf(s.mpy + s.hy), D - 1);
-        if (s.w > 0.f) {
-            for (int iy = ylo; iy <= yhi; ++iy) {
-                int xa, xb;
-                float dx;
-                if (row_span(s, (float)iy - s.mpy, 0, D - 1, xa, xb, dx)) cnt += xb - xa + 1;
-            }
+        int ylo, yhi;
+        footprint_rows(s, D, ylo, yhi);
+        for (int iy = ylo; iy <= yhi; ++iy) {
+            int xa, xb;
+            float dx;
+            if (row_span(s, (float)iy - s.mpy, 0, D - 1, xa, xb, dx)) cnt += xb - xa + 1;
         }
     }
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -206,20 +275,34 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
         !upstream || !partial)
         return CGS_ERR_ARG;
     const int D = grid.size;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t G = cgs_bwd_groups(B, images_per_group);
+    const size_t db_bytes = 2 * (size_t)D * D * sizeof(float);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(upstream) & 15) == 0) && ((D * D) % 4 == 0);
+    if (layout == CGS_LAYOUT_NATURAL && db_bytes <= (size_t)kDBMaxBytes && aligned) {
+        static size_t configured = 0;
+        if (db_bytes > 48 * 1024 && db_bytes > configured) {
+            cudaFuncSetAttribute(raster_bwd_db_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)db_bytes);
+            configured = db_bytes;
+        }
+        dim3 g((unsigned)((n + kBwdThreadsDB - 1) / kBwdThreadsDB), (unsigned)G);
+        raster_bwd_db_kernel<<<g, kBwdThreadsDB, db_bytes, st>>>(splat, n, poses, B, make_grid_f(grid), upstream,
+                                                                 partial, images_per_group);
+        return check_launch("raster_bwd_db_kernel");
+    }
     int HB = kBandBytes / (D * (int)sizeof(float));
     if (HB < 1) return CGS_ERR_UNSUPPORTED;
     HB = HB > D ? D : HB;
-    size_t smem = (size_t)HB * D * sizeof(float);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
+    const size_t smem = (size_t)HB * D * sizeof(float);
+    static size_t configured_band = 0;
+    if (smem > 48 * 1024 && smem > configured_band) {
+        cudaFuncSetAttribute(raster_bwd_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured_band = smem;
     }
-    int64_t G = cgs_bwd_groups(B, images_per_group);
-    dim3 g((unsigned)((n + kGPC - 1) / kGPC), (unsigned)G);
-    raster_bwd_kernel<<<g, kBwdThreads, smem, (cudaStream_t)stream>>>(
-        splat, n, poses, B, make_grid_f(grid), upstream, layout, partial, images_per_group, HB);
-    return check_launch("raster_bwd_kernel");
+    dim3 g((unsigned)((n + kBwdThreadsBand - 1) / kBwdThreadsBand), (unsigned)G);
+    raster_bwd_band_kernel<<<g, kBwdThreadsBand, smem, st>>>(splat, n, poses, B, make_grid_f(grid), upstream, layout,
+                                                             partial, images_per_group, HB);
+    return check_launch("raster_bwd_band_kernel");
 }
 
 extern "C" int cgs_count_pairs(const float *splat, int64_t n, const double *poses, int32_t B,

@@ -22,8 +22,9 @@
 // w = amp / (2 pi sqrt(det)) <= amp / (2 pi sqrt(that)).
 //
 // Along a row, e = exp(-q/2) follows e_{k+1} = e_k g_k, g_{k+1} = g_k c with
-// c = 2^(2A): two FMULs per pixel instead of an MUFU.EX2, restarted every 16
-// pixels so the recurrence error stays below 1e-5.
+// c = 2^(2A): two FMULs per pixel instead of an MUFU.EX2, restarted every 32
+// pixels so the recurrence error stays below 2e-5.  Rounding to int uses the
+// FMA-pipe magic-number trick (common.cuh fast_rint) instead of F2I on the XU.
 #include <cmath>
 
 #include "common.cuh"
@@ -35,6 +36,7 @@ constexpr int kRChunk = 4096;              // Gaussians per CTA
 constexpr int kRBandBytes = 64 * 1024;     // int32 accumulator rows per CTA
 constexpr int kWbBlock = 1024;
 constexpr float kFixedRange = 1073741824.f;  // 2^30
+constexpr float kContribRange = 4194304.f;   // 2^22
 
 __global__ void __launch_bounds__(kWbBlock) wbound_partial_kernel(const float *__restrict__ splat, int64_t n,
                                                                   double h, float *__restrict__ part) {
@@ -50,29 +52,58 @@ __global__ void __launch_bounds__(kWbBlock) wbound_partial_kernel(const float *_
         // 1.001: headroom for the fp32 evaluation of w inside the kernels
         wb = (float)(1.001 * amp / (2.0 * kPiD * sqrt(det)));
     }
-    __shared__ float ws[kWbBlock / 32];
-    float v = warp_sum(wb);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __shared__ float ws[kWbBlock / 32], wm[kWbBlock / 32];
+    float v = warp_sum(wb), m = wb;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) {
+        ws[threadIdx.x >> 5] = v;
+        wm[threadIdx.x >> 5] = m;
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
-        float t = warp_sum(ws[threadIdx.x]);
-        if (threadIdx.x == 0) part[blockIdx.x] = t;
+        float t = warp_sum(ws[threadIdx.x]), mm = wm[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+        if (threadIdx.x == 0) {
+            part[blockIdx.x] = t;
+            part[gridDim.x + blockIdx.x] = mm;
+        }
     }
 }
 
-// scale = 2^30 / sum(part), written to part[nparts]; fixed-order reduction
+// scale = min(2^30 / sum wb, 2^22 / max wb) -> part[2 nparts]; fixed-order
+// reduction.  The first bound keeps every pixel sum below 2^30; the second
+// keeps every single contribution below 2^22, where fast_rint is exact.
 __global__ void __launch_bounds__(256) wbound_scale_kernel(float *part, int nparts) {
     __shared__ double ws[8];
+    __shared__ float wm[8];
     double t = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += 256) t += part[i];
+    float m = 0.f;
+    for (int i = threadIdx.x; i < nparts; i += 256) {
+        t += part[i];
+        m = fmaxf(m, part[nparts + i]);
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
+    for (int o = 16; o > 0; o >>= 1) {
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        ws[threadIdx.x >> 5] = t;
+        wm[threadIdx.x >> 5] = m;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         double s = 0.0;
-        for (int w = 0; w < 8; ++w) s += ws[w];
-        part[nparts] = s > 0.0 ? (float)((double)kFixedRange / s) : 1.f;
+        float mx = 0.f;
+        for (int w = 0; w < 8; ++w) {
+            s += ws[w];
+            mx = fmaxf(mx, wm[w]);
+        }
+        double sc = s > 0.0 ? (double)kFixedRange / s : 1.0;
+        if (mx > 0.f) sc = fmin(sc, (double)kContribRange / mx);
+        part[2 * nparts] = (float)sc;
     }
 }
 
@@ -104,17 +135,18 @@ __global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
             if (!row_span(s, dy, 0, D - 1, xa, xb, dx)) continue;
             const float Ckdy2 = s.Ck * dy * dy;
             int *row = band + (iy - r0) * D;
-            for (int x0 = xa; x0 <= xb; x0 += 16) {
-                // restart the recurrence from an exact exp every 16 pixels
+            for (int x0 = xa; x0 <= xb; x0 += 32) {
+                // restart the recurrence from an exact exp every 32 pixels
                 float e = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
                 float gg = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
-                const int xe = min(xb, x0 + 15);
+                const int xe = min(xb, x0 + 31);
+#pragma unroll 4
                 for (int x = x0; x <= xe; ++x) {
-                    atomicAdd(row + x, __float2int_rn(fmaf(wS, e, -wsubS)));
+                    atomicAdd(row + x, fast_rint(fmaf(wS, e, -wsubS)));
                     e *= gg;
                     gg *= c;
                 }
-                dx += 16.f;
+                dx += 32.f;
             }
         }
     }
@@ -145,7 +177,7 @@ using namespace cgs;
 
 extern "C" size_t cgs_render_workspace_bytes(int64_t n) {
     int64_t parts = (n + kWbBlock - 1) / kWbBlock;
-    return (size_t)(parts + 1) * sizeof(float);
+    return (size_t)(2 * parts + 1) * sizeof(float);
 }
 
 extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
@@ -171,12 +203,12 @@ extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, in
     const int64_t count = (int64_t)B * D * D;
     cudaMemsetAsync(out, 0, sizeof(int) * count, st);
     dim3 g((unsigned)((n + kRChunk - 1) / kRChunk), (unsigned)B, (unsigned)bands);
-    raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), part + parts, HB,
+    raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), part + 2 * parts, HB,
                                                          reinterpret_cast<int *>(out));
     int rc = check_launch("raster_fwd_atomic_kernel");
     if (rc) return rc;
     const int64_t threads = (count + 3) / 4;
     fixed_to_float_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(reinterpret_cast<int *>(out), count,
-                                                                           part + parts);
+                                                                           part + 2 * parts);
     return check_launch("fixed_to_float_kernel");
 }
