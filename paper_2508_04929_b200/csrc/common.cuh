@@ -178,6 +178,36 @@ __device__ __forceinline__ bool row_span(const Splat2 &s, float dy, int xlo, int
     return xa <= xb;
 }
 
+// ---- packed f32x2 arithmetic (sm_100a FFMA2 / FMUL2 / FADD2) --------------
+// One instruction updates two fp32 lanes: same FMA-pipe throughput as two
+// FFMAs but half the issue slots (profiles/microbench_ffma2_r01.txt), which
+// is what the issue-bound pixel loops need.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 // float -> nearest int32 on the FMA/ALU pipes (no F2I on the XU pipe):
 // valid for |x| < 2^22; returns round-to-nearest-even(x).
 __device__ __forceinline__ int fast_rint(float x) {

@@ -38,34 +38,61 @@ struct Moments {
 // Walk rows [ya, yb] of one footprint over upstream rows stored from row r0.
 __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, int D, int ya, int yb,
                                          const Splat2 &s, float c2A, Moments &M) {
-    for (int iy = ya; iy <= yb; ++iy) {
-        const float dy = (float)iy - s.mpy;
-        int xa, xb;
-        float dx;
-        if (!row_span(s, dy, 0, D - 1, xa, xb, dx)) continue;
-        const float *row = img + (iy - r0) * D;
-        float rE = 0.f, rG = 0.f, rX = 0.f, rXX = 0.f;
-        // e = 2^(A dx'^2 + Ck dy^2) by the recurrence e_{k+1} = e_k g_k,
-        // g_{k+1} = g_k c (c = 2^(2A)), restarted from an exact exp every 32
-        // pixels (relative error < 2e-5 at the row's peak)
+    // e = 2^(A dx'^2 + Ck dy^2) along a row by the recurrence e_{k+1} = e_k g_k,
+    // g_{k+1} = g_k c (c = 2^(2A)), two pixels per packed f32x2 step:
+    // (e_k, e_k+1) *= (g_k g_k+1, g_k+1 g_k+2), that pair *= c^4.  Restarted
+    // from an exact exp every 32 pixels (relative error < 2e-5 at the peak).
+    const float c = c2A, c4 = (c * c) * (c * c);
+    const uint64_t C4 = f2pack(c4, c4), TWO = f2pack(2.f, 2.f);
+    float dy = (float)ya - s.mpy;
+    float xcv = fmaf(-s.slope, dy, s.mpx);
+    const float *row = img + (ya - r0) * D;
+    for (int iy = ya; iy <= yb; ++iy, dy += 1.f, xcv -= s.slope, row += D) {
+        const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
+        if (rem <= 0.f) continue;
+        const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
+        const int xa = max((int)ceilf(xcv - half), 0);
+        const int xb = min((int)floorf(xcv + half), D - 1);
+        if (xa > xb) continue;
+        float dx = (float)xa - xcv;
+        const float Ckdy2 = s.Ck * dy * dy;
+        uint64_t aE = 0, aG = 0, aX = 0, aXX = 0;  // packed (0.f, 0.f)
+        float tE = 0.f, tG = 0.f, tX = 0.f, tXX = 0.f;
         for (int x0 = xa; x0 <= xb; x0 += 32) {
-            float e = ex2_approx(fmaf(s.A * dx, dx, s.Ck * dy * dy));
-            float gg = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
+            const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
+            const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
+            const float g1 = g0 * c;
+            uint64_t E = f2pack(e0, e0 * g0);
+            uint64_t R = f2pack(g0 * g1, g1 * g1 * c);
+            uint64_t DX = f2pack(dx, dx + 1.f);
             const int xe = min(xb, x0 + 31);
-#pragma unroll 4
-            for (int x = x0; x <= xe; ++x) {
-                const float gp = row[x];
-                const float ge = gp * e;
-                rE += ge;
-                rG += gp;
-                const float t = ge * dx;
-                rX += t;
-                rXX = fmaf(t, dx, rXX);
-                e *= gg;
-                gg *= c2A;
-                dx += 1.f;
+            int x = x0;
+#pragma unroll 2
+            for (; x < xe; x += 2) {
+                const uint64_t GP = f2pack(row[x], row[x + 1]);
+                const uint64_t GE = f2mul(GP, E);
+                aE = f2add(aE, GE);
+                aG = f2add(aG, GP);
+                const uint64_t T = f2mul(GE, DX);
+                aX = f2add(aX, T);
+                aXX = f2fma(T, DX, aXX);
+                E = f2mul(E, R);
+                R = f2mul(R, C4);
+                DX = f2add(DX, TWO);
             }
+            if (x == xe) {  // odd tail pixel
+                const float e = f2unpack(E).x, d = f2unpack(DX).x, gp = row[x];
+                const float ge = gp * e, t = ge * d;
+                tE += ge;
+                tG += gp;
+                tX += t;
+                tXX = fmaf(t, d, tXX);
+            }
+            dx += 32.f;
         }
+        const float2 vE = f2unpack(aE), vG = f2unpack(aG), vX = f2unpack(aX), vXX = f2unpack(aXX);
+        const float rE = vE.x + vE.y + tE, rG = vG.x + vG.y + tG, rX = vX.x + vX.y + tX;
+        const float rXX = vXX.x + vXX.y + tXX;
         M.xx += rXX;
         M.e += rE;
         M.g += rG;

@@ -128,24 +128,42 @@ __global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
         const int yhi = min(min((int)floorf(s.mpy + s.hy), D - 1), r1 - 1);
         const float wS = s.w * scale, wsubS = s.w * kSub * scale;
         const float c = exp2f(2.f * s.A);  // g_{k+1} / g_k
-        for (int iy = ylo; iy <= yhi; ++iy) {
-            const float dy = (float)iy - s.mpy;
-            int xa, xb;
-            float dx;
-            if (!row_span(s, dy, 0, D - 1, xa, xb, dx)) continue;
+        const float c4 = (c * c) * (c * c);
+        // v = wS e - wS sub + 1.5*2^23: the FFMA that evaluates the contribution
+        // also places its rounded integer in the low mantissa bits (fast_rint)
+        const uint64_t WS = f2pack(wS, wS), BIAS = f2pack(12582912.0f - wsubS, 12582912.0f - wsubS);
+        const uint64_t C4 = f2pack(c4, c4);
+        float dy = (float)ylo - s.mpy;
+        float xcv = fmaf(-s.slope, dy, s.mpx);
+        int *row = band + (ylo - r0) * D;
+        for (int iy = ylo; iy <= yhi; ++iy, dy += 1.f, xcv -= s.slope, row += D) {
+            const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
+            if (rem <= 0.f) continue;
+            const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
+            const int xa = max((int)ceilf(xcv - half), 0);
+            const int xb = min((int)floorf(xcv + half), D - 1);
+            if (xa > xb) continue;
+            float dx = (float)xa - xcv;
             const float Ckdy2 = s.Ck * dy * dy;
-            int *row = band + (iy - r0) * D;
             for (int x0 = xa; x0 <= xb; x0 += 32) {
-                // restart the recurrence from an exact exp every 32 pixels
-                float e = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
-                float gg = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
+                // restart the recurrence from an exact exp every 32 pixels;
+                // two pixels per packed step (see raster_bwd.cu bwd_rows)
+                const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
+                const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
+                const float g1 = g0 * c;
+                uint64_t E = f2pack(e0, e0 * g0);
+                uint64_t R = f2pack(g0 * g1, g1 * g1 * c);
                 const int xe = min(xb, x0 + 31);
-#pragma unroll 4
-                for (int x = x0; x <= xe; ++x) {
-                    atomicAdd(row + x, fast_rint(fmaf(wS, e, -wsubS)));
-                    e *= gg;
-                    gg *= c;
+                int x = x0;
+#pragma unroll 2
+                for (; x < xe; x += 2) {
+                    const float2 v = f2unpack(f2fma(WS, E, BIAS));
+                    atomicAdd(row + x, __float_as_int(v.x) - 0x4B400000);
+                    atomicAdd(row + x + 1, __float_as_int(v.y) - 0x4B400000);
+                    E = f2mul(E, R);
+                    R = f2mul(R, C4);
                 }
+                if (x == xe) atomicAdd(row + x, fast_rint(fmaf(wS, f2unpack(E).x, -wsubS)));
                 dx += 32.f;
             }
         }
