@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcgs_b200.so")
+# CGS_B200_LIB selects an alternative in-tree build (kernel A/B experiments)
+LIB_PATH = os.environ.get("CGS_B200_LIB") or os.path.join(_HERE, "libcgs_b200.so")
 
 CGS_OK = 0
 CGS_LAYOUT_NATURAL = 0

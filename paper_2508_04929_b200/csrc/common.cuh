@@ -207,6 +207,20 @@ __device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
+// in-place forms keep accumulators in their register pair (no MOV shuffles)
+__device__ __forceinline__ void f2acc_add(uint64_t &acc, uint64_t a) {
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(a));
+}
+__device__ __forceinline__ void f2acc_fma(uint64_t &acc, uint64_t a, uint64_t b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void f2scale(uint64_t &a, uint64_t b) {
+    asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(b));
+}
+__device__ __forceinline__ float f2sum(uint64_t v) {
+    const float2 p = f2unpack(v);
+    return p.x + p.y;
+}
 
 // float -> nearest int32 on the FMA/ALU pipes (no F2I on the XU pipe):
 // valid for |x| < 2^22; returns round-to-nearest-even(x).

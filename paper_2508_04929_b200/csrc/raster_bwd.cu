@@ -35,13 +35,29 @@ struct Moments {
     float e, g, x, y, xx, xy, yy;
 };
 
+// One pixel pair (or a single pixel when GP's high lane is 0) of a row walk:
+// packed per-row sums of ge, g, ge dx', ge dx'^2.
+struct RowSums {
+    uint64_t e = 0, g = 0, x = 0, xx = 0;  // (0.f, 0.f)
+};
+
+__device__ __forceinline__ void bwd_pair(RowSums &a, uint64_t GP, uint64_t E, uint64_t DX) {
+    const uint64_t GE = f2mul(GP, E);
+    f2acc_add(a.e, GE);
+    f2acc_add(a.g, GP);
+    const uint64_t T = f2mul(GE, DX);
+    f2acc_add(a.x, T);
+    f2acc_fma(a.xx, T, DX);
+}
+
 // Walk rows [ya, yb] of one footprint over upstream rows stored from row r0.
+// e = 2^(A dx'^2 + Ck dy^2) along a row by the recurrence e_{k+1} = e_k g_k,
+// g_{k+1} = g_k c (c = 2^(2A)), two pixels per packed f32x2 step:
+// (e_k, e_k+1) *= (g_k g_k+1, g_k+1 g_k+2), that pair *= c^4 (relative error
+// < 2e-5 over 32 pixels).  Rows longer than 32 pixels take an exact exp per
+// pixel instead.
 __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, int D, int ya, int yb,
                                          const Splat2 &s, float c2A, Moments &M) {
-    // e = 2^(A dx'^2 + Ck dy^2) along a row by the recurrence e_{k+1} = e_k g_k,
-    // g_{k+1} = g_k c (c = 2^(2A)), two pixels per packed f32x2 step:
-    // (e_k, e_k+1) *= (g_k g_k+1, g_k+1 g_k+2), that pair *= c^4.  Restarted
-    // from an exact exp every 32 pixels (relative error < 2e-5 at the peak).
     const float c = c2A, c4 = (c * c) * (c * c);
     const uint64_t C4 = f2pack(c4, c4), TWO = f2pack(2.f, 2.f);
     float dy = (float)ya - s.mpy;
@@ -54,49 +70,34 @@ __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, 
         const int xa = max((int)ceilf(xcv - half), 0);
         const int xb = min((int)floorf(xcv + half), D - 1);
         if (xa > xb) continue;
-        float dx = (float)xa - xcv;
+        const float dx = (float)xa - xcv;
         const float Ckdy2 = s.Ck * dy * dy;
-        uint64_t aE = 0, aG = 0, aX = 0, aXX = 0;  // packed (0.f, 0.f)
-        float tE = 0.f, tG = 0.f, tX = 0.f, tXX = 0.f;
-        for (int x0 = xa; x0 <= xb; x0 += 32) {
+        RowSums a;
+        if (xb - xa < 32) {
             const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
             const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
             const float g1 = g0 * c;
             uint64_t E = f2pack(e0, e0 * g0);
             uint64_t R = f2pack(g0 * g1, g1 * g1 * c);
             uint64_t DX = f2pack(dx, dx + 1.f);
-            const int xe = min(xb, x0 + 31);
-            int x = x0;
-#pragma unroll 2
-            for (; x < xe; x += 2) {
-                const uint64_t GP = f2pack(row[x], row[x + 1]);
-                const uint64_t GE = f2mul(GP, E);
-                aE = f2add(aE, GE);
-                aG = f2add(aG, GP);
-                const uint64_t T = f2mul(GE, DX);
-                aX = f2add(aX, T);
-                aXX = f2fma(T, DX, aXX);
-                E = f2mul(E, R);
-                R = f2mul(R, C4);
-                DX = f2add(DX, TWO);
+            int x = xa;
+            for (; x < xb; x += 2) {
+                bwd_pair(a, f2pack(row[x], row[x + 1]), E, DX);
+                f2scale(E, R);
+                f2scale(R, C4);
+                f2acc_add(DX, TWO);
             }
-            if (x == xe) {  // odd tail pixel
-                const float e = f2unpack(E).x, d = f2unpack(DX).x, gp = row[x];
-                const float ge = gp * e, t = ge * d;
-                tE += ge;
-                tG += gp;
-                tX += t;
-                tXX = fmaf(t, d, tXX);
-            }
-            dx += 32.f;
+            if (x == xb) bwd_pair(a, f2pack(row[x], 0.f), E, DX);
+        } else {
+            float d = dx;
+            for (int x = xa; x <= xb; ++x, d += 1.f)
+                bwd_pair(a, f2pack(row[x], 0.f), f2pack(ex2_approx(fmaf(s.A * d, d, Ckdy2)), 0.f), f2pack(d, 0.f));
         }
-        const float2 vE = f2unpack(aE), vG = f2unpack(aG), vX = f2unpack(aX), vXX = f2unpack(aXX);
-        const float rE = vE.x + vE.y + tE, rG = vG.x + vG.y + tG, rX = vX.x + vX.y + tX;
-        const float rXX = vXX.x + vXX.y + tXX;
-        M.xx += rXX;
+        const float rE = f2sum(a.e), rX = f2sum(a.x);
         M.e += rE;
-        M.g += rG;
+        M.g += f2sum(a.g);
         M.x += rX;
+        M.xx += f2sum(a.xx);
         M.y = fmaf(dy, rE, M.y);
         M.xy = fmaf(dy, rX, M.xy);
         M.yy = fmaf(dy * dy, rE, M.yy);

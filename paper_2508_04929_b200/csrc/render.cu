@@ -143,28 +143,28 @@ __global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
             const int xa = max((int)ceilf(xcv - half), 0);
             const int xb = min((int)floorf(xcv + half), D - 1);
             if (xa > xb) continue;
-            float dx = (float)xa - xcv;
+            const float dx = (float)xa - xcv;
             const float Ckdy2 = s.Ck * dy * dy;
-            for (int x0 = xa; x0 <= xb; x0 += 32) {
-                // restart the recurrence from an exact exp every 32 pixels;
-                // two pixels per packed step (see raster_bwd.cu bwd_rows)
+            if (xb - xa < 32) {
+                // recurrence, two pixels per packed step (raster_bwd.cu bwd_rows)
                 const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
                 const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
                 const float g1 = g0 * c;
                 uint64_t E = f2pack(e0, e0 * g0);
                 uint64_t R = f2pack(g0 * g1, g1 * g1 * c);
-                const int xe = min(xb, x0 + 31);
-                int x = x0;
-#pragma unroll 2
-                for (; x < xe; x += 2) {
+                int x = xa;
+                for (; x < xb; x += 2) {
                     const float2 v = f2unpack(f2fma(WS, E, BIAS));
                     atomicAdd(row + x, __float_as_int(v.x) - 0x4B400000);
                     atomicAdd(row + x + 1, __float_as_int(v.y) - 0x4B400000);
-                    E = f2mul(E, R);
-                    R = f2mul(R, C4);
+                    f2scale(E, R);
+                    f2scale(R, C4);
                 }
-                if (x == xe) atomicAdd(row + x, fast_rint(fmaf(wS, f2unpack(E).x, -wsubS)));
-                dx += 32.f;
+                if (x == xb) atomicAdd(row + x, fast_rint(fmaf(wS, f2unpack(E).x, -wsubS)));
+            } else {  // long rows: exact exp per pixel
+                float d = dx;
+                for (int x = xa; x <= xb; ++x, d += 1.f)
+                    atomicAdd(row + x, fast_rint(fmaf(wS, ex2_approx(fmaf(s.A * d, d, Ckdy2)), -wsubS)));
             }
         }
     }
