@@ -181,46 +181,15 @@ __device__ __forceinline__ bool row_span(const Splat2 &s, float dy, int xlo, int
 // ---- packed f32x2 arithmetic (sm_100a FFMA2 / FMUL2 / FADD2) --------------
 // One instruction updates two fp32 lanes: same FMA-pipe throughput as two
 // FFMAs but half the issue slots (profiles/microbench_ffma2_r01.txt), which
-// is what the issue-bound pixel loops need.
-__device__ __forceinline__ uint64_t f2pack(float a, float b) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ float2 f2unpack(uint64_t v) {
-    float2 r;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-    return r;
-}
-__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-// in-place forms keep accumulators in their register pair (no MOV shuffles)
-__device__ __forceinline__ void f2acc_add(uint64_t &acc, uint64_t a) {
-    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(a));
-}
-__device__ __forceinline__ void f2acc_fma(uint64_t &acc, uint64_t a, uint64_t b) {
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
-}
-__device__ __forceinline__ void f2scale(uint64_t &a, uint64_t b) {
-    asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(b));
-}
-__device__ __forceinline__ float f2sum(uint64_t v) {
-    const float2 p = f2unpack(v);
-    return p.x + p.y;
-}
+// is what the issue-bound pixel loops need.  CUDA 12.8+ intrinsics on float2.
+__device__ __forceinline__ float2 f2pack(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ void f2acc_add(float2 &acc, float2 a) { acc = __fadd2_rn(acc, a); }
+__device__ __forceinline__ void f2acc_fma(float2 &acc, float2 a, float2 b) { acc = __ffma2_rn(a, b, acc); }
+__device__ __forceinline__ void f2scale(float2 &a, float2 b) { a = __fmul2_rn(a, b); }
+__device__ __forceinline__ float f2sum(float2 v) { return v.x + v.y; }
 
 // float -> nearest int32 on the FMA/ALU pipes (no F2I on the XU pipe):
 // valid for |x| < 2^22; returns round-to-nearest-even(x).

@@ -38,14 +38,14 @@ struct Moments {
 // One pixel pair (or a single pixel when GP's high lane is 0) of a row walk:
 // packed per-row sums of ge, g, ge dx', ge dx'^2.
 struct RowSums {
-    uint64_t e = 0, g = 0, x = 0, xx = 0;  // (0.f, 0.f)
+    float2 e = {0.f, 0.f}, g = {0.f, 0.f}, x = {0.f, 0.f}, xx = {0.f, 0.f};
 };
 
-__device__ __forceinline__ void bwd_pair(RowSums &a, uint64_t GP, uint64_t E, uint64_t DX) {
-    const uint64_t GE = f2mul(GP, E);
+__device__ __forceinline__ void bwd_pair(RowSums &a, float2 GP, float2 E, float2 DX) {
+    const float2 GE = f2mul(GP, E);
     f2acc_add(a.e, GE);
     f2acc_add(a.g, GP);
-    const uint64_t T = f2mul(GE, DX);
+    const float2 T = f2mul(GE, DX);
     f2acc_add(a.x, T);
     f2acc_fma(a.xx, T, DX);
 }
@@ -59,7 +59,7 @@ __device__ __forceinline__ void bwd_pair(RowSums &a, uint64_t GP, uint64_t E, ui
 __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, int D, int ya, int yb,
                                          const Splat2 &s, float c2A, Moments &M) {
     const float c = c2A, c4 = (c * c) * (c * c);
-    const uint64_t C4 = f2pack(c4, c4), TWO = f2pack(2.f, 2.f);
+    const float2 C4 = f2pack(c4, c4), TWO = f2pack(2.f, 2.f);
     float dy = (float)ya - s.mpy;
     float xcv = fmaf(-s.slope, dy, s.mpx);
     const float *row = img + (ya - r0) * D;
@@ -77,10 +77,11 @@ __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, 
             const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
             const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
             const float g1 = g0 * c;
-            uint64_t E = f2pack(e0, e0 * g0);
-            uint64_t R = f2pack(g0 * g1, g1 * g1 * c);
-            uint64_t DX = f2pack(dx, dx + 1.f);
+            float2 E = f2pack(e0, e0 * g0);
+            float2 R = f2pack(g0 * g1, g1 * g1 * c);
+            float2 DX = f2pack(dx, dx + 1.f);
             int x = xa;
+#pragma unroll 1
             for (; x < xb; x += 2) {
                 bwd_pair(a, f2pack(row[x], row[x + 1]), E, DX);
                 f2scale(E, R);

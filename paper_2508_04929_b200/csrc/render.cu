@@ -131,8 +131,8 @@ __global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
         const float c4 = (c * c) * (c * c);
         // v = wS e - wS sub + 1.5*2^23: the FFMA that evaluates the contribution
         // also places its rounded integer in the low mantissa bits (fast_rint)
-        const uint64_t WS = f2pack(wS, wS), BIAS = f2pack(12582912.0f - wsubS, 12582912.0f - wsubS);
-        const uint64_t C4 = f2pack(c4, c4);
+        const float2 WS = f2pack(wS, wS), BIAS = f2pack(12582912.0f - wsubS, 12582912.0f - wsubS);
+        const float2 C4 = f2pack(c4, c4);
         float dy = (float)ylo - s.mpy;
         float xcv = fmaf(-s.slope, dy, s.mpx);
         int *row = band + (ylo - r0) * D;
@@ -150,17 +150,17 @@ __global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
                 const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
                 const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
                 const float g1 = g0 * c;
-                uint64_t E = f2pack(e0, e0 * g0);
-                uint64_t R = f2pack(g0 * g1, g1 * g1 * c);
+                float2 E = f2pack(e0, e0 * g0);
+                float2 R = f2pack(g0 * g1, g1 * g1 * c);
                 int x = xa;
                 for (; x < xb; x += 2) {
-                    const float2 v = f2unpack(f2fma(WS, E, BIAS));
+                    const float2 v = f2fma(WS, E, BIAS);
                     atomicAdd(row + x, __float_as_int(v.x) - 0x4B400000);
                     atomicAdd(row + x + 1, __float_as_int(v.y) - 0x4B400000);
                     f2scale(E, R);
                     f2scale(R, C4);
                 }
-                if (x == xb) atomicAdd(row + x, fast_rint(fmaf(wS, f2unpack(E).x, -wsubS)));
+                if (x == xb) atomicAdd(row + x, fast_rint(fmaf(wS, E.x, -wsubS)));
             } else {  // long rows: exact exp per pixel
                 float d = dx;
                 for (int x = xa; x <= xb; ++x, d += 1.f)
