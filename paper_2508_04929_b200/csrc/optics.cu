@@ -21,6 +21,7 @@ namespace cgs {
 
 struct CtfConst {
     double lam, cs, du, dv, c2a, s2a, s1mw2, w, phase, bfac, dA;
+    double inv_dA, pl, cs3;  // 1/(D A), pi lambda, pi/2 Cs lambda^3 (fast path)
 };
 
 __host__ __device__ inline double electron_wavelength_A(double kv) {
@@ -85,11 +86,39 @@ __device__ __forceinline__ int wrap_freq(int f, int D, int c0) {
     return v;
 }
 
+// H for the step's multiply: chi in fp64 without divisions (k^2 cos 2(theta -
+// theta_a) = (kx^2 - ky^2) cos 2theta_a + 2 kx ky sin 2theta_a), reduced mod
+// 2 pi in fp64, then an fp32 sincos; |H - H_ref| < 1e-6 (fp32 pipeline).
+__device__ __forceinline__ float ctf_value_fast(const CtfConst &c, int fy, int fx) {
+    const double kx = fx * c.inv_dA, ky = fy * c.inv_dA;
+    const double k2 = kx * kx + ky * ky;
+    const double ck2 = (kx * kx - ky * ky) * c.c2a + 2.0 * kx * ky * c.s2a;
+    const double dk2 = 0.5 * ((c.du + c.dv) * k2 + (c.du - c.dv) * ck2);
+    double chi = c.pl * dk2 - c.cs3 * k2 * k2 + c.phase;
+    chi -= 6.283185307179586 * rint(chi * 0.15915494309189535);
+    float sn, cs;
+    sincosf((float)chi, &sn, &cs);
+    float H = -((float)c.s1mw2 * sn + (float)c.w * cs);
+    if (c.bfac > 0.0) H *= __expf((float)(-c.bfac * k2 * 0.25));
+    return H;
+}
+
 // spectrum[b][jy][jx] *= H_sym(fy, fx) / D^2 over the R2C half spectrum
-__global__ void ctf_multiply_kernel(float2 *__restrict__ spec, int D, double pix,
-                                    const double *__restrict__ ctf, const double *__restrict__ Harr) {
+__global__ void __launch_bounds__(256) ctf_multiply_kernel(float2 *__restrict__ spec, int D, double pix,
+                                                           const double *__restrict__ ctf,
+                                                           const double *__restrict__ Harr) {
     const int b = blockIdx.y;
     const int W = D / 2 + 1;
+    __shared__ CtfConst cc;
+    if (ctf) {  // per-image constants once per block (wavelength, 2 theta_a trig)
+        if (threadIdx.x == 0) {
+            cc = load_ctf(ctf + 8 * (int64_t)b, D, pix);
+            cc.inv_dA = 1.0 / cc.dA;
+            cc.pl = kPiD * cc.lam;
+            cc.cs3 = 0.5 * kPiD * cc.cs * cc.lam * cc.lam * cc.lam;
+        }
+        __syncthreads();
+    }
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= D * W) return;
     const int jy = idx / W, jx = idx - jy * W, c0 = D / 2;
@@ -98,9 +127,8 @@ __global__ void ctf_multiply_kernel(float2 *__restrict__ spec, int D, double pix
     const bool nyq = (D % 2 == 0) && (fy == -c0 || fx == -c0);
     double H;
     if (ctf) {
-        CtfConst c = load_ctf(ctf + 8 * (int64_t)b, D, pix);
-        H = ctf_value(c, fy, fx);
-        if (nyq) H = 0.5 * (H + ctf_value(c, wrap_freq(fy, D, c0), wrap_freq(fx, D, c0)));
+        H = ctf_value_fast(cc, fy, fx);
+        if (nyq) H = 0.5 * (H + ctf_value_fast(cc, wrap_freq(fy, D, c0), wrap_freq(fx, D, c0)));
     } else {
         const double *Hb = Harr + (int64_t)b * D * D;
         H = Hb[(fy + c0) * D + fx + c0];
@@ -114,22 +142,35 @@ __global__ void ctf_multiply_kernel(float2 *__restrict__ spec, int D, double pix
 }
 
 // loss_b = mean((model - obs)^2) in fp64; resid = 2/D^2 (model - obs)
-__global__ void __launch_bounds__(256) loss_resid_kernel(const float *__restrict__ model,
-                                                         const float *__restrict__ obs, int D,
-                                                         double *__restrict__ loss,
-                                                         float *__restrict__ resid,
-                                                         int32_t *status) {
+__global__ void __launch_bounds__(1024) loss_resid_kernel(const float *__restrict__ model,
+                                                          const float *__restrict__ obs, int D,
+                                                          double *__restrict__ loss,
+                                                          float *__restrict__ resid,
+                                                          int32_t *status) {
     const int b = blockIdx.x;
     const int64_t off = (int64_t)b * D * D;
     const int npix = D * D;
     const float sc = 2.f / (float)npix;
     double acc = 0.0;
-    for (int i = threadIdx.x; i < npix; i += blockDim.x) {
+    int i0 = 0;
+    if ((npix & 3) == 0) {  // vectorised main part
+        const float4 *m4 = reinterpret_cast<const float4 *>(model + off);
+        const float4 *o4 = reinterpret_cast<const float4 *>(obs + off);
+        float4 *r4 = reinterpret_cast<float4 *>(resid + off);
+        for (int i = threadIdx.x; i < (npix >> 2); i += blockDim.x) {
+            const float4 m = m4[i], o = o4[i];
+            const float4 d = make_float4(m.x - o.x, m.y - o.y, m.z - o.z, m.w - o.w);
+            acc += (double)d.x * d.x + (double)d.y * d.y + (double)d.z * d.z + (double)d.w * d.w;
+            if (resid) r4[i] = make_float4(sc * d.x, sc * d.y, sc * d.z, sc * d.w);
+        }
+        i0 = npix;
+    }
+    for (int i = i0 + threadIdx.x; i < npix; i += blockDim.x) {
         float d = model[off + i] - obs[off + i];
         acc += (double)d * (double)d;
         if (resid) resid[off + i] = sc * d;
     }
-    __shared__ double ws[8];
+    __shared__ double ws[32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
@@ -226,7 +267,7 @@ extern "C" int cgs_ctf_apply(void *plan, const float *in, float *out, int32_t B,
 extern "C" int cgs_loss_residual(const float *model, const float *obs, int32_t B, int32_t size,
                                  double *loss, float *resid, int32_t *status, void *stream) {
     if (B <= 0 || size < 1 || !model || !obs || !loss) return CGS_ERR_ARG;
-    loss_resid_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(model, obs, size, loss, resid, status);
+    loss_resid_kernel<<<B, 1024, 0, (cudaStream_t)stream>>>(model, obs, size, loss, resid, status);
     return check_launch("loss_resid_kernel");
 }
 
