@@ -1,0 +1,108 @@
+"""Multi-process data parallelism on CPU (gloo, world_size 2).
+
+The GPU run all-reduces the 10-float per-Gaussian world-frame accumulator
+with NCCL between the backward and the epilogue (paper_2508_04929_b200.parallel).
+Here the same host logic -- batch sharding, the accumulator all-reduce, the
+global 1/B scale -- runs over gloo with the CPU oracle computing each rank's
+accumulator, and must equal the single-process full-batch gradient.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, grads_close
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _inputs(oracle):
+    grid = oracle.Grid(32, 0.5, 3.0)
+    params = oracle.init_random(300, 0, grid)
+    rng = np.random.default_rng(4)
+    params[:, 3:6] = oracle.inverse_activate(rng.uniform(1.0, 2.5, (300, 3)) * grid.pixel_width)
+    params[:, 6:10] = rng.standard_normal((300, 4))
+    poses = [oracle.sample_pose(np.random.default_rng(50 + i)) for i in range(6)]
+    ups = [np.random.default_rng(90 + i).standard_normal((32, 32)) for i in range(6)]
+    return grid, params, poses, ups
+
+
+def _worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import cgs_oracle as oracle
+    from paper_2508_04929_b200 import parallel
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    grid, params, poses, ups = _inputs(oracle)
+    batch = np.arange(len(poses))
+    local = parallel.shard(batch, rank, world)
+    acc = np.zeros((len(params), 10))
+    for i in local:
+        W, t = poses[i]
+        proj = oracle.project(params, W, t, grid)
+        acc += oracle.world_accumulator(proj, oracle.backward_raw_sums(params, W, t, grid, ups[i], proj))
+    t_acc = torch.from_numpy(acc)
+    parallel.allreduce_accumulator(t_acc)
+    grads = oracle.grads_from_world_accumulator(params, t_acc.numpy()) / len(batch)
+    gathered = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(gathered, torch.tensor([len(local)]))
+    if rank == 0:
+        np.savez(out_path, grads=grads, counts=np.array([int(g) for g in gathered]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_allreduce_matches_single_process(oracle, tmp_path):
+    out = str(tmp_path / "dp.npz")
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    res = np.load(out)
+    grid, params, poses, ups = _inputs(oracle)
+    ref = np.zeros_like(params)
+    for (W, t), up in zip(poses, ups):
+        ref += oracle.rasterize_backward(params, W, t, grid, up)
+    ref /= len(poses)
+    assert list(res["counts"]) == [3, 3]
+    grads_close(res["grads"], ref, 1e-10, 1e-12)
+
+
+def test_shard_partitions_every_batch():
+    from paper_2508_04929_b200 import parallel
+
+    rng = np.random.default_rng(0)
+    for B in (1, 2, 7, 256, 257):
+        for world in (1, 2, 3, 8):
+            idx = rng.permutation(1000)[:B]
+            parts = [parallel.shard(idx, r, world) for r in range(world)]
+            assert np.array_equal(np.concatenate(parts), idx)
+            assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+
+
+def test_epoch_batches_follow_reference_shuffle():
+    from paper_2508_04929_b200 import parallel
+
+    a = parallel.epoch_batches(10, 1, np.random.default_rng(3))
+    b = np.random.default_rng(3).permutation(10)  # train.py:220,230
+    assert [int(x[0]) for x in a] == list(b)
+    c = parallel.epoch_batches(10, 4, np.random.default_rng(3))
+    assert [len(x) for x in c] == [4, 4, 2]
+
+
+@pytest.mark.skipif(not dist.is_available(), reason="torch.distributed unavailable")
+def test_allreduce_is_noop_without_process_group():
+    from paper_2508_04929_b200 import parallel
+
+    t = torch.ones(5)
+    assert parallel.allreduce_accumulator(t) is t and torch.equal(t, torch.ones(5))
