@@ -178,6 +178,49 @@ __device__ __forceinline__ bool row_span(const Splat2 &s, float dy, int xlo, int
     return xa <= xb;
 }
 
+// ---- footprint boxes and their CTA-wide union -----------------------------
+// With Gaussians in spatial (Morton) order, the footprints of a CTA's
+// Gaussians in one image cover a small region, so the kernels stage (or
+// accumulate into) only that region of the image in shared memory.
+struct Box {
+    int x0, x1, y0, y1;  // inclusive pixel bounds; empty when x0 > x1
+};
+
+__device__ __forceinline__ Box footprint_box(const Splat2 &s, bool live, int ylo, int yhi, int D) {
+    Box b{0x7fffffff, -1, 0x7fffffff, -1};
+    if (live && ylo <= yhi) {
+        b.x0 = max((int)floorf(s.mpx - s.hx) - 1, 0);
+        b.x1 = min((int)ceilf(s.mpx + s.hx) + 1, D - 1);
+        b.y0 = ylo;
+        b.y1 = yhi;
+    }
+    return b;
+}
+
+// Union of every thread's box; red is shared scratch of 4 x (blockDim/32) ints.
+// Contains __syncthreads: call from all threads.
+__device__ __forceinline__ Box block_union(const Box &b, int *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int x0 = __reduce_min_sync(0xffffffffu, b.x0), y0 = __reduce_min_sync(0xffffffffu, b.y0);
+    const int x1 = __reduce_max_sync(0xffffffffu, b.x1), y1 = __reduce_max_sync(0xffffffffu, b.y1);
+    __syncthreads();  // earlier readers of red are done
+    if (lane == 0) {
+        red[warp] = x0;
+        red[nw + warp] = x1;
+        red[2 * nw + warp] = y0;
+        red[3 * nw + warp] = y1;
+    }
+    __syncthreads();
+    Box r{0x7fffffff, -1, 0x7fffffff, -1};
+    for (int w = 0; w < nw; ++w) {
+        r.x0 = min(r.x0, red[w]);
+        r.x1 = max(r.x1, red[nw + w]);
+        r.y0 = min(r.y0, red[2 * nw + w]);
+        r.y1 = max(r.y1, red[3 * nw + w]);
+    }
+    return r;
+}
+
 // ---- packed f32x2 arithmetic (sm_100a FFMA2 / FMUL2 / FADD2) --------------
 // One instruction updates two fp32 lanes: same FMA-pipe throughput as two
 // FFMAs but half the issue slots (profiles/microbench_ffma2_r01.txt), which

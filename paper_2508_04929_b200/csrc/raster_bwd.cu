@@ -22,6 +22,8 @@
 // shared memory with 1-D bulk async copies (TMA engine, mbarrier completion),
 // so image b+1 streams in while image b is processed; larger D falls back to
 // synchronous row bands.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cgs {
@@ -56,19 +58,21 @@ __device__ __forceinline__ void bwd_pair(RowSums &a, float2 GP, float2 E, float2
 // (e_k, e_k+1) *= (g_k g_k+1, g_k+1 g_k+2), that pair *= c^4 (relative error
 // < 2e-5 over 32 pixels).  Rows longer than 32 pixels take an exact exp per
 // pixel instead.
-__device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, int D, int ya, int yb,
-                                         const Splat2 &s, float c2A, Moments &M) {
+// img points at pixel (r0, 0) of a staged block with row stride `ld`; pixel
+// columns are clipped to [xlo, xhi] (absolute image coordinates).
+__device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, int ld, int xlo, int xhi, int ya,
+                                         int yb, const Splat2 &s, float c2A, Moments &M) {
     const float c = c2A, c4 = (c * c) * (c * c);
     const float2 C4 = f2pack(c4, c4), TWO = f2pack(2.f, 2.f);
     float dy = (float)ya - s.mpy;
     float xcv = fmaf(-s.slope, dy, s.mpx);
-    const float *row = img + (ya - r0) * D;
-    for (int iy = ya; iy <= yb; ++iy, dy += 1.f, xcv -= s.slope, row += D) {
+    const float *row = img + (ya - r0) * ld;
+    for (int iy = ya; iy <= yb; ++iy, dy += 1.f, xcv -= s.slope, row += ld) {
         const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
         if (rem <= 0.f) continue;
         const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
-        const int xa = max((int)ceilf(xcv - half), 0);
-        const int xb = min((int)floorf(xcv + half), D - 1);
+        const int xa = max((int)ceilf(xcv - half), xlo);
+        const int xb = min((int)floorf(xcv + half), xhi);
         if (xa > xb) continue;
         const float dx = (float)xa - xcv;
         const float Ckdy2 = s.Ck * dy * dy;
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(kBwdThreadsDB, 1) raster_bwd_db_kernel(
         const float c2A = exp2f(2.f * s.A);
         mbar_wait(&bars[i & 1], (uint32_t)((i >> 1) & 1));
         Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        bwd_rows(smem_db + (i & 1) * D * D, 0, D, ylo, yhi, s, c2A, M);
+        bwd_rows(smem_db + (i & 1) * D * D, 0, D, 0, D - 1, ylo, yhi, s, c2A, M);
         if (ylo <= yhi) accumulate_world(M, s, P, G.inv_h, acc);
         __syncthreads();  // every thread is done reading buf[i & 1]
         if (threadIdx.x == 0 && i + 2 < nimg) {
@@ -258,7 +262,63 @@ __global__ void __launch_bounds__(kBwdThreadsBand, 3) raster_bwd_band_kernel(
             __syncthreads();
             stage_rows(img, upstream, b, D, r0, r1, layout);
             __syncthreads();
-            bwd_rows(img, r0, D, max(ylo, r0), min(yhi, r1 - 1), s, c2A, M);
+            bwd_rows(img, r0, D, 0, D - 1, max(ylo, r0), min(yhi, r1 - 1), s, c2A, M);
+        }
+        if (ylo <= yhi) accumulate_world(M, s, P, G.inv_h, acc);
+    }
+    if (valid) store_partial(partial, grp, n, g, acc);
+}
+
+// Region staging (default): per image the CTA stages only the union of its
+// Gaussians' footprint boxes, in row bands of at most kRegFloats floats.  With
+// Gaussians in spatial order the region is a few hundred pixels, so shared
+// memory stays small and several CTAs share an SM; in any order it is correct
+// (the region then grows to the whole image and is processed band by band).
+constexpr int kRegThreads = 256;
+constexpr int kRegFloats = 4096;  // 16 KB per band
+
+__global__ void __launch_bounds__(kRegThreads, 3) raster_bwd_region_kernel(
+    const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
+    const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
+    __shared__ __align__(16) float reg[kRegFloats];
+    __shared__ int red[4 * (kRegThreads / 32)];
+    const int D = G.D;
+    const int64_t g = (int64_t)blockIdx.x * kRegThreads + threadIdx.x;
+    const bool valid = g < n;
+    const int grp = blockIdx.y;
+    const int b_begin = grp * ipg, b_end = min(B, b_begin + ipg);
+    SplatRec rec{};
+    if (valid) rec = load_splat(splat, g);
+    float acc[CGS_ACC_STRIDE];
+#pragma unroll
+    for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = 0.f;
+
+    for (int b = b_begin; b < b_end; ++b) {
+        const PoseF P = load_pose_f(poses, b);
+        Splat2 s{};
+        int ylo = 1, yhi = 0;
+        if (valid) {
+            s = project2(rec, P, G);
+            footprint_rows(s, D, ylo, yhi);
+        }
+        const Box R = block_union(footprint_box(s, valid, ylo, yhi, D), red);
+        if (R.x0 > R.x1) continue;  // uniform
+        const int W = R.x1 - R.x0 + 1;
+        const int HBr = max(1, kRegFloats / W);
+        const float c2A = exp2f(2.f * s.A);
+        const float *src = upstream + (int64_t)b * D * D;
+        Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int by0 = R.y0; by0 <= R.y1; by0 += HBr) {
+            const int by1 = min(R.y1, by0 + HBr - 1);
+            const int cnt = (by1 - by0 + 1) * W;
+            __syncthreads();  // previous band fully consumed
+            for (int i = threadIdx.x; i < cnt; i += kRegThreads) {
+                const int r = i / W;
+                reg[i] = __ldg(src + (int64_t)(by0 + r) * D + R.x0 + (i - r * W));
+            }
+            __syncthreads();
+            const int ya = max(ylo, by0), yb = min(yhi, by1);
+            if (ya <= yb) bwd_rows(reg - R.x0, by0, W, R.x0, R.x1, ya, yb, s, c2A, M);
         }
         if (ylo <= yhi) accumulate_world(M, s, P, G.inv_h, acc);
     }
@@ -306,9 +366,21 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
     const int D = grid.size;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t G = cgs_bwd_groups(B, images_per_group);
+    // kernel variant: region (default) | db | band; CGS_BWD_KERNEL overrides for A/B runs
+    static int variant = -1;
+    if (variant < 0) {
+        const char *v = getenv("CGS_BWD_KERNEL");
+        variant = (v && v[0] == 'd') ? 1 : (v && v[0] == 'b') ? 2 : 0;
+    }
+    if (layout == CGS_LAYOUT_NATURAL && variant == 0) {
+        dim3 g((unsigned)((n + kRegThreads - 1) / kRegThreads), (unsigned)G);
+        raster_bwd_region_kernel<<<g, kRegThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), upstream, partial,
+                                                            images_per_group);
+        return check_launch("raster_bwd_region_kernel");
+    }
     const size_t db_bytes = 2 * (size_t)D * D * sizeof(float);
     const bool aligned = ((reinterpret_cast<uintptr_t>(upstream) & 15) == 0) && ((D * D) % 4 == 0);
-    if (layout == CGS_LAYOUT_NATURAL && db_bytes <= (size_t)kDBMaxBytes && aligned) {
+    if (layout == CGS_LAYOUT_NATURAL && variant == 1 && db_bytes <= (size_t)kDBMaxBytes && aligned) {
         static size_t configured = 0;
         if (db_bytes > 48 * 1024 && db_bytes > configured) {
             cudaFuncSetAttribute(raster_bwd_db_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)db_bytes);

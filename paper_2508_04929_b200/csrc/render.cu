@@ -32,8 +32,8 @@
 namespace cgs {
 
 constexpr int kRThreads = 256;
-constexpr int kRChunk = 4096;              // Gaussians per CTA
-constexpr int kRBandBytes = 64 * 1024;     // int32 accumulator rows per CTA
+constexpr int kRegInts = 4096;             // int32 accumulator band per CTA (16 KB)
+constexpr int kRImagesPerCTA = 16;
 constexpr int kWbBlock = 1024;
 constexpr float kFixedRange = 1073741824.f;  // 2^30
 constexpr float kContribRange = 4194304.f;   // 2^22
@@ -107,72 +107,103 @@ __global__ void __launch_bounds__(256) wbound_scale_kernel(float *part, int npar
     }
 }
 
-__global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
-    const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, GridF G,
-    const float *__restrict__ scale_ptr, int HB, int *__restrict__ out) {
-    extern __shared__ int band[];
-    const int D = G.D;
-    const int b = blockIdx.y;
-    const int r0 = blockIdx.z * HB, r1 = min(D, r0 + HB);
-    const int npx = (r1 - r0) * D;
-    for (int i = threadIdx.x; i < npx; i += kRThreads) band[i] = 0;
-    const float scale = *scale_ptr;
-    const PoseF P = load_pose_f(poses, b);
-    const int64_t g_begin = (int64_t)blockIdx.x * kRChunk;
-    const int64_t g_end = min(n, g_begin + kRChunk);
-    __syncthreads();
-    for (int64_t g = g_begin + threadIdx.x; g < g_end; g += kRThreads) {
-        const Splat2 s = project2(load_splat(splat, g), P, G);
-        if (!(s.w > 0.f)) continue;
-        const int ylo = max(max((int)ceilf(s.mpy - s.hy), 0), r0);
-        const int yhi = min(min((int)floorf(s.mpy + s.hy), D - 1), r1 - 1);
-        const float wS = s.w * scale, wsubS = s.w * kSub * scale;
-        const float c = exp2f(2.f * s.A);  // g_{k+1} / g_k
-        const float c4 = (c * c) * (c * c);
-        // v = wS e - wS sub + 1.5*2^23: the FFMA that evaluates the contribution
-        // also places its rounded integer in the low mantissa bits (fast_rint)
-        const float2 WS = f2pack(wS, wS), BIAS = f2pack(12582912.0f - wsubS, 12582912.0f - wsubS);
-        const float2 C4 = f2pack(c4, c4);
-        float dy = (float)ylo - s.mpy;
-        float xcv = fmaf(-s.slope, dy, s.mpx);
-        int *row = band + (ylo - r0) * D;
-        for (int iy = ylo; iy <= yhi; ++iy, dy += 1.f, xcv -= s.slope, row += D) {
-            const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
-            if (rem <= 0.f) continue;
-            const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
-            const int xa = max((int)ceilf(xcv - half), 0);
-            const int xb = min((int)floorf(xcv + half), D - 1);
-            if (xa > xb) continue;
-            const float dx = (float)xa - xcv;
-            const float Ckdy2 = s.Ck * dy * dy;
-            if (xb - xa < 32) {
-                // recurrence, two pixels per packed step (raster_bwd.cu bwd_rows)
-                const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
-                const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
-                const float g1 = g0 * c;
-                float2 E = f2pack(e0, e0 * g0);
-                float2 R = f2pack(g0 * g1, g1 * g1 * c);
-                int x = xa;
-                for (; x < xb; x += 2) {
-                    const float2 v = f2fma(WS, E, BIAS);
-                    atomicAdd(row + x, __float_as_int(v.x) - 0x4B400000);
-                    atomicAdd(row + x + 1, __float_as_int(v.y) - 0x4B400000);
-                    f2scale(E, R);
-                    f2scale(R, C4);
-                }
-                if (x == xb) atomicAdd(row + x, fast_rint(fmaf(wS, E.x, -wsubS)));
-            } else {  // long rows: exact exp per pixel
-                float d = dx;
-                for (int x = xa; x <= xb; ++x, d += 1.f)
-                    atomicAdd(row + x, fast_rint(fmaf(wS, ex2_approx(fmaf(s.A * d, d, Ckdy2)), -wsubS)));
+// Add one footprint's rows [ya, yb] into the int32 block at acc (pixel (r0, 0),
+// row stride ld), columns clipped to [xlo, xhi].
+__device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, int xlo, int xhi, int ya, int yb,
+                                         const Splat2 &s, float scale) {
+    const float wS = s.w * scale, wsubS = s.w * kSub * scale;
+    const float c = exp2f(2.f * s.A);  // g_{k+1} / g_k
+    const float c4 = (c * c) * (c * c);
+    // v = wS e - wS sub + 1.5*2^23: the FFMA that evaluates the contribution
+    // also places its rounded integer in the low mantissa bits (fast_rint)
+    const float2 WS = f2pack(wS, wS), BIAS = f2pack(12582912.0f - wsubS, 12582912.0f - wsubS);
+    const float2 C4 = f2pack(c4, c4);
+    float dy = (float)ya - s.mpy;
+    float xcv = fmaf(-s.slope, dy, s.mpx);
+    int *row = acc + (ya - r0) * ld;
+    for (int iy = ya; iy <= yb; ++iy, dy += 1.f, xcv -= s.slope, row += ld) {
+        const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
+        if (rem <= 0.f) continue;
+        const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
+        const int xa = max((int)ceilf(xcv - half), xlo);
+        const int xb = min((int)floorf(xcv + half), xhi);
+        if (xa > xb) continue;
+        const float dx = (float)xa - xcv;
+        const float Ckdy2 = s.Ck * dy * dy;
+        if (xb - xa < 32) {
+            // recurrence, two pixels per packed step (raster_bwd.cu bwd_rows)
+            const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
+            const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
+            const float g1 = g0 * c;
+            float2 E = f2pack(e0, e0 * g0);
+            float2 R = f2pack(g0 * g1, g1 * g1 * c);
+            int x = xa;
+#pragma unroll 1
+            for (; x < xb; x += 2) {
+                const float2 v = f2fma(WS, E, BIAS);
+                atomicAdd(row + x, __float_as_int(v.x) - 0x4B400000);
+                atomicAdd(row + x + 1, __float_as_int(v.y) - 0x4B400000);
+                f2scale(E, R);
+                f2scale(R, C4);
             }
+            if (x == xb) atomicAdd(row + x, fast_rint(fmaf(wS, E.x, -wsubS)));
+        } else {  // long rows: exact exp per pixel
+            float d = dx;
+            for (int x = xa; x <= xb; ++x, d += 1.f)
+                atomicAdd(row + x, fast_rint(fmaf(wS, ex2_approx(fmaf(s.A * d, d, Ckdy2)), -wsubS)));
         }
     }
-    __syncthreads();
-    int *dst = out + (int64_t)b * D * D + (int64_t)r0 * D;
-    for (int i = threadIdx.x; i < npx; i += kRThreads) {
-        const int v = band[i];
-        if (v) atomicAdd(dst + i, v);
+}
+
+// CTA = (256 Gaussians, group of images).  Per image the CTA accumulates only
+// the union of its Gaussians' footprint boxes (row bands of kRegInts ints) and
+// adds the band to the global int32 image with one atomic per non-zero pixel.
+// With Gaussians in spatial (Morton) order the region is small.
+__global__ void __launch_bounds__(kRThreads, 4) raster_fwd_atomic_kernel(
+    const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
+    const float *__restrict__ scale_ptr, int ipg, int *__restrict__ out) {
+    __shared__ __align__(16) int reg[kRegInts];
+    __shared__ int red[4 * (kRThreads / 32)];
+    const int D = G.D;
+    const int64_t g = (int64_t)blockIdx.x * kRThreads + threadIdx.x;
+    const bool valid = g < n;
+    const int b_begin = blockIdx.y * ipg, b_end = min(B, b_begin + ipg);
+    const float scale = *scale_ptr;
+    SplatRec rec{};
+    if (valid) rec = load_splat(splat, g);
+    for (int b = b_begin; b < b_end; ++b) {
+        const PoseF P = load_pose_f(poses, b);
+        Splat2 s{};
+        int ylo = 1, yhi = 0;
+        if (valid) {
+            s = project2(rec, P, G);
+            if (s.w > 0.f) {
+                ylo = max((int)ceilf(s.mpy - s.hy), 0);
+                yhi = min((int)floorf(s.mpy + s.hy), D - 1);
+            }
+        }
+        const Box R = block_union(footprint_box(s, valid, ylo, yhi, D), red);
+        if (R.x0 > R.x1) continue;  // uniform
+        const int W = R.x1 - R.x0 + 1;
+        const int HBr = max(1, kRegInts / W);
+        int *dst = out + (int64_t)b * D * D;
+        for (int by0 = R.y0; by0 <= R.y1; by0 += HBr) {
+            const int by1 = min(R.y1, by0 + HBr - 1);
+            const int cnt = (by1 - by0 + 1) * W;
+            __syncthreads();  // previous band flushed
+            for (int i = threadIdx.x; i < cnt; i += kRThreads) reg[i] = 0;
+            __syncthreads();
+            const int ya = max(ylo, by0), yb = min(yhi, by1);
+            if (ya <= yb) fwd_rows(reg - R.x0, by0, W, R.x0, R.x1, ya, yb, s, scale);
+            __syncthreads();
+            for (int i = threadIdx.x; i < cnt; i += kRThreads) {
+                const int v = reg[i];
+                if (v) {
+                    const int r = i / W;
+                    atomicAdd(dst + (int64_t)(by0 + r) * D + R.x0 + (i - r * W), v);
+                }
+            }
+        }
     }
 }
 
@@ -208,21 +239,11 @@ extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, in
     const double h = 2.0 * grid.extent / grid.size;
     wbound_partial_kernel<<<parts, kWbBlock, 0, st>>>(splat, n, h, part);
     wbound_scale_kernel<<<1, 256, 0, st>>>(part, parts);
-    int HB = kRBandBytes / (D * (int)sizeof(int));
-    if (HB < 1) return CGS_ERR_UNSUPPORTED;
-    HB = HB > D ? D : HB;
-    const int bands = (D + HB - 1) / HB;
-    const size_t smem = (size_t)HB * D * sizeof(int);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(raster_fwd_atomic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
     const int64_t count = (int64_t)B * D * D;
     cudaMemsetAsync(out, 0, sizeof(int) * count, st);
-    dim3 g((unsigned)((n + kRChunk - 1) / kRChunk), (unsigned)B, (unsigned)bands);
-    raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), part + 2 * parts, HB,
-                                                         reinterpret_cast<int *>(out));
+    dim3 g((unsigned)((n + kRThreads - 1) / kRThreads), (unsigned)((B + kRImagesPerCTA - 1) / kRImagesPerCTA));
+    raster_fwd_atomic_kernel<<<g, kRThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), part + 2 * parts,
+                                                      kRImagesPerCTA, reinterpret_cast<int *>(out));
     int rc = check_launch("raster_fwd_atomic_kernel");
     if (rc) return rc;
     const int64_t threads = (count + 3) / 4;

@@ -193,6 +193,13 @@ class Reconstructor:
         self.config = config or TrainConfig(batch_size=batch_size, mode=mode)
         self.mode = mode
         self.n = int(params.shape[0])
+        # Gaussians live on the device in spatial (Morton) order: a CTA's
+        # Gaussians then project into a small region of each image, which is
+        # what the region-staged kernels exploit.  Per-Gaussian math does not
+        # depend on the order (renders are integer sums), so results are
+        # unchanged; params_host() returns the caller's order.
+        self.perm = morton_order(np.asarray(params)[:, :3], grid.extent)
+        params = np.asarray(params, dtype=np.float64)[self.perm]
         self.params = torch.as_tensor(np.ascontiguousarray(params, dtype=np.float64)).to(dev)
         self.m = torch.zeros_like(self.params)
         self.v = torch.zeros_like(self.params)
@@ -290,7 +297,36 @@ class Reconstructor:
                 raise DegenerateRotationError("quaternion with zero or non-finite norm")
 
     def params_host(self) -> np.ndarray:
-        return self.params.cpu().numpy()
+        """Parameters in the caller's Gaussian order."""
+        out = np.empty((self.n, 11), dtype=np.float64)
+        out[self.perm] = self.params.cpu().numpy()
+        return out
+
+    def reorder(self) -> None:
+        """Re-sort the device-resident Gaussians (and Adam moments) by Morton code
+        of their current means, e.g. once per epoch as they move."""
+        torch = _torch()
+        local = morton_order(self.params[:, :3].cpu().numpy(), self.grid.extent)
+        idx = torch.as_tensor(local, device=self.params.device)
+        self.params = self.params.index_select(0, idx).contiguous()
+        self.m = self.m.index_select(0, idx).contiguous()
+        self.v = self.v.index_select(0, idx).contiguous()
+        self.perm = self.perm[local]
+
+
+def morton_order(means: np.ndarray, extent: float) -> np.ndarray:
+    """Stable argsort of the 30-bit Morton (Z-order) codes of 3-D points in
+    [-extent, extent]^3 (10 bits per axis)."""
+    q = np.clip(((np.asarray(means, np.float64) / extent + 1.0) * 511.5).astype(np.int64), 0, 1023)
+
+    def spread(v):
+        v = (v | (v << 16)) & 0x030000FF
+        v = (v | (v << 8)) & 0x0300F00F
+        v = (v | (v << 4)) & 0x030C30C3
+        return (v | (v << 2)) & 0x09249249
+
+    code = spread(q[:, 0]) | (spread(q[:, 1]) << 1) | (spread(q[:, 2]) << 2)
+    return np.argsort(code, kind="stable")
 
 
 def _dist_active() -> bool:
@@ -378,6 +414,8 @@ def train(dataset: Dataset, config: TrainConfig, *, n_gaussians: int, out_dir: s
 
     for epoch in range(config.epochs):
         lr = config.epoch_lr(epoch)
+        if epoch > 0:
+            rec.reorder()  # keep the device order spatial as the means move
         order = shuffle_rng.permutation(R)
         batches = [order[i:i + B] for i in range(0, R, B)]
         if epoch == 0:
