@@ -32,8 +32,8 @@
 namespace cgs {
 
 constexpr int kRThreads = 256;
-constexpr int kRegInts = 4096;             // int32 accumulator band per CTA (16 KB)
-constexpr int kRImagesPerCTA = 16;
+constexpr int kRChunk = 4096;              // Gaussians per CTA
+constexpr int kRBandBytes = 64 * 1024;     // int32 accumulator rows per CTA
 constexpr int kWbBlock = 1024;
 constexpr float kFixedRange = 1073741824.f;  // 2^30
 constexpr float kContribRange = 4194304.f;   // 2^22
@@ -155,55 +155,43 @@ __device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, 
     }
 }
 
-// CTA = (256 Gaussians, group of images).  Per image the CTA accumulates only
-// the union of its Gaussians' footprint boxes (row bands of kRegInts ints) and
-// adds the band to the global int32 image with one atomic per non-zero pixel.
-// With Gaussians in spatial (Morton) order the region is small.
-__global__ void __launch_bounds__(kRThreads, 4) raster_fwd_atomic_kernel(
-    const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
-    const float *__restrict__ scale_ptr, int ipg, int *__restrict__ out) {
-    __shared__ __align__(16) int reg[kRegInts];
-    __shared__ int red[4 * (kRThreads / 32)];
+// CTA = (chunk of kRChunk Gaussians, image, band of rows); the band's int32
+// accumulator (whole 128^2 image in 64 KB) lives in shared memory and is
+// added to the global image once at the end.  Lanes of a warp must hit
+// unrelated pixels to keep ATOMS conflicts rare, but the device order of the
+// Gaussians is spatial (Morton, chosen for the backward's region staging), so
+// the chunk visits Gaussians in a scrambled order: logical index i maps to
+// g = (i * A) mod n with gcd(A, n) = 1, stepped incrementally.
+__global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
+    const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, GridF G,
+    const float *__restrict__ scale_ptr, int HB, int64_t mulA, int *__restrict__ out) {
+    extern __shared__ int band[];
     const int D = G.D;
-    const int64_t g = (int64_t)blockIdx.x * kRThreads + threadIdx.x;
-    const bool valid = g < n;
-    const int b_begin = blockIdx.y * ipg, b_end = min(B, b_begin + ipg);
+    const int b = blockIdx.y;
+    const int r0 = blockIdx.z * HB, r1 = min(D, r0 + HB);
+    const int npx = (r1 - r0) * D;
+    for (int i = threadIdx.x; i < npx; i += kRThreads) band[i] = 0;
     const float scale = *scale_ptr;
-    SplatRec rec{};
-    if (valid) rec = load_splat(splat, g);
-    for (int b = b_begin; b < b_end; ++b) {
-        const PoseF P = load_pose_f(poses, b);
-        Splat2 s{};
-        int ylo = 1, yhi = 0;
-        if (valid) {
-            s = project2(rec, P, G);
-            if (s.w > 0.f) {
-                ylo = max((int)ceilf(s.mpy - s.hy), 0);
-                yhi = min((int)floorf(s.mpy + s.hy), D - 1);
-            }
-        }
-        const Box R = block_union(footprint_box(s, valid, ylo, yhi, D), red);
-        if (R.x0 > R.x1) continue;  // uniform
-        const int W = R.x1 - R.x0 + 1;
-        const int HBr = max(1, kRegInts / W);
-        int *dst = out + (int64_t)b * D * D;
-        for (int by0 = R.y0; by0 <= R.y1; by0 += HBr) {
-            const int by1 = min(R.y1, by0 + HBr - 1);
-            const int cnt = (by1 - by0 + 1) * W;
-            __syncthreads();  // previous band flushed
-            for (int i = threadIdx.x; i < cnt; i += kRThreads) reg[i] = 0;
-            __syncthreads();
-            const int ya = max(ylo, by0), yb = min(yhi, by1);
-            if (ya <= yb) fwd_rows(reg - R.x0, by0, W, R.x0, R.x1, ya, yb, s, scale);
-            __syncthreads();
-            for (int i = threadIdx.x; i < cnt; i += kRThreads) {
-                const int v = reg[i];
-                if (v) {
-                    const int r = i / W;
-                    atomicAdd(dst + (int64_t)(by0 + r) * D + R.x0 + (i - r * W), v);
-                }
-            }
-        }
+    const PoseF P = load_pose_f(poses, b);
+    const int64_t i_begin = (int64_t)blockIdx.x * kRChunk;
+    const int64_t i_end = min(n, i_begin + kRChunk);
+    const int64_t stepA = (kRThreads * mulA) % n;
+    int64_t g = ((i_begin + threadIdx.x) % n) * mulA % n;
+    __syncthreads();
+    for (int64_t i = i_begin + threadIdx.x; i < i_end; i += kRThreads) {
+        const Splat2 s = project2(load_splat(splat, g), P, G);
+        g += stepA;
+        if (g >= n) g -= n;
+        if (!(s.w > 0.f)) continue;
+        const int ylo = max(max((int)ceilf(s.mpy - s.hy), 0), r0);
+        const int yhi = min(min((int)floorf(s.mpy + s.hy), D - 1), r1 - 1);
+        if (ylo <= yhi) fwd_rows(band, r0, D, 0, D - 1, ylo, yhi, s, scale);
+    }
+    __syncthreads();
+    int *dst = out + (int64_t)b * D * D + (int64_t)r0 * D;
+    for (int i = threadIdx.x; i < npx; i += kRThreads) {
+        const int v = band[i];
+        if (v) atomicAdd(dst + i, v);
     }
 }
 
@@ -224,6 +212,15 @@ __global__ void fixed_to_float_kernel(int *__restrict__ buf, int64_t count, cons
 
 using namespace cgs;
 
+// A multiplier coprime with n, near the golden ratio of n (a bijective stride)
+static int64_t scramble_multiplier(int64_t n) {
+    auto gcd = [](int64_t a, int64_t b) { while (b) { int64_t t = a % b; a = b; b = t; } return a; };
+    if (n < 3) return 1;
+    for (int64_t a = (int64_t)(0.6180339887 * (double)n) | 1; a > 1; a -= 2)
+        if (gcd(a, n) == 1) return a;
+    return 1;
+}
+
 extern "C" size_t cgs_render_workspace_bytes(int64_t n) {
     int64_t parts = (n + kWbBlock - 1) / kWbBlock;
     return (size_t)(2 * parts + 1) * sizeof(float);
@@ -239,11 +236,21 @@ extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, in
     const double h = 2.0 * grid.extent / grid.size;
     wbound_partial_kernel<<<parts, kWbBlock, 0, st>>>(splat, n, h, part);
     wbound_scale_kernel<<<1, 256, 0, st>>>(part, parts);
+    int HB = kRBandBytes / (D * (int)sizeof(int));
+    if (HB < 1) return CGS_ERR_UNSUPPORTED;
+    HB = HB > D ? D : HB;
+    const int bands = (D + HB - 1) / HB;
+    const size_t smem = (size_t)HB * D * sizeof(int);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(raster_fwd_atomic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
     const int64_t count = (int64_t)B * D * D;
     cudaMemsetAsync(out, 0, sizeof(int) * count, st);
-    dim3 g((unsigned)((n + kRThreads - 1) / kRThreads), (unsigned)((B + kRImagesPerCTA - 1) / kRImagesPerCTA));
-    raster_fwd_atomic_kernel<<<g, kRThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), part + 2 * parts,
-                                                      kRImagesPerCTA, reinterpret_cast<int *>(out));
+    dim3 g((unsigned)((n + kRChunk - 1) / kRChunk), (unsigned)B, (unsigned)bands);
+    raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), part + 2 * parts, HB,
+                                                         scramble_multiplier(n), reinterpret_cast<int *>(out));
     int rc = check_launch("raster_fwd_atomic_kernel");
     if (rc) return rc;
     const int64_t threads = (count + 3) / 4;
