@@ -107,6 +107,7 @@ struct Splat2 {
     float hx, hy;          // half-extents of the q < cutoff ellipse [px]
 };
 
+// fast approximate rcp/sqrt (MUFU, ~1 ulp): the raster tolerances are 1e-4/1e-3
 __device__ __forceinline__ Splat2 project2(const SplatRec &r, const PoseF &P, const GridF &G) {
     Splat2 s;
     // B2 = W[:2] M, mean2 = W[:2] mu + t  (splat.py:197-200), in pixel units
@@ -129,35 +130,35 @@ __device__ __forceinline__ Splat2 project2(const SplatRec &r, const PoseF &P, co
     float det = m01 * m01 + m02 * m02 + m12 * m12;
     float mid = 0.5f * (c00 + c11);
     float hd = 0.5f * (c00 - c11);
-    float rad = sqrtf(hd * hd + c01 * c01);
+    float rad = sqrt_approx(hd * hd + c01 * c01);
     float l1 = mid + rad;
-    float l2 = l1 > 0.f ? det / l1 : 0.f;
+    float l2 = l1 > 0.f ? __fdividef(det, l1) : 0.f;
     if (l2 < kEigenFloorPx2) {
         // floor the small eigenvalue, keep the eigenvector (splat.py:245-259)
         float a1 = fmaxf(l1, kEigenFloorPx2), a2 = kEigenFloorPx2;
         float vx = c01, vy = l1 - c00;
         float ux = l1 - c11, uy = c01;
         if (ux * ux + uy * uy > vx * vx + vy * vy) { vx = ux; vy = uy; }
-        float nn = sqrtf(vx * vx + vy * vy);
-        if (nn == 0.f) { vx = 1.f; vy = 0.f; } else { vx /= nn; vy /= nn; }
+        float nn2 = vx * vx + vy * vy;
+        if (nn2 == 0.f) { vx = 1.f; vy = 0.f; } else { const float inn = rsqrtf(nn2); vx *= inn; vy *= inn; }
         c00 = a1 * vx * vx + a2 * vy * vy;
         c01 = (a1 - a2) * vx * vy;
         c11 = a1 * vy * vy + a2 * vx * vx;
         det = a1 * a2;
     }
-    float inv_det = 1.f / det;
+    float inv_det = __fdividef(1.f, det);
     s.p00 = c11 * inv_det;
     s.p01 = -c01 * inv_det;
     s.p11 = c00 * inv_det;
-    s.cnorm = G.inv_2pi_h2 / sqrtf(det);
+    s.cnorm = G.inv_2pi_h2 * rsqrtf(det);
     s.w = r.amp * s.cnorm;
     s.A = -0.5f * kLog2e * s.p00;
     s.Bc = -kLog2e * s.p01;
     s.C = -0.5f * kLog2e * s.p11;
-    s.hx = sqrtf(kCutoffSq * c00);
-    s.hy = sqrtf(kCutoffSq * c11);
-    s.slope = s.p01 / s.p00;
-    s.k = 1.f / c11;
+    s.hx = sqrt_approx(kCutoffSq * c00);
+    s.hy = sqrt_approx(kCutoffSq * c11);
+    s.slope = __fdividef(s.p01, s.p00);
+    s.k = __fdividef(1.f, c11);
     s.Ck = -0.5f * kLog2e * s.k;
     s.inv_sqrt_p00 = rsqrtf(s.p00);
     return s;

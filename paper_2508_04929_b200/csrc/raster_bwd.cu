@@ -32,6 +32,7 @@ constexpr int kBwdThreadsDB = 512;       // double-buffered kernel: Gaussians pe
 constexpr int kBwdThreadsBand = 256;     // band kernel
 constexpr int kBandBytes = 96 * 1024;    // upstream rows staged per band
 constexpr int kDBMaxBytes = 200 * 1024;  // two whole images must fit
+constexpr int kRowPad = 4;                // floats of slack after every staging buffer (bwd_rows reads ahead)
 
 struct Moments {
     float e, g, x, y, xx, xy, yy;
@@ -72,7 +73,7 @@ __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, 
         if (rem <= 0.f) continue;
         const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
         const int xa = max((int)ceilf(xcv - half), xlo);
-        const int xb = min((int)floorf(xcv + half), xhi);
+        int xb = min((int)floorf(xcv + half), xhi);
         if (xa > xb) continue;
         const float dx = (float)xa - xcv;
         const float Ckdy2 = s.Ck * dy * dy;
@@ -84,15 +85,22 @@ __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, 
             float2 E = f2pack(e0, e0 * g0);
             float2 R = f2pack(g0 * g1, g1 * g1 * c);
             float2 DX = f2pack(dx, dx + 1.f);
-            int x = xa;
+            // software-pipelined: the next pair's loads issue before this
+            // pair's math (they may read up to 2 floats past the span; every
+            // staging buffer carries kRowPad floats of slack)
+            const float *p = row + xa;
+            float2 GP = f2pack(p[0], p[1]);
+            const float *pe = row + xb;
 #pragma unroll 1
-            for (; x < xb; x += 2) {
-                bwd_pair(a, f2pack(row[x], row[x + 1]), E, DX);
+            for (; p < pe; p += 2) {
+                const float2 GN = f2pack(p[2], p[3]);
+                bwd_pair(a, GP, E, DX);
                 f2scale(E, R);
                 f2scale(R, C4);
                 f2acc_add(DX, TWO);
+                GP = GN;
             }
-            if (x == xb) bwd_pair(a, f2pack(row[x], 0.f), E, DX);
+            if (p == pe) bwd_pair(a, f2pack(GP.x, 0.f), E, DX);
         } else {
             float d = dx;
             for (int x = xa; x <= xb; ++x, d += 1.f)
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(kBwdThreadsDB, 1) raster_bwd_db_kernel(
             s = project2(rec, P, G);
             footprint_rows(s, D, ylo, yhi);
         }
-        const float c2A = exp2f(2.f * s.A);
+        const float c2A = ex2_approx(2.f * s.A);
         mbar_wait(&bars[i & 1], (uint32_t)((i >> 1) & 1));
         Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bwd_rows(smem_db + (i & 1) * D * D, 0, D, 0, D - 1, ylo, yhi, s, c2A, M);
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(kBwdThreadsBand, 3) raster_bwd_band_kernel(
             s = project2(rec, P, G);
             footprint_rows(s, D, ylo, yhi);
         }
-        const float c2A = exp2f(2.f * s.A);
+        const float c2A = ex2_approx(2.f * s.A);
         Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int r0 = 0; r0 < D; r0 += HB) {
             const int r1 = min(D, r0 + HB);
@@ -280,7 +288,7 @@ constexpr int kRegFloats = 4096;  // 16 KB per band
 __global__ void __launch_bounds__(kRegThreads, 3) raster_bwd_region_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
-    __shared__ __align__(16) float reg[kRegFloats];
+    __shared__ __align__(16) float reg[kRegFloats + kRowPad];
     __shared__ int red[4 * (kRegThreads / 32)];
     const int D = G.D;
     const int64_t g = (int64_t)blockIdx.x * kRegThreads + threadIdx.x;
@@ -305,7 +313,7 @@ __global__ void __launch_bounds__(kRegThreads, 3) raster_bwd_region_kernel(
         if (R.x0 > R.x1) continue;  // uniform
         const int W = R.x1 - R.x0 + 1;
         const int HBr = max(1, kRegFloats / W);
-        const float c2A = exp2f(2.f * s.A);
+        const float c2A = ex2_approx(2.f * s.A);
         const float *src = upstream + (int64_t)b * D * D;
         Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int by0 = R.y0; by0 <= R.y1; by0 += HBr) {
@@ -378,7 +386,7 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
                                                             images_per_group);
         return check_launch("raster_bwd_region_kernel");
     }
-    const size_t db_bytes = 2 * (size_t)D * D * sizeof(float);
+    const size_t db_bytes = (2 * (size_t)D * D + kRowPad) * sizeof(float);
     const bool aligned = ((reinterpret_cast<uintptr_t>(upstream) & 15) == 0) && ((D * D) % 4 == 0);
     if (layout == CGS_LAYOUT_NATURAL && variant == 1 && db_bytes <= (size_t)kDBMaxBytes && aligned) {
         static size_t configured = 0;
@@ -394,7 +402,7 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
     int HB = kBandBytes / (D * (int)sizeof(float));
     if (HB < 1) return CGS_ERR_UNSUPPORTED;
     HB = HB > D ? D : HB;
-    const size_t smem = (size_t)HB * D * sizeof(float);
+    const size_t smem = ((size_t)HB * D + kRowPad) * sizeof(float);
     static size_t configured_band = 0;
     if (smem > 48 * 1024 && smem > configured_band) {
         cudaFuncSetAttribute(raster_bwd_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) wbound_scale_kernel(float *part, int npar
 __device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, int xlo, int xhi, int ya, int yb,
                                          const Splat2 &s, float scale) {
     const float wS = s.w * scale, wsubS = s.w * kSub * scale;
-    const float c = exp2f(2.f * s.A);  // g_{k+1} / g_k
+    const float c = ex2_approx(2.f * s.A);  // g_{k+1} / g_k
     const float c4 = (c * c) * (c * c);
     // v = wS e - wS sub + 1.5*2^23: the FFMA that evaluates the contribution
     // also places its rounded integer in the low mantissa bits (fast_rint)
