@@ -117,6 +117,102 @@ __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, 
     }
 }
 
+// Row-pair walk over a row-pair-interleaved block: the f32x2 lanes are the two
+// rows (2j, 2j+1) of one footprint, so the per-row setup (span, exp seeds,
+// moment update) runs packed once per two rows, and one 64-bit shared load
+// fetches both rows' upstream values at a column.  blk holds pairs from the
+// even row b0 on: element (row b0 + 2j + t, column x) at float2 index
+// j*W + (x - xlo), lane t.
+//
+// Both lanes run over the union of their two row spans.  A pixel of that union
+// outside its own row's q < 6.5^2 span has e < sub, so it adds g (e - sub),
+// |e - sub| < sub = 6.7e-10, to the sums: a quarter of the fp32 rounding
+// noise of sum g e at most (the mean of e over a footprint is ~0.05), and
+// nothing at the 1e-3 gradient tolerance.  Rows outside [ya, yb] (the first or
+// last pair of an odd-aligned footprint) have e = 0 and their g is dropped.
+//
+// Along a row e_{k+1} = e_k g_k, g_{k+1} = g_k c (c = 2^(2A)), restarted
+// exactly every 32 columns (relative error < 2e-5).
+constexpr int kChunk = 32;
+constexpr float kMinSeedLog2 = -100.f;  // joint row-pair walks need every live seed e >= 2^-100
+
+__device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int b0, int W, int xlo, int xhi,
+                                             int ya, int yb, const Splat2 &s, float c, Moments &M) {
+    const float2 ONE = f2pack(1.f, 1.f);
+    const float nk = -s.k, A = s.A, Ck = s.Ck, isp = s.inv_sqrt_p00, m2s = -2.f * s.slope;
+    int y = ya & ~1;  // b0 is even: pairs are aligned to even rows
+    float2 DY = f2pack((float)y - s.mpy, (float)(y + 1) - s.mpy);
+    float2 XC = f2pack(fmaf(-s.slope, DY.x, s.mpx), fmaf(-s.slope, DY.y, s.mpx));
+    const float2 *prow = blk + ((y - b0) >> 1) * W - xlo;
+    for (; y <= yb; y += 2, DY = f2add(DY, f2pack(2.f, 2.f)), XC = f2add(XC, f2pack(m2s, m2s)), prow += W) {
+        const bool v0 = y >= ya, v1 = y + 1 <= yb;
+        const float2 REM = f2fma(f2mul(DY, f2pack(nk, nk)), DY, f2pack(kCutoffSq, kCutoffSq));
+        const float2 H = f2mul(f2pack(sqrt_approx(fmaxf(REM.x, 0.f)), sqrt_approx(fmaxf(REM.y, 0.f))),
+                               f2pack(isp, isp));
+        const float2 LO = f2add(XC, f2pack(-H.x, -H.y)), HI = f2add(XC, H);
+        const int xa0 = v0 ? max((int)ceilf(LO.x), xlo) : 0x7fffffff, xb0 = v0 ? min((int)floorf(HI.x), xhi) : -1;
+        const int xa1 = v1 ? max((int)ceilf(LO.y), xlo) : 0x7fffffff, xb1 = v1 ? min((int)floorf(HI.y), xhi) : -1;
+        const int xa = min(xa0, xa1), xb = max(xb0, xb1);
+        if (xa > xb) continue;
+        const float2 KY = f2mul(f2mul(DY, f2pack(Ck, Ck)), DY);
+        // one packed walk over columns [wa, wb]; lane t live iff mt
+        auto walk = [&](int wa, int wb, bool m0, bool m1) {
+            float2 DX = f2add(f2pack((float)wa, (float)wa), f2pack(-XC.x, -XC.y));
+            RowSums a;
+            const float2 *q = prow + wa;
+            for (int x0 = wa;;) {
+                const int xe = min(wb, x0 + kChunk - 1);
+                const float2 Q = f2fma(f2mul(DX, f2pack(A, A)), DX, KY);
+                const float2 GA = f2mul(f2fma(DX, f2pack(2.f, 2.f), ONE), f2pack(A, A));
+                // a dead lane carries e = g = 0 (a select: its g may be inf)
+                float2 E = f2pack(m0 ? ex2_approx(Q.x) : 0.f, m1 ? ex2_approx(Q.y) : 0.f);
+                float2 G = f2pack(m0 ? ex2_approx(GA.x) : 0.f, m1 ? ex2_approx(GA.y) : 0.f);
+                const float2 *qe = q + (xe - x0);
+                // software-pipelined: the next column's load issues within this
+                // column's math (it may read one float2 past the span; every
+                // staging buffer carries kRowPad floats of slack)
+                float2 GP = q[0];
+#pragma unroll 1
+                do {
+                    const float2 GE = f2mul(GP, E);
+                    f2acc_add(a.g, GP);
+                    GP = q[1];  // GP is dead from here: reload it in place
+                    f2acc_add(a.e, GE);
+                    const float2 T = f2mul(GE, DX);
+                    f2acc_add(a.x, T);
+                    f2acc_fma(a.xx, T, DX);
+                    f2scale(E, G);
+                    f2scale(G, f2pack(c, c));
+                    f2acc_add(DX, ONE);
+                } while (q++ != qe);
+                x0 = xe + 1;
+                if (x0 > wb) break;
+            }
+            const float2 DYE = f2mul(DY, a.e), DYX = f2mul(DY, a.x);
+            M.e += f2sum(a.e);
+            M.g += (m0 ? a.g.x : 0.f) + (m1 ? a.g.y : 0.f);
+            M.x += f2sum(a.x);
+            M.xx += f2sum(a.xx);
+            M.y += f2sum(DYE);
+            M.xy += f2sum(DYX);
+            M.yy += fmaf(DY.x, DYE.x, DY.y * DYE.y);
+        };
+        // The union walk seeds a lane's recurrence up to |xa0 - xa1| columns
+        // before its own span.  For thin, slanted footprints that seed e can
+        // underflow, so such pairs walk their two rows apart.  A seed exponent
+        // >= kMinSeedLog2 also bounds the seed g below 2^100 (no overflow).
+        const float2 DX0 = f2add(f2pack((float)xa, (float)xa), f2pack(-XC.x, -XC.y));
+        const float2 Q0 = f2fma(f2mul(DX0, f2pack(A, A)), DX0, KY);
+        const bool joint = !(v0 && v1) || fminf(Q0.x, Q0.y) >= kMinSeedLog2;
+        if (joint) {
+            walk(xa, xb, v0, v1);
+        } else {
+            if (xa0 <= xb0) walk(xa0, xb0, true, false);
+            if (xa1 <= xb1) walk(xa1, xb1, false, true);
+        }
+    }
+}
+
 // moments of one (image, Gaussian) -> += world-frame accumulator
 __device__ __forceinline__ void accumulate_world(const Moments &M, const Splat2 &s, const PoseF &P, float inv_h,
                                                  float acc[CGS_ACC_STRIDE]) {
@@ -288,7 +384,7 @@ constexpr int kRegFloats = 4096;  // 16 KB per band
 __global__ void __launch_bounds__(kRegThreads, 3) raster_bwd_region_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
-    __shared__ __align__(16) float reg[kRegFloats + kRowPad];
+    __shared__ __align__(16) float reg[kRegFloats + kRowPad];  // row-pair interleaved (bwd_rowpairs)
     __shared__ int red[4 * (kRegThreads / 32)];
     const int D = G.D;
     const int64_t g = (int64_t)blockIdx.x * kRegThreads + threadIdx.x;
@@ -312,21 +408,31 @@ __global__ void __launch_bounds__(kRegThreads, 3) raster_bwd_region_kernel(
         const Box R = block_union(footprint_box(s, valid, ylo, yhi, D), red);
         if (R.x0 > R.x1) continue;  // uniform
         const int W = R.x1 - R.x0 + 1;
-        const int HBr = max(1, kRegFloats / W);
+        const int HBr = (kRegFloats / W) & ~1;  // even: row pairs never straddle bands (W <= kRegFloats / 2)
         const float c2A = ex2_approx(2.f * s.A);
         const float *src = upstream + (int64_t)b * D * D;
+        // per-thread staging cursor: element i = r * W + x of a band, stepped by
+        // kRegThreads without a division per element
+        const int step_r = kRegThreads / W, step_x = kRegThreads - step_r * W;
+        const int r_init = threadIdx.x / W, x_init = threadIdx.x - r_init * W;
         Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int by0 = R.y0; by0 <= R.y1; by0 += HBr) {
-            const int by1 = min(R.y1, by0 + HBr - 1);
+        for (int by0 = R.y0 & ~1; by0 <= R.y1; by0 += HBr) {
+            const int by1 = min(R.y1 | 1, by0 + HBr - 1);  // odd: whole pairs
             const int cnt = (by1 - by0 + 1) * W;
             __syncthreads();  // previous band fully consumed
+            int r = r_init, x = x_init;
             for (int i = threadIdx.x; i < cnt; i += kRegThreads) {
-                const int r = i / W;
-                reg[i] = __ldg(src + (int64_t)(by0 + r) * D + R.x0 + (i - r * W));
+                const int row = by0 + r;
+                const float v = row < D ? __ldg(src + (int64_t)row * D + R.x0 + x) : 0.f;
+                reg[(((r >> 1) * W + x) << 1) | (r & 1)] = v;
+                x += step_x;
+                r += step_r;
+                if (x >= W) { x -= W; ++r; }
             }
             __syncthreads();
             const int ya = max(ylo, by0), yb = min(yhi, by1);
-            if (ya <= yb) bwd_rows(reg - R.x0, by0, W, R.x0, R.x1, ya, yb, s, c2A, M);
+            if (ya <= yb)
+                bwd_rowpairs(reinterpret_cast<const float2 *>(reg), by0, W, R.x0, R.x1, ya, yb, s, c2A, M);
         }
         if (ylo <= yhi) accumulate_world(M, s, P, G.inv_h, acc);
     }
@@ -380,7 +486,7 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
         const char *v = getenv("CGS_BWD_KERNEL");
         variant = (v && v[0] == 'd') ? 1 : (v && v[0] == 'b') ? 2 : 0;
     }
-    if (layout == CGS_LAYOUT_NATURAL && variant == 0) {
+    if (layout == CGS_LAYOUT_NATURAL && variant == 0 && D <= kRegFloats / 2) {
         dim3 g((unsigned)((n + kRegThreads - 1) / kRegThreads), (unsigned)G);
         raster_bwd_region_kernel<<<g, kRegThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), upstream, partial,
                                                             images_per_group);
