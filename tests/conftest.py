@@ -36,7 +36,9 @@ def oracle():
 def rel_l2(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
-    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+    err = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+    _log_margin("rel_l2", err, float("nan"))
+    return err
 
 
 def grads_close(a, b, rtol, floor_frac):
@@ -54,5 +56,16 @@ def grads_close(a, b, rtol, floor_frac):
     for j in range(b.shape[1]):
         den = max(np.linalg.norm(b[:, j]), floor)
         errs.append(float(np.linalg.norm(a[:, j] - b[:, j]) / den))
+    _log_margin("grads", max(errs), rtol)
     assert max(errs) <= rtol, errs
     return errs
+
+
+def _log_margin(kind, err, tol):
+    """Append (test, kind, worst error, tolerance) to $CGS_MARGIN_LOG when set: the
+    precision margin of every parity check, tracked across kernel changes."""
+    path = os.environ.get("CGS_MARGIN_LOG")
+    if path:
+        test = os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
+        with open(path, "a") as f:
+            f.write(f"{test}\t{kind}\t{err:.3e}\t{tol:.1e}\n")
