@@ -13,6 +13,7 @@ constexpr double kCutoffSqD = kCullSigma * kCullSigma;
 constexpr float kCutoffSq = 42.25f;
 constexpr double kPiD = 3.14159265358979323846;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kEigenFloorPx2 = 0.01f;            // (EIGEN_FLOOR_FRACTION * h)^2 / h^2, splat.py:55
 // sub = exp(-cutoff_sq / 2) (splat.py:51) as the fp32 boundary value
 constexpr float kSub = 6.6915861e-10f;

@@ -405,10 +405,16 @@ __global__ void __launch_bounds__(kBwdThreadsBand, 3) raster_bwd_band_kernel(
 // Gaussians in spatial order the region is a few hundred pixels, so shared
 // memory stays small and several CTAs share an SM; in any order it is correct
 // (the region then grows to the whole image and is processed band by band).
-constexpr int kRegThreads = 256;
+#ifndef CGS_BWD_REG_THREADS
+#define CGS_BWD_REG_THREADS 256
+#endif
+#ifndef CGS_BWD_MINB
+#define CGS_BWD_MINB 3
+#endif
+constexpr int kRegThreads = CGS_BWD_REG_THREADS;
 constexpr int kRegFloats = 4096;  // 16 KB per band
 
-__global__ void __launch_bounds__(kRegThreads, 3) raster_bwd_region_kernel(
+__global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
     __shared__ __align__(16) float reg[kRegFloats + kRowPad];  // row-pair interleaved (bwd_rowpairs)

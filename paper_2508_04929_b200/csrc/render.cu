@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) wbound_scale_kernel(float *part, int npar
 // Add one footprint's rows [ya, yb] into the int32 block at acc (pixel (r0, 0),
 // row stride ld), columns clipped to [xlo, xhi].
 __device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, int xlo, int xhi, int ya, int yb,
-                                         const Splat2 &s, float scale) {
+                                         const Splat2 &s, float scale, float cut) {
     const float wS = s.w * scale, wsubS = s.w * kSub * scale;
     const float c = ex2_approx(2.f * s.A);  // g_{k+1} / g_k
     const float c4 = (c * c) * (c * c);
@@ -122,7 +122,7 @@ __device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, 
     float xcv = fmaf(-s.slope, dy, s.mpx);
     int *row = acc + (ya - r0) * ld;
     for (int iy = ya; iy <= yb; ++iy, dy += 1.f, xcv -= s.slope, row += ld) {
-        const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
+        const float rem = fmaf(-s.k * dy, dy, cut);
         if (rem <= 0.f) continue;
         const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
         const int xa = max((int)ceilf(xcv - half), xlo);
@@ -183,9 +183,17 @@ __global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
         g += stepA;
         if (g >= n) g -= n;
         if (!(s.w > 0.f)) continue;
-        const int ylo = max(max((int)ceilf(s.mpy - s.hy), 0), r0);
-        const int yhi = min(min((int)floorf(s.mpy + s.hy), D - 1), r1 - 1);
-        if (ylo <= yhi) fwd_rows(band, r0, D, 0, D - 1, ylo, yhi, s, scale);
+        // Contribution-exact footprint: a pixel adds round(wS (e - sub)) units,
+        // which is 0 wherever e < sub + 0.5 / wS.  Walk only q < cut with
+        // e(cut) = sub + 0.4995 / wS (the 1e-3 margin keeps every pixel that
+        // can round to >= 1 unit): the same integer image, far fewer updates.
+        const float thr = kSub + 0.4995f / (s.w * scale);
+        if (!(thr < 1.f)) continue;
+        const float cut = fminf(kCutoffSq, -2.f * kLn2 * __log2f(thr));
+        const float hy = s.hy * sqrt_approx(cut * (1.f / kCutoffSq));
+        const int ylo = max(max((int)ceilf(s.mpy - hy), 0), r0);
+        const int yhi = min(min((int)floorf(s.mpy + hy), D - 1), r1 - 1);
+        if (ylo <= yhi) fwd_rows(band, r0, D, 0, D - 1, ylo, yhi, s, scale, cut);
     }
     __syncthreads();
     int *dst = out + (int64_t)b * D * D + (int64_t)r0 * D;
