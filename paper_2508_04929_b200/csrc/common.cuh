@@ -199,27 +199,29 @@ __device__ __forceinline__ Box footprint_box(const Splat2 &s, bool live, int ylo
     return b;
 }
 
-// Union of every thread's box; red is shared scratch of 4 x (blockDim/32) ints.
-// Contains __syncthreads: call from all threads.
-__device__ __forceinline__ Box block_union(const Box &b, int *red) {
+// Union of every thread's box.  red is shared scratch of 8 x (blockDim/32)
+// ints used in two halves by call parity, so one barrier per call suffices:
+// the half written now was last read two calls ago, before the previous call's
+// barrier.  That barrier also orders everything each thread did before the
+// call ahead of everything after it (callers rely on it).  Needs blockDim <= 1024.
+__device__ __forceinline__ Box block_union(const Box &b, int *red, int parity) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int x0 = __reduce_min_sync(0xffffffffu, b.x0), y0 = __reduce_min_sync(0xffffffffu, b.y0);
     const int x1 = __reduce_max_sync(0xffffffffu, b.x1), y1 = __reduce_max_sync(0xffffffffu, b.y1);
-    __syncthreads();  // earlier readers of red are done
+    int *rr = red + (parity & 1) * 4 * nw;
     if (lane == 0) {
-        red[warp] = x0;
-        red[nw + warp] = x1;
-        red[2 * nw + warp] = y0;
-        red[3 * nw + warp] = y1;
+        rr[warp] = x0;
+        rr[nw + warp] = x1;
+        rr[2 * nw + warp] = y0;
+        rr[3 * nw + warp] = y1;
     }
     __syncthreads();
-    Box r{0x7fffffff, -1, 0x7fffffff, -1};
-    for (int w = 0; w < nw; ++w) {
-        r.x0 = min(r.x0, red[w]);
-        r.x1 = max(r.x1, red[nw + w]);
-        r.y0 = min(r.y0, red[2 * nw + w]);
-        r.y1 = max(r.y1, red[3 * nw + w]);
-    }
+    const bool in = lane < nw;
+    Box r;
+    r.x0 = __reduce_min_sync(0xffffffffu, in ? rr[lane] : 0x7fffffff);
+    r.x1 = __reduce_max_sync(0xffffffffu, in ? rr[nw + lane] : -1);
+    r.y0 = __reduce_min_sync(0xffffffffu, in ? rr[2 * nw + lane] : 0x7fffffff);
+    r.y1 = __reduce_max_sync(0xffffffffu, in ? rr[3 * nw + lane] : -1);
     return r;
 }
 

@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
     __shared__ __align__(16) float reg[kRegFloats + kRowPad];  // row-pair interleaved (bwd_rowpairs)
-    __shared__ int red[4 * (kRegThreads / 32)];
+    __shared__ int red[8 * (kRegThreads / 32)];
     const int D = G.D;
     const int64_t g = (int64_t)blockIdx.x * kRegThreads + threadIdx.x;
     const bool valid = g < n;
@@ -438,10 +438,13 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
             s = project2(rec, P, G);
             footprint_rows(s, D, ylo, yhi);
         }
-        const Box R = block_union(footprint_box(s, valid, ylo, yhi, D), red);
+        // its barrier also retires every thread's reads of reg for the previous image
+        const Box R = block_union(footprint_box(s, valid, ylo, yhi, D), red, b);
         if (R.x0 > R.x1) continue;  // uniform
         const int W = R.x1 - R.x0 + 1;
-        const int HBr = (kRegFloats / W) & ~1;  // even: row pairs never straddle bands (W <= kRegFloats / 2)
+        // rows per band, even so row pairs never straddle bands (W <= kRegFloats / 2);
+        // the division only runs for regions larger than one band
+        const int HBr = ((R.y1 | 1) - (R.y0 & ~1) + 1) * W <= kRegFloats ? D + 2 : (kRegFloats / W) & ~1;
         const float c2A = ex2_approx(2.f * s.A);
         const float *src = upstream + (int64_t)b * D * D;
         Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
         for (int by0 = R.y0 & ~1; by0 <= R.y1; by0 += HBr) {
             const int by1 = min(R.y1 | 1, by0 + HBr - 1);  // odd: whole pairs
             const int np = (by1 - by0 + 1) >> 1;
-            __syncthreads();  // previous band fully consumed
+            if (by0 != (R.y0 & ~1)) __syncthreads();  // previous band fully consumed (block_union covers the first)
             // a warp per row pair, lanes along columns: coalesced row loads,
             // one 64-bit store of both rows per column
             for (int j = threadIdx.x >> 5; j < np; j += kRegThreads / 32) {
