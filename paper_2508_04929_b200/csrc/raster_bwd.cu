@@ -409,9 +409,10 @@ __global__ void __launch_bounds__(kBwdThreadsBand, 3) raster_bwd_band_kernel(
 #define CGS_BWD_REG_THREADS 256
 #endif
 #ifndef CGS_BWD_MINB
-#define CGS_BWD_MINB 3
+#define CGS_BWD_MINB 4
 #endif
 constexpr int kRegThreads = CGS_BWD_REG_THREADS;
+constexpr int kMaxPoseImages = 64;  // image groups up to this size keep fp32 poses in shared memory
 constexpr int kRegFloats = 4096;  // 16 KB per band
 
 __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_kernel(
@@ -419,23 +420,42 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
     __shared__ __align__(16) float reg[kRegFloats + kRowPad];  // row-pair interleaved (bwd_rowpairs)
     __shared__ int red[8 * (kRegThreads / 32)];
+    // Register budget: the walk needs ~40 registers, so per-thread state that
+    // is touched once per image lives outside the register file: the world
+    // accumulator in shared memory (column-major: conflict-free), poses as fp32
+    // in shared memory, and the splat record re-read from L1 each image.
+    __shared__ float accs[CGS_ACC_STRIDE * kRegThreads];
+    __shared__ float poses_f[kMaxPoseImages * 8];
     const int D = G.D;
     const int64_t g = (int64_t)blockIdx.x * kRegThreads + threadIdx.x;
     const bool valid = g < n;
     const int grp = blockIdx.y;
     const int b_begin = grp * ipg, b_end = min(B, b_begin + ipg);
-    SplatRec rec{};
-    if (valid) rec = load_splat(splat, g);
-    float acc[CGS_ACC_STRIDE];
+    const bool pose_smem = b_end - b_begin <= kMaxPoseImages;
+    if (pose_smem)
+        for (int i = threadIdx.x; i < (b_end - b_begin) * 8; i += kRegThreads) {
+            const int k = i & 7;
+            poses_f[i] = (float)poses[12 * (int64_t)(b_begin + (i >> 3)) + (k < 6 ? k : k + 3)];
+        }
 #pragma unroll
-    for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = 0.f;
+    for (int c = 0; c < CGS_ACC_STRIDE; ++c) accs[c * kRegThreads + threadIdx.x] = 0.f;
+    for (int i = threadIdx.x; i < kRegFloats + kRowPad; i += kRegThreads) reg[i] = 0.f;  // finite reads past spans
+    __syncthreads();
+    auto pose = [&](int b) {
+        if (!pose_smem) return load_pose_f(poses, b);
+        const float *q = poses_f + 8 * (b - b_begin);
+        PoseF P;
+        P.w0[0] = q[0]; P.w0[1] = q[1]; P.w0[2] = q[2];
+        P.w1[0] = q[3]; P.w1[1] = q[4]; P.w1[2] = q[5];
+        P.tx = q[6]; P.ty = q[7];
+        return P;
+    };
 
     for (int b = b_begin; b < b_end; ++b) {
-        const PoseF P = load_pose_f(poses, b);
         Splat2 s{};
         int ylo = 1, yhi = 0;
         if (valid) {
-            s = project2(rec, P, G);
+            s = project2(load_splat(splat, g), pose(b), G);
             footprint_rows(s, D, ylo, yhi);
         }
         // its barrier also retires every thread's reads of reg for the previous image
@@ -467,9 +487,21 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
             if (ya <= yb)
                 bwd_rowpairs(reinterpret_cast<const float2 *>(reg), by0, W, R.x0, R.x1, ya, yb, s, c2A, M);
         }
-        if (ylo <= yhi) accumulate_world(M, s, P, G.inv_h, acc);
+        if (ylo <= yhi) {
+            float acc[CGS_ACC_STRIDE];
+#pragma unroll
+            for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = accs[c * kRegThreads + threadIdx.x];
+            accumulate_world(M, s, pose(b), G.inv_h, acc);
+#pragma unroll
+            for (int c = 0; c < CGS_ACC_STRIDE; ++c) accs[c * kRegThreads + threadIdx.x] = acc[c];
+        }
     }
-    if (valid) store_partial(partial, grp, n, g, acc);
+    if (valid) {
+        float acc[CGS_ACC_STRIDE];
+#pragma unroll
+        for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = accs[c * kRegThreads + threadIdx.x];
+        store_partial(partial, grp, n, g, acc);
+    }
 }
 
 // In-ellipse pair count per image (same row spans as the backward).
