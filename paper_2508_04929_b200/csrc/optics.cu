@@ -13,6 +13,7 @@
 #include <cufft.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 
 #include "common.cuh"
@@ -184,6 +185,277 @@ __global__ void __launch_bounds__(1024) loss_resid_kernel(const float *__restric
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fused CTF -> MSE -> CTF^T for D = 32 R (R = 1, 2, 4), one CTA per PAIR of
+// images, everything in shared memory: render + obs in, upstream + loss out.
+// cuFFT needs 4 passes over HBM per transform plus the multiply kernels
+// (~0.15 ms for a 256-image C2 batch); this kernel reads each input once and
+// writes the upstream once.
+//
+// Two real images share one complex transform: z = a + i b.  With
+// Z = FFT2(z), A(k) = (Z(k) + conj Z(-k)) / 2, B(k) = (Z(k) - conj Z(-k)) / 2i,
+// and the real, even filters H1, H2 (H_sym, see top of file):
+//   W(k) = H1 A + i H2 B = P Z(k) + Q conj Z(-k),  P = (H1+H2)/2, Q = (H1-H2)/2
+// so IFFT2(W) = filt_H1(a) + i filt_H2(b) exactly: the reference's
+// Re(ifft2(H fft2(x))) for both images from one forward and one inverse
+// transform.  The residuals (2/D^2 (model - obs), train.py:153) are packed the
+// same way for the CTF^T pass (H is real and even, so CTF^T = CTF).
+//
+// 1-D transforms run one per warp on a row or column of the padded smem array:
+// lane l holds x[l + 32 j], j < R; a radix-R DIF step in registers (with
+// twiddles W_D^{l m}) then a 32-point DIF across lanes by shuffles leaves
+// X[m + R bitrev5(l)] in lane l, element m, stored back where it was loaded
+// from.  The spectrum therefore lives in that permuted order, and the inverse
+// runs the exact mirror network (DIT, conjugate twiddles), which takes the
+// permuted order back to natural order.  The 1/D^2 of the inverse is folded
+// into P and Q.
+template <int R>
+struct WarpFft {
+    float2 tw1[R];  // W_D^{l m}
+    float2 tws[5];  // lane stage s = 16 >> st: W_{2s}^{l mod s} on upper lanes, 1 on lower
+    float sg[5];    // +1 lower lane, -1 upper lane
+
+    __device__ __forceinline__ void init(int lane) {
+        constexpr int D = 32 * R;
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            float sn, cs;
+            sincospif(-2.f * (float)(lane * m) / (float)D, &sn, &cs);
+            tw1[m] = make_float2(cs, sn);
+        }
+#pragma unroll
+        for (int st = 0; st < 5; ++st) {
+            const int s = 16 >> st;
+            const bool up = (lane & s) != 0;
+            float sn = 0.f, cs = 1.f;
+            if (up) sincospif(-(float)(lane & (s - 1)) / (float)s, &sn, &cs);
+            tws[st] = make_float2(cs, sn);
+            sg[st] = up ? -1.f : 1.f;
+        }
+    }
+    static __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+        return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    }
+    static __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+        return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+    }
+    static __device__ __forceinline__ float2 shfl(float2 v, int s) {
+        return make_float2(__shfl_xor_sync(0xffffffffu, v.x, s), __shfl_xor_sync(0xffffffffu, v.y, s));
+    }
+    // radix-R DFT across the register elements, sign -1 (forward) or +1 (inverse, unscaled)
+    template <int SIGN>
+    static __device__ __forceinline__ void dft_r(float2 v[R]) {
+        if constexpr (R == 2) {
+            const float2 a = v[0], b = v[1];
+            v[0] = make_float2(a.x + b.x, a.y + b.y);
+            v[1] = make_float2(a.x - b.x, a.y - b.y);
+        } else if constexpr (R == 4) {
+            const float2 a = v[0], b = v[1], c = v[2], d = v[3];
+            const float2 s0 = make_float2(a.x + c.x, a.y + c.y), d0 = make_float2(a.x - c.x, a.y - c.y);
+            const float2 s1 = make_float2(b.x + d.x, b.y + d.y), d1 = make_float2(b.x - d.x, b.y - d.y);
+            // SIGN -1: X1 = d0 - i d1, X3 = d0 + i d1; SIGN +1 swaps them
+            const float2 mi = make_float2(d0.x + d1.y, d0.y - d1.x), pi = make_float2(d0.x - d1.y, d0.y + d1.x);
+            v[0] = make_float2(s0.x + s1.x, s0.y + s1.y);
+            v[2] = make_float2(s0.x - s1.x, s0.y - s1.y);
+            v[1] = SIGN < 0 ? mi : pi;
+            v[3] = SIGN < 0 ? pi : mi;
+        }
+    }
+    __device__ __forceinline__ void fwd(float2 v[R]) const {
+        dft_r<-1>(v);
+#pragma unroll
+        for (int m = 1; m < R; ++m) v[m] = cmul(v[m], tw1[m]);
+#pragma unroll
+        for (int st = 0; st < 5; ++st) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                const float2 p = shfl(v[m], 16 >> st);
+                const float2 t = make_float2(fmaf(sg[st], v[m].x, p.x), fmaf(sg[st], v[m].y, p.y));
+                v[m] = cmul(t, tws[st]);
+            }
+        }
+    }
+    __device__ __forceinline__ void inv(float2 v[R]) const {  // unscaled: D x the inverse DFT
+#pragma unroll
+        for (int st = 4; st >= 0; --st) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                const float2 t = cmulc(v[m], tws[st]);
+                const float2 p = shfl(t, 16 >> st);
+                v[m] = make_float2(fmaf(sg[st], t.x, p.x), fmaf(sg[st], t.y, p.y));
+            }
+        }
+#pragma unroll
+        for (int m = 1; m < R; ++m) v[m] = cmulc(v[m], tw1[m]);
+        dft_r<1>(v);
+    }
+};
+
+__device__ __forceinline__ int bitrev5(int l) { return (int)(__brev((unsigned)l) >> 27); }
+
+constexpr int kFusedThreads = 512;
+
+// One pass of 1-D transforms over all rows (COLS = false) or columns of Z.
+template <int R, bool INV, bool COLS>
+__device__ __forceinline__ void fft_pass(float2 *Z, int P, const WarpFft<R> &F) {
+    constexpr int D = 32 * R;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r = warp; r < D; r += kFusedThreads / 32) {
+        float2 v[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) v[j] = COLS ? Z[(lane + 32 * j) * P + r] : Z[r * P + lane + 32 * j];
+        if (INV) F.inv(v); else F.fwd(v);
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            if (COLS) Z[(lane + 32 * j) * P + r] = v[j];
+            else Z[r * P + lane + 32 * j] = v[j];
+        }
+    }
+}
+
+// position p (0..D-1) of the permuted spectrum <-> frequency index k
+template <int R>
+__device__ __forceinline__ int perm_k(int p) { return (p >> 5) + R * bitrev5(p & 31); }
+template <int R>
+__device__ __forceinline__ int perm_p(int k) { return bitrev5(k / R) + 32 * (k % R); }
+
+// H_sym at frequency index (ky, kx) of the full D x D grid
+__device__ __forceinline__ float ctf_sym(const CtfConst &c, int D, int ky, int kx) {
+    const int c0 = D / 2;
+    const int fy = ky < D - c0 ? ky : ky - D, fx = kx < D - c0 ? kx : kx - D;
+    float H = ctf_value_fast(c, fy, fx);
+    if ((D % 2 == 0) && (fy == -c0 || fx == -c0))
+        H = 0.5f * (H + ctf_value_fast(c, wrap_freq(fy, D, c0), wrap_freq(fx, D, c0)));
+    return H;
+}
+
+// W(k) = P Z(k) + Q conj Z(-k) over the permuted spectrum, pairs (k, -k) at once
+template <int R>
+__device__ __forceinline__ void ctf_combine(float2 *Z, int P, const CtfConst *cc, bool two, float norm) {
+    constexpr int D = 32 * R;
+    for (int idx = threadIdx.x; idx < D * D; idx += kFusedThreads) {
+        const int py = idx / D, px = idx - py * D;
+        const int ky = perm_k<R>(py), kx = perm_k<R>(px);
+        const int ny = ky ? D - ky : 0, nx = kx ? D - kx : 0;
+        const int qy = perm_p<R>(ny), qx = perm_p<R>(nx);
+        const int idx2 = qy * D + qx;
+        if (idx2 < idx) continue;  // the partner's thread handles the pair
+        const float h1 = ctf_sym(cc[0], D, ky, kx), h2 = two ? ctf_sym(cc[1], D, ky, kx) : 0.f;
+        const float Pc = 0.5f * (h1 + h2) * norm, Qc = 0.5f * (h1 - h2) * norm;
+        const float2 z1 = Z[py * P + px], z2 = Z[qy * P + qx];
+        Z[py * P + px] = make_float2(Pc * z1.x + Qc * z2.x, Pc * z1.y - Qc * z2.y);
+        if (idx2 != idx) Z[qy * P + qx] = make_float2(Pc * z2.x + Qc * z1.x, Pc * z2.y - Qc * z1.y);
+    }
+}
+
+__device__ __forceinline__ double block_sum_f64(double v, double *scratch) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < kFusedThreads / 32; ++w) t += scratch[w];
+    return t;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kFusedThreads, 1) ctf_mse_fused_kernel(
+    const float *__restrict__ render, const float *__restrict__ obs, int B, double pix,
+    const double *__restrict__ ctf, float *__restrict__ model, float *__restrict__ upstream,
+    double *__restrict__ loss, int32_t *status) {
+    constexpr int D = 32 * R, P = D + 1;  // padded rows: conflict-free column passes
+    extern __shared__ float2 Z[];
+    __shared__ CtfConst cc[2];
+    __shared__ double scratch[kFusedThreads / 32];
+    const int b0 = 2 * blockIdx.x;
+    const bool two = b0 + 1 < B;
+    if (threadIdx.x < 2 && (threadIdx.x == 0 || two)) {
+        CtfConst c = load_ctf(ctf + 8 * (int64_t)(b0 + threadIdx.x), D, pix);
+        c.inv_dA = 1.0 / c.dA;
+        c.pl = kPiD * c.lam;
+        c.cs3 = 0.5 * kPiD * c.cs * c.lam * c.lam * c.lam;
+        cc[threadIdx.x] = c;
+    }
+    WarpFft<R> F;
+    F.init(threadIdx.x & 31);
+    const float *r1 = render + (int64_t)b0 * D * D, *r2 = r1 + D * D;
+    for (int i = threadIdx.x; i < D * D; i += kFusedThreads) {
+        const int y = i / D, x = i - y * D;
+        Z[y * P + x] = make_float2(r1[i], two ? r2[i] : 0.f);
+    }
+    __syncthreads();
+    const float norm = 1.f / (float)(D * D);
+    // model = CTF (render)
+    fft_pass<R, false, false>(Z, P, F);
+    __syncthreads();
+    fft_pass<R, false, true>(Z, P, F);
+    __syncthreads();
+    ctf_combine<R>(Z, P, cc, two, norm);
+    __syncthreads();
+    fft_pass<R, true, true>(Z, P, F);
+    __syncthreads();
+    fft_pass<R, true, false>(Z, P, F);
+    __syncthreads();
+    // residual 2/D^2 (model - obs), loss = mean (model - obs)^2 in fp64
+    const float *o1 = obs + (int64_t)b0 * D * D, *o2 = o1 + D * D;
+    const float sc = 2.f * norm;
+    double a1 = 0.0, a2 = 0.0;
+    for (int i = threadIdx.x; i < D * D; i += kFusedThreads) {
+        const int y = i / D, x = i - y * D;
+        const float2 m = Z[y * P + x];
+        if (model) {
+            model[(int64_t)b0 * D * D + i] = m.x;
+            if (two) model[(int64_t)(b0 + 1) * D * D + i] = m.y;
+        }
+        const float d1 = m.x - o1[i], d2 = two ? m.y - o2[i] : 0.f;
+        a1 += (double)d1 * d1;
+        a2 += (double)d2 * d2;
+        Z[y * P + x] = make_float2(sc * d1, sc * d2);
+    }
+    a1 = block_sum_f64(a1, scratch);
+    a2 = block_sum_f64(a2, scratch);
+    if (threadIdx.x == 0) {
+        const double l1 = a1 / (double)(D * D), l2 = a2 / (double)(D * D);
+        loss[b0] = l1;
+        if (two) loss[b0 + 1] = l2;
+        if (status && (!isfinite(l1) || (two && !isfinite(l2)))) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
+    }
+    // upstream = CTF^T (residual)
+    fft_pass<R, false, false>(Z, P, F);
+    __syncthreads();
+    fft_pass<R, false, true>(Z, P, F);
+    __syncthreads();
+    ctf_combine<R>(Z, P, cc, two, norm);
+    __syncthreads();
+    fft_pass<R, true, true>(Z, P, F);
+    __syncthreads();
+    fft_pass<R, true, false>(Z, P, F);
+    __syncthreads();
+    float *u1 = upstream + (int64_t)b0 * D * D, *u2 = u1 + D * D;
+    for (int i = threadIdx.x; i < D * D; i += kFusedThreads) {
+        const int y = i / D, x = i - y * D;
+        const float2 u = Z[y * P + x];
+        u1[i] = u.x;
+        if (two) u2[i] = u.y;
+    }
+}
+
+template <int R>
+static int launch_ctf_mse_fused(const float *render, const float *obs, int B, double pix, const double *ctf,
+                                float *model, float *upstream, double *loss, int32_t *status, cudaStream_t st) {
+    constexpr int D = 32 * R;
+    const size_t smem = (size_t)D * (D + 1) * sizeof(float2);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(ctf_mse_fused_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    ctf_mse_fused_kernel<R><<<(B + 1) / 2, kFusedThreads, smem, st>>>(render, obs, B, pix, ctf, model, upstream,
+                                                                      loss, status);
+    return check_launch("ctf_mse_fused_kernel");
+}
+
 struct FftPlan {
     cufftHandle r2c, c2r;
     int D, B;
@@ -276,6 +548,15 @@ extern "C" int cgs_ctf_mse(void *plan, const float *render, const float *obs, in
                            float *upstream, double *loss, int32_t *status, int32_t layout,
                            void *stream) {
     if (!render || !obs || !upstream || !loss) return CGS_ERR_ARG;
+    // fused single-kernel path for D = 64 / 128 (CGS_CTF_CUFFT=1 forces cuFFT, for A/B)
+    static const bool force_cufft = getenv("CGS_CTF_CUFFT") && getenv("CGS_CTF_CUFFT")[0] == '1';
+    if (ctf && !force_cufft && render != upstream && grid.pixel_size > 0 && B > 0) {
+        cudaStream_t st = (cudaStream_t)stream;
+        if (grid.size == 128)
+            return launch_ctf_mse_fused<4>(render, obs, B, grid.pixel_size, ctf, model, upstream, loss, status, st);
+        if (grid.size == 64)
+            return launch_ctf_mse_fused<2>(render, obs, B, grid.pixel_size, ctf, model, upstream, loss, status, st);
+    }
     const float *m = render;
     if (ctf) {
         float *dst = model ? model : upstream;

@@ -281,6 +281,42 @@ def test_ctf_evaluate_and_apply():
         assert rel_l2(out2, c[f"ctf{i}_applied"]) < 1e-5
 
 
+@pytest.mark.parametrize("D", [64, 128])
+def test_fused_ctf_mse_matches_oracle(oracle, D):
+    """K4 as one kernel per image pair (optics.cu ctf_mse_fused_kernel): model,
+    loss and CTF^T upstream against the reference's centred complex FFTs, with an
+    odd batch (a half-empty pair), astigmatism (Nyquist H_sym), phase shift and
+    B-factor."""
+    B = 3
+    grid = oracle.Grid(D, 0.5, 1.5)
+    rng = np.random.default_rng(D)
+    render = rng.standard_normal((B, D, D)).astype(np.float32)
+    obs = rng.standard_normal((B, D, D)).astype(np.float32)
+    ctfs = [oracle.Ctf(12000.0, 15000.0, 0.7), oracle.Ctf(20000.0, 18000.0, -0.3, phase_shift=0.4),
+            oracle.Ctf(9000.0, 9500.0, 1.2, b_factor=40.0)]
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(D, grid.extent, grid.pixel_size)
+    r, o = _dev(render, torch.float32), _dev(obs, torch.float32)
+    c = _dev(np.stack([x.as_array() for x in ctfs]), torch.float64)
+    model = torch.empty_like(r)
+    up = torch.empty_like(r)
+    loss = torch.empty(B, dtype=torch.float64, device=r.device)
+    status = torch.zeros(1, dtype=torch.int32, device=r.device)
+    spec = torch.empty(2 * int(ctx.lib.cgs_fft_spectrum_elems(D, B)), dtype=torch.float32, device=r.device)
+    _lib.call("cgs_ctf_mse", ctx.plan(D, B), r.data_ptr(), o.data_ptr(), B, gs, c.data_ptr(), spec.data_ptr(),
+              model.data_ptr(), up.data_ptr(), loss.data_ptr(), status.data_ptr(), _lib.CGS_LAYOUT_NATURAL,
+              ctx.stream)
+    torch.cuda.synchronize()
+    for b in range(B):
+        H = oracle.ctf_evaluate(ctfs[b], grid)
+        m_ref = oracle.apply_ctf(render[b].astype(np.float64), H)
+        u_ref = oracle.apply_ctf((2.0 / (D * D)) * (m_ref - obs[b]), H)
+        assert rel_l2(model[b].cpu().numpy(), m_ref) < 1e-5
+        assert rel_l2(up[b].cpu().numpy(), u_ref) < 1e-5
+        assert abs(loss[b].item() - oracle.loss_mse(m_ref, obs[b])) <= 1e-5 * oracle.loss_mse(m_ref, obs[b])
+    assert status.item() == 0
+
+
 def _full_step_device(params, poses, grid, obs, ctfs, render="direct"):
     """Run the engine's fused K0..K5 + epilogue grads for a batch; return (losses, grads)."""
     ctx = engine.DeviceContext.get()
