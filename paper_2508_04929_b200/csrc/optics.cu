@@ -98,7 +98,7 @@ __device__ __forceinline__ float ctf_value_fast(const CtfConst &c, int fy, int f
     double chi = c.pl * dk2 - c.cs3 * k2 * k2 + c.phase;
     chi -= 6.283185307179586 * rint(chi * 0.15915494309189535);
     float sn, cs;
-    sincosf((float)chi, &sn, &cs);
+    __sincosf((float)chi, &sn, &cs);  // |chi| <= pi: MUFU sin/cos, abs error < 6e-7
     float H = -((float)c.s1mw2 * sn + (float)c.w * cs);
     if (c.bfac > 0.0) H *= __expf((float)(-c.bfac * k2 * 0.25));
     return H;
@@ -300,16 +300,23 @@ template <int R, bool INV, bool COLS>
 __device__ __forceinline__ void fft_pass(float2 *Z, int P, const WarpFft<R> &F) {
     constexpr int D = 32 * R;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto addr = [&](int r, int j) { return COLS ? (lane + 32 * j) * P + r : r * P + lane + 32 * j; };
+    // the next line's loads issue before this line's transform
+    float2 nx[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) nx[j] = Z[addr(warp, j)];
     for (int r = warp; r < D; r += kFusedThreads / 32) {
         float2 v[R];
 #pragma unroll
-        for (int j = 0; j < R; ++j) v[j] = COLS ? Z[(lane + 32 * j) * P + r] : Z[r * P + lane + 32 * j];
+        for (int j = 0; j < R; ++j) v[j] = nx[j];
+        const int rn = r + kFusedThreads / 32;
+        if (rn < D) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) nx[j] = Z[addr(rn, j)];
+        }
         if (INV) F.inv(v); else F.fwd(v);
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-            if (COLS) Z[(lane + 32 * j) * P + r] = v[j];
-            else Z[r * P + lane + 32 * j] = v[j];
-        }
+        for (int j = 0; j < R; ++j) Z[addr(r, j)] = v[j];
     }
 }
 
@@ -379,6 +386,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ctf_mse_fused_kernel(
     }
     WarpFft<R> F;
     F.init(threadIdx.x & 31);
+    {  // warm L2 with the observations, read only after the first CTF pass
+        const char *ob = reinterpret_cast<const char *>(obs + (int64_t)b0 * D * D);
+        const int bytes = (two ? 2 : 1) * D * D * (int)sizeof(float);
+        for (int off = threadIdx.x * 128; off < bytes; off += kFusedThreads * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
+    }
     const float *r1 = render + (int64_t)b0 * D * D, *r2 = r1 + D * D;
     for (int i = threadIdx.x; i < D * D; i += kFusedThreads) {
         const int y = i / D, x = i - y * D;
