@@ -160,7 +160,7 @@ class ClockSampler:
         self.proc = None
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20",
                  "-i", str(index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -324,7 +324,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "global_batch": global_batch, "parallelism": f"dp{world}", "ctf": True,
                    "l2": f"inputs larger than L2: {DATASET}-particle dataset ({DATASET * D * D * 4 >> 20} MiB) cycled"},
         "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": engine.StepPipeline.OWN_LAUNCHES_PER_STEP * args.steps + (args.steps if world > 1 else 0),
+        "gpu_launches": rec.pipeline(BATCH).own_launches_per_step(ctf=True) * args.steps + (args.steps if world > 1 else 0),
         "roofline": {"bound": "fp32_sfu_issue", "kernel": "raster_bwd", "achieved": bwd_achieved, "peak": bwd_peak,
                      "unit": "Gpair/s", "frac": bwd_achieved / bwd_peak, "traffic": traffic,
                      "peak_basis": (f"SURVEY.md 8(d): 1 EX2 + 15 FP32 per in-ellipse pair, 128 FP32 lanes/clk/SM "

@@ -16,6 +16,7 @@ Pipeline of one step (call stack A):
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -292,9 +293,14 @@ class StepPipeline:
                   _ptr(self.scan_ws), s)
 
     # kernels of libcgs_b200 launched by one forward_backward + adam (bench accounting), direct mode:
-    # prepare, wbound_partial, wbound_scale, raster_fwd_atomic, fixed_to_float, ctf_multiply x2,
-    # loss_resid, raster_bwd, epilogue_adam  (cuFFT's own R2C/C2R kernels are library launches)
-    OWN_LAUNCHES_PER_STEP = 10
+    # prepare, wbound_partial, wbound_scale, raster_fwd_atomic, fixed_to_float, K4, raster_bwd,
+    # epilogue_adam.  K4 is one ctf_mse_fused kernel for D = 64 / 128; otherwise ctf_multiply x2 +
+    # loss_resid around cuFFT's own R2C/C2R kernels (library launches, not counted).
+    def own_launches_per_step(self, ctf: bool = True) -> int:
+        if not ctf:
+            return 8
+        fused = self.D in (64, 128) and os.environ.get("CGS_CTF_CUFFT", "0") != "1"
+        return 8 if fused else 10
 
     def forward_backward(self, params, poses, obs, ctf, events=None):
         """K0..K5 for a batch; leaves partial accumulators in self.partial.
