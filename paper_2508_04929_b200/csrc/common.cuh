@@ -35,6 +35,19 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return y;
 }
 
+// one MUFU each, no denormal fix-up code (projection inputs are >= (0.1 px)^2)
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Image-independent geometry of one Gaussian, written by cgs_prepare:
 // rec[0..2] mean, rec[3] amp, rec[4..12] M = R diag(s) row-major.
 struct SplatRec {
@@ -133,7 +146,7 @@ __device__ __forceinline__ Splat2 project2(const SplatRec &r, const PoseF &P, co
     float hd = 0.5f * (c00 - c11);
     float rad = sqrt_approx(hd * hd + c01 * c01);
     float l1 = mid + rad;
-    float l2 = l1 > 0.f ? __fdividef(det, l1) : 0.f;
+    float l2 = l1 > 0.f ? det * rcp_approx(l1) : 0.f;
     if (l2 < kEigenFloorPx2) {
         // floor the small eigenvalue, keep the eigenvector (splat.py:245-259)
         float a1 = fmaxf(l1, kEigenFloorPx2), a2 = kEigenFloorPx2;
@@ -141,27 +154,27 @@ __device__ __forceinline__ Splat2 project2(const SplatRec &r, const PoseF &P, co
         float ux = l1 - c11, uy = c01;
         if (ux * ux + uy * uy > vx * vx + vy * vy) { vx = ux; vy = uy; }
         float nn2 = vx * vx + vy * vy;
-        if (nn2 == 0.f) { vx = 1.f; vy = 0.f; } else { const float inn = rsqrtf(nn2); vx *= inn; vy *= inn; }
+        if (nn2 == 0.f) { vx = 1.f; vy = 0.f; } else { const float inn = rsqrt_approx(nn2); vx *= inn; vy *= inn; }
         c00 = a1 * vx * vx + a2 * vy * vy;
         c01 = (a1 - a2) * vx * vy;
         c11 = a1 * vy * vy + a2 * vx * vx;
         det = a1 * a2;
     }
-    float inv_det = __fdividef(1.f, det);
+    float inv_det = rcp_approx(det);
     s.p00 = c11 * inv_det;
     s.p01 = -c01 * inv_det;
     s.p11 = c00 * inv_det;
-    s.cnorm = G.inv_2pi_h2 * rsqrtf(det);
+    s.cnorm = G.inv_2pi_h2 * rsqrt_approx(det);
     s.w = r.amp * s.cnorm;
     s.A = -0.5f * kLog2e * s.p00;
     s.Bc = -kLog2e * s.p01;
     s.C = -0.5f * kLog2e * s.p11;
     s.hx = sqrt_approx(kCutoffSq * c00);
     s.hy = sqrt_approx(kCutoffSq * c11);
-    s.slope = __fdividef(s.p01, s.p00);
-    s.k = __fdividef(1.f, c11);
+    s.slope = s.p01 * rcp_approx(s.p00);
+    s.k = rcp_approx(c11);
     s.Ck = -0.5f * kLog2e * s.k;
-    s.inv_sqrt_p00 = rsqrtf(s.p00);
+    s.inv_sqrt_p00 = rsqrt_approx(s.p00);
     return s;
 }
 

@@ -415,6 +415,7 @@ constexpr int kRegThreads = CGS_BWD_REG_THREADS;
 constexpr int kMaxPoseImages = 64;  // image groups up to this size keep fp32 poses in shared memory
 constexpr int kRegFloats = 4096;  // 16 KB per band
 
+template <bool kPoseSmem>
 __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
     const bool valid = g < n;
     const int grp = blockIdx.y;
     const int b_begin = grp * ipg, b_end = min(B, b_begin + ipg);
-    const bool pose_smem = b_end - b_begin <= kMaxPoseImages;
+    constexpr bool pose_smem = kPoseSmem;  // host guarantees ipg <= kMaxPoseImages when set
     if (pose_smem)
         for (int i = threadIdx.x; i < (b_end - b_begin) * 8; i += kRegThreads) {
             const int k = i & 7;
@@ -553,8 +554,12 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
     }
     if (layout == CGS_LAYOUT_NATURAL && variant == 0 && D <= kRegFloats / 2) {
         dim3 g((unsigned)((n + kRegThreads - 1) / kRegThreads), (unsigned)G);
-        raster_bwd_region_kernel<<<g, kRegThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), upstream, partial,
-                                                            images_per_group);
+        if (images_per_group <= kMaxPoseImages)
+            raster_bwd_region_kernel<true><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), upstream,
+                                                                      partial, images_per_group);
+        else
+            raster_bwd_region_kernel<false><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), upstream,
+                                                                       partial, images_per_group);
         return check_launch("raster_bwd_region_kernel");
     }
     const size_t db_bytes = (2 * (size_t)D * D + kRowPad) * sizeof(float);
