@@ -155,71 +155,85 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
         const int xa = min(xa0, xa1), xb = max(xb0, xb1);
         if (xa > xb) continue;
         const float2 KY = f2mul(f2mul(DY, f2pack(Ck, Ck)), DY);
-        // one packed walk over columns [wa, wb]; lane t live iff mt
-        auto walk = [&](int wa, int wb, bool m0, bool m1) {
-            float2 DX = f2add(f2pack((float)wa, (float)wa), f2pack(-XC.x, -XC.y));
-            RowSums a;
-            const float2 *q = prow + wa;
-            for (int x0 = wa;;) {
-                const int xe = min(wb, x0 + kChunk - 1);
-                const float2 Q = f2fma(f2mul(DX, f2pack(A, A)), DX, KY);
-                const float2 GA = f2mul(f2fma(DX, f2pack(2.f, 2.f), ONE), f2pack(A, A));
-                // a dead lane carries e = g = 0 (a select: its g may be inf)
-                float2 E = f2pack(m0 ? ex2_approx(Q.x) : 0.f, m1 ? ex2_approx(Q.y) : 0.f);
-                float2 G = f2pack(m0 ? ex2_approx(GA.x) : 0.f, m1 ? ex2_approx(GA.y) : 0.f);
-                const float2 *qe = q + (xe - x0);
-                // software-pipelined loads may read one float2 past the span
-                // (every staging buffer carries kRowPad floats of slack)
-                float2 GP = q[0];
-                // Per column only the running sums C = sum w, S1 = sum C,
-                // S2 = sum S1 (w = g e): with u = n - k (n columns, k = 0..n-1)
-                // S1 = sum u w and 2 S2 - S1 = sum u^2 w, so at the end of the
-                // run, with D = dx' one past its last column (dx'_k = D - u),
-                //   sum w dx' = D C - S1,  sum w dx'^2 = D (D C - 2 S1) + 2 S2 - S1
-                // (6 packed ops per column instead of 9; for n <= 32 the
-                // rounding of the expansion stays below 1e-4 of sum |w| dx'^2).
-                float2 C = {0.f, 0.f}, S1 = {0.f, 0.f}, S2 = {0.f, 0.f};
-                auto column = [&](float2 V) {
-                    f2acc_fma(C, V, E);
-                    f2acc_add(a.g, V);
-                    f2acc_add(S1, C);
-                    f2acc_add(S2, S1);
-                    f2scale(E, G);
-                    f2scale(G, f2pack(c, c));
-                };
-                // two columns per trip, loads one trip ahead in alternating
-                // registers; an odd column count peels one column first
-                if (((xe - x0) & 1) == 0) {
-                    const float2 V1 = q[1];
-                    column(GP);
-                    GP = V1;
-                    ++q;
-                }
-#pragma unroll 1
-                while (q < qe) {
-                    const float2 V1 = q[1];
-                    column(GP);
-                    GP = q[2];
-                    column(V1);
-                    q += 2;
-                }
-                // q is now the next chunk's first column
-                const float nf = (float)(xe - x0 + 1);
-                DX = f2add(DX, f2pack(nf, nf));
-                const float2 X1 = f2fma(DX, C, f2pack(-S1.x, -S1.y));
-                const float2 PP = f2add(X1, f2pack(-S1.x, -S1.y));
-                const float2 QQ = f2fma(S2, f2pack(2.f, 2.f), f2pack(-S1.x, -S1.y));
-                f2acc_add(a.e, C);
-                f2acc_add(a.x, X1);
-                f2acc_add(a.xx, f2fma(DX, PP, QQ));
-                x0 = xe + 1;
-                if (x0 > wb) break;
+        // One run of n <= kChunk columns from q, seeded at offset DX; lane t live
+        // iff mt.  Per column only the running sums C = sum w, S1 = sum C,
+        // S2 = sum S1 (w = g e) are kept: with u = n - k (k = 0..n-1) S1 = sum u w
+        // and 2 S2 - S1 = sum u^2 w, so with D = dx' one past the last column
+        // (dx'_k = D - u)
+        //   sum w dx' = D C - S1,  sum w dx'^2 = D (D C - 2 S1) + 2 S2 - S1
+        // (6 packed ops per column instead of 9; for n <= 32 the rounding of the
+        // expansion stays below 1e-4 of sum |w| dx'^2).  Returns, per lane,
+        // (sum w, sum w dx', sum w dx'^2, sum g).
+        struct RunSums {
+            float2 e, x, xx, g;
+        };
+        auto run = [&](const float2 *q, int n, float2 DX, bool m0, bool m1) -> RunSums {
+            const float2 Q = f2fma(f2mul(DX, f2pack(A, A)), DX, KY);
+            const float2 GA = f2mul(f2fma(DX, f2pack(2.f, 2.f), ONE), f2pack(A, A));
+            // a dead lane carries e = g = 0 (a select: its g may be inf)
+            float2 E = f2pack(m0 ? ex2_approx(Q.x) : 0.f, m1 ? ex2_approx(Q.y) : 0.f);
+            float2 G = f2pack(m0 ? ex2_approx(GA.x) : 0.f, m1 ? ex2_approx(GA.y) : 0.f);
+            float2 C = {0.f, 0.f}, S1 = {0.f, 0.f}, S2 = {0.f, 0.f}, SG = {0.f, 0.f};
+            auto column = [&](float2 V) {
+                f2acc_fma(C, V, E);
+                f2acc_add(SG, V);
+                f2acc_add(S1, C);
+                f2acc_add(S2, S1);
+                f2scale(E, G);
+                f2scale(G, f2pack(c, c));
+            };
+            // two columns per trip, loads one trip ahead (they may read one
+            // float2 past the span: every staging buffer carries kRowPad floats
+            // of slack); an odd column count peels one column first
+            const float2 *qe = q + (n - 1);
+            float2 GP = q[0];
+            if (n & 1) {
+                const float2 V1 = q[1];
+                column(GP);
+                GP = V1;
+                ++q;
             }
-            const float2 DYE = f2mul(DY, a.e), DYX = f2mul(DY, a.x);
-            M.e += f2sum(a.e);
-            M.g += (m0 ? a.g.x : 0.f) + (m1 ? a.g.y : 0.f);
-            M.x += f2sum(a.x);
-            M.xx += f2sum(a.xx);
+#pragma unroll 1
+            for (; q < qe; q += 2) {
+                const float2 V1 = q[1];
+                column(GP);
+                GP = q[2];
+                column(V1);
+            }
+            const float nf = (float)n;
+            const float2 Dn = f2add(DX, f2pack(nf, nf));
+            const float2 NS1 = f2pack(-S1.x, -S1.y);
+            const float2 X1 = f2fma(Dn, C, NS1);
+            RunSums r;
+            r.e = C;
+            r.x = X1;
+            r.xx = f2fma(Dn, f2add(X1, NS1), f2fma(S2, f2pack(2.f, 2.f), NS1));
+            r.g = SG;
+            return r;
+        };
+        // one packed walk over columns [wa, wb]: a single run, or runs of
+        // kChunk columns (each restarts the exp recurrence exactly)
+        auto walk = [&](int wa, int wb, bool m0, bool m1) {
+            const float2 DX = f2add(f2pack((float)wa, (float)wa), f2pack(-XC.x, -XC.y));
+            RunSums r;
+            if (wb - wa < kChunk) [[likely]] {
+                r = run(prow + wa, wb - wa + 1, DX, m0, m1);
+            } else {
+                r = RunSums{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+                for (int x0 = wa; x0 <= wb; x0 += kChunk) {
+                    const float o = (float)(x0 - wa);
+                    const RunSums t = run(prow + x0, min(kChunk, wb - x0 + 1), f2add(DX, f2pack(o, o)), m0, m1);
+                    r.e = f2add(r.e, t.e);
+                    r.x = f2add(r.x, t.x);
+                    r.xx = f2add(r.xx, t.xx);
+                    r.g = f2add(r.g, t.g);
+                }
+            }
+            const float2 DYE = f2mul(DY, r.e), DYX = f2mul(DY, r.x);
+            M.e += f2sum(r.e);
+            M.g += (m0 ? r.g.x : 0.f) + (m1 ? r.g.y : 0.f);
+            M.x += f2sum(r.x);
+            M.xx += f2sum(r.xx);
             M.y += f2sum(DYE);
             M.xy += f2sum(DYX);
             M.yy += fmaf(DY.x, DYE.x, DY.y * DYE.y);
