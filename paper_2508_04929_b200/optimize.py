@@ -220,6 +220,7 @@ class Reconstructor:
         self.ipg = images_per_group
         self.tile = tile
         self._pipes: dict = {}
+        self._copy_stream = None  # H2D stream of step_host
 
     # -- helpers -------------------------------------------------------------
     def local_slice(self, indices: np.ndarray) -> np.ndarray:
@@ -257,15 +258,25 @@ class Reconstructor:
     def step_host(self, obs, poses, ctfs, lr: float, *, global_batch: int, loss_out=None):
         """Public end-to-end step from (pinned) HOST buffers of this rank's batch.
 
-        Copies the batch host->device on the current stream, runs the step and
-        copies the per-image losses device->host into ``loss_out`` (pinned), all
-        stream-ordered; the caller synchronises when it needs the numbers.
+        Copies the batch host->device on a dedicated copy stream, runs the step
+        on the current stream once the copy has landed, and copies the per-image
+        losses device->host into ``loss_out`` (pinned).  Nothing synchronises the
+        host, so back-to-back calls overlap the next batch's H2D (PCIe) with
+        this batch's kernels; the caller synchronises when it needs the numbers.
         """
         torch = _torch()
         dev = self.ctx.device
-        o = obs.to(dev, non_blocking=True)
-        p = poses.to(dev, non_blocking=True)
-        c = None if ctfs is None else ctfs.to(dev, non_blocking=True)
+        compute = torch.cuda.current_stream(dev)
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(dev)
+        with torch.cuda.stream(self._copy_stream):
+            o = obs.to(dev, non_blocking=True)
+            p = poses.to(dev, non_blocking=True)
+            c = None if ctfs is None else ctfs.to(dev, non_blocking=True)
+        compute.wait_stream(self._copy_stream)
+        for t in (o, p, c):  # allocated on the copy stream, consumed on the compute stream
+            if t is not None:
+                t.record_stream(compute)
         loss = self.step_batch(o, p, c, lr, global_batch=global_batch)
         if loss_out is not None:
             loss_out.copy_(loss, non_blocking=True)
