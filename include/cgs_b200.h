@@ -171,6 +171,16 @@ int cgs_ctf_mse(void *plan, const float *render, const float *obs, int32_t B, cg
                 const double *ctf, void *spectrum, float *model, float *upstream, double *loss,
                 int32_t *status, int32_t layout, void *stream);
 
+/* Batched Fourier filter out = Re ifft2(F fft2(in)), per image F = H_sym (CTF,
+ * ctf f64 [B][8], may be NULL) x the sub-pixel shift ramp
+ * exp(-2 pi i (fx tx + fy ty) / D) (shifts f64 [B][2] pixels, may be NULL):
+ * apply_ctf (optics.py:124-141) followed by phase_shift_translate
+ * (optics.py:144-159), as simulate (simulate.py:241-244) and the observed-image
+ * centring (train.py:124-133) use them.  One kernel; in-place allowed.
+ * Sizes 32, 64, 128 (else CGS_ERR_UNSUPPORTED). */
+int cgs_fourier_filter(const float *in, float *out, int32_t B, cgs_grid grid, const double *ctf,
+                       const double *shifts, void *stream);
+
 /* ---- K5: fused backward (backward_pixels, _kernels.py:128-190, plus the
  * per-image part of rasterize_backward, splat.py:332-349) ------------------
  * Gaussian-major: each CTA owns a chunk of Gaussians and a group of images,

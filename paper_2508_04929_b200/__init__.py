@@ -63,6 +63,6 @@ from .render import (
     rasterize_batch,
     view_transform,
 )
-from .synth import make_phantom, sample_pose
+from .synth import DefocusRange, NoiseModel, SimSpec, make_phantom, sample_pose, simulate, snr_from_db
 
 __version__ = "0.1.0"

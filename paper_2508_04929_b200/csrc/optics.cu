@@ -454,6 +454,138 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ctf_mse_fused_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
+// General Fourier filter on image pairs: out = Re ifft2(F . fft2(in)) with, per
+// image, F = H_sym (CTF, optional) x exp(-2 pi i (fx tx + fy ty) / D) (a
+// sub-pixel shift by (tx, ty) pixels, optional; phase_shift_translate,
+// optics.py:144-159).  Same packed-pair scheme as ctf_mse_fused_kernel with a
+// complex filter: only the Hermitian part Fh(k) = (F(k) + conj F(-k)) / 2 of a
+// filter reaches the real output, and with it W(k) = P Z(k) + Q conj Z(-k),
+// P, Q = (Fh1 +- Fh2) / 2, W(-k) = conj(P) Z(-k) + conj(Q) conj Z(k).
+// Centred and natural layouts give the same result (the filter is a circular
+// convolution), so images stay in natural layout.
+__device__ __forceinline__ float2 shift_ramp(float tx, float ty, int D, int fy, int fx) {
+    float sn, cs;
+    // exp(-2 pi i (fx tx + fy ty) / D), phase reduced in fp32 turns first
+    float t = (fx * tx + fy * ty) / (float)D;
+    t -= rintf(t);
+    sincospif(-2.f * t, &sn, &cs);
+    return make_float2(cs, sn);
+}
+
+struct FilterSpec {
+    bool ctf, shift;
+    CtfConst cc;
+    float tx, ty;
+};
+
+// Fh(k) at frequency index (ky, kx); 1 when the image has no filter part
+__device__ __forceinline__ float2 filter_h(const FilterSpec &f, int D, int ky, int kx) {
+    const int c0 = D / 2;
+    const int fy = ky < D - c0 ? ky : ky - D, fx = kx < D - c0 ? kx : kx - D;
+    float h = f.ctf ? ctf_sym(f.cc, D, ky, kx) : 1.f;
+    if (!f.shift) return make_float2(h, 0.f);
+    const float2 r = shift_ramp(f.tx, f.ty, D, fy, fx);
+    float2 rh = r;
+    if ((D % 2 == 0) && (fy == -c0 || fx == -c0)) {  // -k wraps onto the grid: average with conj F(-k)
+        const float2 rm = shift_ramp(f.tx, f.ty, D, wrap_freq(fy, D, c0), wrap_freq(fx, D, c0));
+        rh = make_float2(0.5f * (r.x + rm.x), 0.5f * (r.y - rm.y));
+    }
+    return make_float2(h * rh.x, h * rh.y);
+}
+
+template <int R>
+__device__ __forceinline__ void filter_combine(float2 *Z, int P, const FilterSpec *fs, bool two, float norm) {
+    constexpr int D = 32 * R;
+    for (int idx = threadIdx.x; idx < D * D; idx += kFusedThreads) {
+        const int py = idx / D, px = idx - py * D;
+        const int ky = perm_k<R>(py), kx = perm_k<R>(px);
+        const int ny = ky ? D - ky : 0, nx = kx ? D - kx : 0;
+        const int qy = perm_p<R>(ny), qx = perm_p<R>(nx);
+        const int idx2 = qy * D + qx;
+        if (idx2 < idx) continue;
+        const float2 f1 = filter_h(fs[0], D, ky, kx);
+        const float2 f2 = two ? filter_h(fs[1], D, ky, kx) : make_float2(0.f, 0.f);
+        const float2 Pc = make_float2(0.5f * (f1.x + f2.x) * norm, 0.5f * (f1.y + f2.y) * norm);
+        const float2 Qc = make_float2(0.5f * (f1.x - f2.x) * norm, 0.5f * (f1.y - f2.y) * norm);
+        const float2 z1 = Z[py * P + px], z2 = Z[qy * P + qx];
+        const float2 z2c = make_float2(z2.x, -z2.y), z1c = make_float2(z1.x, -z1.y);
+        // W(k) = P z1 + Q conj(z2)
+        Z[py * P + px] = make_float2(Pc.x * z1.x - Pc.y * z1.y + Qc.x * z2c.x - Qc.y * z2c.y,
+                                     Pc.x * z1.y + Pc.y * z1.x + Qc.x * z2c.y + Qc.y * z2c.x);
+        if (idx2 != idx)  // W(-k) = conj(P) z2 + conj(Q) conj(z1)
+            Z[qy * P + qx] = make_float2(Pc.x * z2.x + Pc.y * z2.y + Qc.x * z1c.x + Qc.y * z1c.y,
+                                         Pc.x * z2.y - Pc.y * z2.x + Qc.x * z1c.y - Qc.y * z1c.x);
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kFusedThreads, 1) fourier_filter_kernel(const float *__restrict__ in,
+                                                                          float *__restrict__ out, int B, double pix,
+                                                                          const double *__restrict__ ctf,
+                                                                          const double *__restrict__ shifts) {
+    constexpr int D = 32 * R, P = D + 1;
+    extern __shared__ float2 Z[];
+    __shared__ FilterSpec fs[2];
+    const int b0 = 2 * blockIdx.x;
+    const bool two = b0 + 1 < B;
+    if (threadIdx.x < 2 && (threadIdx.x == 0 || two)) {
+        const int b = b0 + threadIdx.x;
+        FilterSpec f;
+        f.ctf = ctf != nullptr;
+        if (f.ctf) {
+            CtfConst c = load_ctf(ctf + 8 * (int64_t)b, D, pix);
+            c.inv_dA = 1.0 / c.dA;
+            c.pl = kPiD * c.lam;
+            c.cs3 = 0.5 * kPiD * c.cs * c.lam * c.lam * c.lam;
+            f.cc = c;
+        }
+        f.tx = shifts ? (float)shifts[2 * (int64_t)b] : 0.f;
+        f.ty = shifts ? (float)shifts[2 * (int64_t)b + 1] : 0.f;
+        f.shift = f.tx != 0.f || f.ty != 0.f;
+        fs[threadIdx.x] = f;
+    }
+    WarpFft<R> F;
+    F.init(threadIdx.x & 31);
+    const float *i1 = in + (int64_t)b0 * D * D, *i2 = i1 + D * D;
+    for (int i = threadIdx.x; i < D * D; i += kFusedThreads) {
+        const int y = i / D, x = i - y * D;
+        Z[y * P + x] = make_float2(i1[i], two ? i2[i] : 0.f);
+    }
+    __syncthreads();
+    fft_pass<R, false, false>(Z, P, F);
+    __syncthreads();
+    fft_pass<R, false, true>(Z, P, F);
+    __syncthreads();
+    filter_combine<R>(Z, P, fs, two, 1.f / (float)(D * D));
+    __syncthreads();
+    fft_pass<R, true, true>(Z, P, F);
+    __syncthreads();
+    fft_pass<R, true, false>(Z, P, F);
+    __syncthreads();
+    float *o1 = out + (int64_t)b0 * D * D, *o2 = o1 + D * D;
+    for (int i = threadIdx.x; i < D * D; i += kFusedThreads) {
+        const int y = i / D, x = i - y * D;
+        const float2 u = Z[y * P + x];
+        o1[i] = u.x;
+        if (two) o2[i] = u.y;
+    }
+}
+
+template <int R>
+static int launch_fourier_filter(const float *in, float *out, int B, double pix, const double *ctf,
+                                 const double *shifts, cudaStream_t st) {
+    constexpr int D = 32 * R;
+    const size_t smem = (size_t)D * (D + 1) * sizeof(float2);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(fourier_filter_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    fourier_filter_kernel<R><<<(B + 1) / 2, kFusedThreads, smem, st>>>(in, out, B, pix, ctf, shifts);
+    return check_launch("fourier_filter_kernel");
+}
+
 template <int R>
 static int launch_ctf_mse_fused(const float *render, const float *obs, int B, double pix, const double *ctf,
                                 float *model, float *upstream, double *loss, int32_t *status, cudaStream_t st) {
@@ -561,7 +693,7 @@ extern "C" int cgs_ctf_mse(void *plan, const float *render, const float *obs, in
                            float *upstream, double *loss, int32_t *status, int32_t layout,
                            void *stream) {
     if (!render || !obs || !upstream || !loss) return CGS_ERR_ARG;
-    // fused single-kernel path for D = 64 / 128 (CGS_CTF_CUFFT=1 forces cuFFT, for A/B)
+    // fused single-kernel path for D = 32 / 64 / 128 (CGS_CTF_CUFFT=1 forces cuFFT, for A/B)
     static const bool force_cufft = getenv("CGS_CTF_CUFFT") && getenv("CGS_CTF_CUFFT")[0] == '1';
     if (ctf && !force_cufft && render != upstream && grid.pixel_size > 0 && B > 0) {
         cudaStream_t st = (cudaStream_t)stream;
@@ -569,6 +701,8 @@ extern "C" int cgs_ctf_mse(void *plan, const float *render, const float *obs, in
             return launch_ctf_mse_fused<4>(render, obs, B, grid.pixel_size, ctf, model, upstream, loss, status, st);
         if (grid.size == 64)
             return launch_ctf_mse_fused<2>(render, obs, B, grid.pixel_size, ctf, model, upstream, loss, status, st);
+        if (grid.size == 32)
+            return launch_ctf_mse_fused<1>(render, obs, B, grid.pixel_size, ctf, model, upstream, loss, status, st);
     }
     const float *m = render;
     if (ctf) {
@@ -584,4 +718,16 @@ extern "C" int cgs_ctf_mse(void *plan, const float *render, const float *obs, in
     if (rc) return rc;
     if (ctf) return cgs_ctf_apply(plan, upstream, upstream, B, grid, ctf, nullptr, spectrum, layout, stream);
     return CGS_OK;
+}
+
+extern "C" int cgs_fourier_filter(const float *in, float *out, int32_t B, cgs_grid grid, const double *ctf,
+                                  const double *shifts, void *stream) {
+    if (!in || !out || B <= 0 || grid.size < 1) return CGS_ERR_ARG;
+    if (ctf && !(grid.pixel_size > 0)) return CGS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (grid.size == 128) return launch_fourier_filter<4>(in, out, B, grid.pixel_size, ctf, shifts, st);
+    if (grid.size == 64) return launch_fourier_filter<2>(in, out, B, grid.pixel_size, ctf, shifts, st);
+    if (grid.size == 32) return launch_fourier_filter<1>(in, out, B, grid.pixel_size, ctf, shifts, st);
+    set_error_detail("cgs_fourier_filter", "image size must be 32, 64 or 128");
+    return CGS_ERR_UNSUPPORTED;
 }

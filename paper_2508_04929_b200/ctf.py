@@ -151,9 +151,44 @@ def phase_shift_translate(img: RenderedImage, translation_px) -> RenderedImage:
     if tx == 0.0 and ty == 0.0:
         return RenderedImage(grid=img.grid, pixels=img.pixels.copy())
     D = img.grid.size
+    if D in engine.FILTER_SIZES:
+        out = filter_batch(_dev(img.pixels[None], torch.float32), img.grid, shifts=[(tx, ty)])
+        return RenderedImage(grid=img.grid, pixels=out[0].double().cpu().numpy())
     k = torch.arange(D, dtype=torch.float64, device="cuda") - D // 2
     ramp = torch.exp(-2j * math.pi * (k[None, :] * tx + k[:, None] * ty) / D)
     x = _dev(img.pixels, torch.float64)
     X = torch.fft.fftshift(torch.fft.fft2(torch.fft.ifftshift(x))) * ramp
     y = torch.fft.fftshift(torch.fft.ifft2(torch.fft.ifftshift(X))).real
     return RenderedImage(grid=img.grid, pixels=y.cpu().numpy())
+
+
+def filter_batch(images, grid: GridSpec, *, ctfs=None, shifts=None, out=None):
+    """apply_ctf then phase_shift_translate for a device batch f32 [B][D][D] in
+    one kernel (``cgs_fourier_filter``).  ``ctfs``: CtfParams list, f64 [B][8]
+    array/tensor or None; ``shifts``: [B][2] pixels or None.  D in 32/64/128;
+    other sizes go through cuFFT (CTF) and torch.fft (shift)."""
+    import torch
+
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(grid.size, grid.extent, grid.pixel_size)
+    c = None
+    if ctfs is not None:
+        c = ctfs if isinstance(ctfs, torch.Tensor) else _dev(
+            engine.ctf_array(ctfs) if not isinstance(ctfs, np.ndarray) else ctfs, torch.float64)
+    sh = None
+    if shifts is not None:
+        sh = shifts if isinstance(shifts, torch.Tensor) else _dev(np.asarray(shifts, np.float64).reshape(-1, 2),
+                                                                  torch.float64)
+    if grid.size in engine.FILTER_SIZES:
+        return engine.fourier_filter(ctx, images, gs, ctf=c, shifts=sh, out=out)
+    y = images if c is None else engine.ctf_apply(ctx, images, gs, ctf=c)
+    if sh is not None:
+        D = grid.size
+        k = torch.arange(D, dtype=torch.float64, device=images.device) - D // 2
+        ramp = torch.exp(-2j * math.pi * (k[None, None, :] * sh[:, 0, None, None] + k[None, :, None] * sh[:, 1, None, None]) / D)
+        X = torch.fft.fftshift(torch.fft.fft2(torch.fft.ifftshift(y.double(), dim=(-2, -1))), dim=(-2, -1)) * ramp
+        y = torch.fft.fftshift(torch.fft.ifft2(torch.fft.ifftshift(X, dim=(-2, -1))), dim=(-2, -1)).real.float()
+    if out is not None:
+        out.copy_(y)
+        return out
+    return y

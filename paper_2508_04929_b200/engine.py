@@ -204,6 +204,19 @@ def ctf_apply(ctx, images, grid_s, *, ctf=None, H=None, out=None):
     return out
 
 
+FILTER_SIZES = (32, 64, 128)
+
+
+def fourier_filter(ctx, images, grid_s, *, ctf=None, shifts=None, out=None):
+    """Re ifft2(H_sym . shift ramp . fft2(x)) on a device batch f32 [B][D][D]
+    (apply_ctf then phase_shift_translate), one kernel; D in FILTER_SIZES.
+    ctf f64 [B][8] and shifts f64 [B][2] (pixels) are optional device tensors."""
+    B = images.shape[0]
+    out = out if out is not None else torch.empty_like(images)
+    _lib.call("cgs_fourier_filter", _ptr(images), _ptr(out), B, grid_s, _ptr(ctf), _ptr(shifts), ctx.stream)
+    return out
+
+
 def loss_residual(ctx, model, obs, resid=None):
     B, D = model.shape[0], model.shape[-1]
     loss = torch.empty(B, dtype=torch.float64, device=ctx.device)
@@ -294,12 +307,12 @@ class StepPipeline:
 
     # kernels of libcgs_b200 launched by one forward_backward + adam (bench accounting), direct mode:
     # prepare, wbound_partial, wbound_scale, raster_fwd_atomic, fixed_to_float, K4, raster_bwd,
-    # epilogue_adam.  K4 is one ctf_mse_fused kernel for D = 64 / 128; otherwise ctf_multiply x2 +
+    # epilogue_adam.  K4 is one ctf_mse_fused kernel for D = 32 / 64 / 128; otherwise ctf_multiply x2 +
     # loss_resid around cuFFT's own R2C/C2R kernels (library launches, not counted).
     def own_launches_per_step(self, ctf: bool = True) -> int:
         if not ctf:
             return 8
-        fused = self.D in (64, 128) and os.environ.get("CGS_CTF_CUFFT", "0") != "1"
+        fused = self.D in (32, 64, 128) and os.environ.get("CGS_CTF_CUFFT", "0") != "1"
         return 8 if fused else 10
 
     def forward_backward(self, params, poses, obs, ctf, events=None):

@@ -349,10 +349,30 @@ def _dist_active() -> bool:
         return False
 
 
+def centered_observations(records, grid: GridSpec, chunk: int = 4096) -> np.ndarray:
+    """f32 [R][D][D] observations with their recorded translations removed
+    (train.py:124-133, :222), batched on the GPU: one cgs_fourier_filter launch
+    per chunk of translated records."""
+    from .ctf import filter_batch
+
+    obs = np.stack([np.asarray(r.image, dtype=np.float32) for r in records])
+    shifts = np.stack([np.asarray(r.translation, dtype=np.float64) for r in records]) if len(records) else None
+    moved = np.flatnonzero(np.any(shifts != 0.0, axis=1)) if len(records) else np.zeros(0, int)
+    if len(moved) == 0:
+        return obs
+    torch = _torch()
+    for a in range(0, len(moved), chunk):
+        idx = moved[a:a + chunk]
+        x = torch.as_tensor(obs[idx]).cuda()
+        y = filter_batch(x, grid, shifts=-shifts[idx])
+        obs[idx] = y.cpu().numpy()
+    return obs
+
+
 def _record_arrays(records, grid: GridSpec):
     from .engine import ctf_array, pose_array
 
-    obs = np.stack([_centered_observation(r) for r in records]).astype(np.float32)
+    obs = centered_observations(records, grid)
     poses = pose_array([r.pose.rotation for r in records], [r.pose.translation for r in records])
     ctfs = ctf_array([r.ctf for r in records])
     return obs, poses, ctfs

@@ -1,9 +1,14 @@
 """Synthetic particles on the GPU (the forward model of the reference's simulate.py).
 
-``make_phantom`` and ``sample_pose`` reproduce the reference's seeded draws
-(simulate.py:92-190) so that synthetic inputs match it exactly; rendering,
-CTF modulation and noise for whole particle stacks run on the device
-(``synthetic_stack``): K0/K2/K3 render, K4 CTF, ``torch.randn`` noise.
+``make_phantom``, ``sample_pose`` and every per-particle draw of ``simulate``
+reproduce the reference's seeded generators (simulate.py:92-267) exactly, on
+the host (a few numbers per particle).  The image work runs on the device in
+batches: K0/K3 direct render of the truth, then one ``cgs_fourier_filter``
+launch that applies the CTF and the sub-pixel translation together, then the
+dataset-wide noise calibration.  Noise comes either from the reference's own
+per-particle numpy streams (``noise="numpy"``, bit-compatible datasets) or
+from the device Philox generator (``noise="device"``, for large sets).
+``synthetic_stack`` is the device-resident variant used by bench.py.
 """
 
 from __future__ import annotations
@@ -16,6 +21,7 @@ from . import _lib, engine
 from .mixture import COL_MEAN, COL_QUAT, COL_RAW_AMP, COL_RAW_SCALE, PARAMS_PER_GAUSSIAN, GaussianMixture, GridSpec
 from .mixture import inverse_activate, normalize_quaternion
 from .render import Pose
+from dataclasses import dataclass, replace
 
 PHANTOM_KINDS = ("helix", "blob-cluster", "two-lobe")
 
@@ -116,3 +122,162 @@ def synthetic_stack(truth: GaussianMixture, rotations, grid: GridSpec, *, defocu
         gen.manual_seed(int(noise_seed))
         out += sigma * torch.randn(out.shape, generator=gen, device=ctx.device, dtype=torch.float32)
     return out, ctfs, sigma
+
+
+# ---------------------------------------------------------------------------
+# simulate (simulate.py:35-267)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class NoiseModel:
+    """Gaussian pixel noise with variance var(clean) / snr; snr = inf disables it (simulate.py:35-47)."""
+
+    snr: float
+    seed: int = 0
+
+    def __post_init__(self):
+        if not self.snr > 0:
+            raise ValueError("snr must be positive (use math.inf to disable noise)")
+
+
+def snr_from_db(db: float) -> float:
+    """10**(db / 10) (simulate.py:50-52)."""
+    return 10.0 ** (db / 10.0)
+
+
+def _default_template():
+    from .ctf import CtfParams
+
+    return CtfParams(defocus_u=15000.0, defocus_v=15000.0)
+
+
+@dataclass(frozen=True)
+class DefocusRange:
+    """Uniform defocus, defocus_v = defocus_u, no astigmatism (simulate.py:55-67)."""
+
+    minimum: float
+    maximum: float
+    template: object = None
+
+    def sample(self, rng: np.random.Generator):
+        d = float(rng.uniform(self.minimum, self.maximum))
+        t = self.template if self.template is not None else _default_template()
+        return replace(t, defocus_u=d, defocus_v=d, astigmatism_angle=0.0)
+
+
+@dataclass
+class SimSpec:
+    """simulate.py:70-86."""
+
+    truth: GaussianMixture
+    num_particles: int
+    grid: GridSpec
+    ctf_distribution: object
+    noise: NoiseModel
+    translation_range: float = 0.0
+    integer_translations: bool = False
+    pose_jitter_deg: float = 0.0
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.num_particles < 2:
+            raise ValueError("num_particles must be >= 2 (both half-splits must be non-empty)")
+
+
+@dataclass
+class SimulationResult:
+    dataset: object
+    quaternions: np.ndarray
+    noise_sigma: float
+    images: object = None  # device f32 [K][D][D] when simulate(..., keep_on_device=True)
+
+    @property
+    def records(self):
+        return self.dataset.records
+
+
+def _quaternion_multiply(a, b):
+    aw, ax, ay, az = a
+    bw, bx, by, bz = b
+    return np.array([aw * bw - ax * bx - ay * by - az * bz, aw * bx + ax * bw + ay * bz - az * by,
+                     aw * by - ax * bz + ay * bw + az * bx, aw * bz + ax * by - ay * bx + az * bw])
+
+
+def _jitter_quaternion(rng, degrees):
+    axis = rng.standard_normal(3)
+    axis /= np.linalg.norm(axis)
+    angle = math.radians(degrees) * rng.standard_normal()
+    return np.concatenate(([math.cos(angle / 2.0)], math.sin(angle / 2.0) * axis))
+
+
+def _draws(spec: SimSpec):
+    """The per-particle host draws of simulate.py:224-239, in the reference's order."""
+    n = spec.num_particles
+    true_q = np.empty((n, 4))
+    rec_q = np.empty((n, 4))
+    ctfs = []
+    trans = np.zeros((n, 2))
+    choices = None if isinstance(spec.ctf_distribution, DefocusRange) else list(spec.ctf_distribution)
+    for i in range(n):
+        rng = np.random.default_rng(spec.seed + i)
+        q = sample_rotation_quaternion(rng)
+        true_q[i] = q
+        ctfs.append(spec.ctf_distribution.sample(rng) if choices is None else choices[int(rng.integers(len(choices)))])
+        if spec.translation_range:
+            t = rng.uniform(-spec.translation_range, spec.translation_range, size=2)
+            if spec.integer_translations:
+                t = np.rint(t)
+            trans[i] = t
+        if spec.pose_jitter_deg > 0:
+            q = _quaternion_multiply(_jitter_quaternion(rng, spec.pose_jitter_deg), q)
+        rec_q[i] = q
+    return true_q, rec_q, ctfs, trans
+
+
+def simulate(spec: SimSpec, *, noise: str = "numpy", chunk: int = 1024, keep_on_device: bool = False):
+    """Render, modulate, translate and corrupt particles (simulate.py:204-267) on the GPU.
+
+    noise="numpy" draws each particle's noise from default_rng(noise.seed + i)
+    exactly as the reference (bit-compatible datasets); noise="device" uses the
+    device generator seeded with noise.seed (same distribution, much faster
+    for 1e5 particles).  Images are float32, as the reference stores them.
+    """
+    import torch
+
+    from .ctf import filter_batch
+    from .optimize import Dataset, ParticleRecord
+    from .render import rasterize_batch
+
+    if noise not in ("numpy", "device"):
+        raise ValueError("noise must be 'numpy' or 'device'")
+    grid = spec.grid
+    n, D = spec.num_particles, grid.size
+    true_q, rec_q, ctfs, trans = _draws(spec)
+    R = np.stack([Pose.from_quaternion(q).rotation for q in true_q])
+    ctx = engine.DeviceContext.get()
+    clean = torch.empty((n, D, D), dtype=torch.float32, device=ctx.device)
+    carr = engine.ctf_array(ctfs)
+    moved = bool(np.any(trans != 0.0))
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        img = rasterize_batch(spec.truth, R[a:b], None, grid, device_out=True, method="direct")
+        filter_batch(img, grid, ctfs=carr[a:b], shifts=trans[a:b] if moved else None, out=clean[a:b])
+    sigma = 0.0 if math.isinf(spec.noise.snr) else float(math.sqrt(clean.double().var(unbiased=False).item()
+                                                                    / spec.noise.snr))
+    if sigma > 0.0 and noise == "device":
+        gen = torch.Generator(device=ctx.device)
+        gen.manual_seed(int(spec.noise.seed))
+        clean += sigma * torch.randn(clean.shape, generator=gen, device=ctx.device, dtype=torch.float32)
+    host = clean.cpu().numpy()
+    records = []
+    for i in range(n):
+        img = host[i]
+        if sigma > 0.0 and noise == "numpy":
+            img = (img.astype(np.float64)
+                   + np.random.default_rng(spec.noise.seed + i).normal(0.0, sigma, size=img.shape)).astype(np.float32)
+        records.append(ParticleRecord(image=img, pose=Pose.from_quaternion(rec_q[i]), ctf=ctfs[i],
+                                      translation=trans[i]))
+    images = None
+    if keep_on_device:
+        images = torch.as_tensor(np.stack([r.image for r in records])).to(ctx.device) if noise == "numpy" else clean
+    return SimulationResult(dataset=Dataset(records=records, grid=grid), quaternions=rec_q, noise_sigma=sigma,
+                            images=images)

@@ -236,6 +236,42 @@ def train_case():
     print("train_small", {k: getattr(v, "shape", v) for k, v in out.items()})
 
 
+def simulate_cases():
+    """cryosplat.simulate (simulate.py:204-267): two specs covering DefocusRange and
+    CTF-list sampling, translations (sub-pixel and integer), pose jitter, noise."""
+    from cryosplat.simulate import DefocusRange, NoiseModel, SimSpec, make_phantom, simulate
+
+    out = {}
+    grid = cs.GridSpec(64, 0.5, 1.5)
+    specs = {
+        "a": SimSpec(truth=make_phantom("helix", 12, 0), num_particles=5, grid=grid,
+                     ctf_distribution=DefocusRange(1e4, 2.5e4), noise=NoiseModel(snr=0.5, seed=7), seed=3),
+        "b": SimSpec(truth=make_phantom("blob-cluster", 10, 1), num_particles=4, grid=grid,
+                     ctf_distribution=[cs.CtfParams(12000.0, 15000.0, 0.7), cs.CtfParams(20000.0, 18000.0, -0.3,
+                                                                                          phase_shift=0.4)],
+                     noise=NoiseModel(snr=float("inf")), translation_range=3.0, pose_jitter_deg=2.0, seed=11),
+        "c": SimSpec(truth=make_phantom("two-lobe", 8, 2), num_particles=3, grid=grid,
+                     ctf_distribution=DefocusRange(1.5e4, 2e4), noise=NoiseModel(snr=2.0, seed=1),
+                     translation_range=2.0, integer_translations=True, seed=5),
+    }
+    for k, spec in specs.items():
+        res = simulate(spec)
+        out[f"{k}_images"] = np.stack([r.image for r in res.records])
+        out[f"{k}_quaternions"] = res.quaternions
+        out[f"{k}_rotations"] = np.stack([r.pose.rotation for r in res.records])
+        out[f"{k}_translations"] = np.stack([r.translation for r in res.records])
+        out[f"{k}_defocus"] = np.array([[r.ctf.defocus_u, r.ctf.defocus_v, r.ctf.astigmatism_angle,
+                                         r.ctf.phase_shift] for r in res.records])
+        out[f"{k}_sigma"] = np.array(res.noise_sigma)
+    np.savez_compressed(os.path.join(OUT, "simulate.npz"), **out)
+    print("simulate", sorted(out))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    for name in sys.argv[1:]:
+        globals()[name]()
+    sys.exit(0)
+
 if __name__ == "__main__":
     stack_case("c1_step", 5000, 64, 4, with_ctf=False)
     stack_case("c2_slice", 50000, 128, 2, with_ctf=True, light=True)

@@ -139,3 +139,39 @@ def test_view_transform_and_projection_scalar_forms():
     assert float(sg.density(np.zeros(2))) == pytest.approx(1.0 / (2 * np.pi * 1e-4), rel=1e-12)
     with pytest.raises(cs.DegenerateSplatError):
         cs.orthographic_project(cs.CameraSpaceGaussian(np.zeros(3), np.diag([1.0, -1.0, 1.0])))
+
+
+def _simulate_specs():
+    import math
+
+    from paper_2508_04929_b200 import synth
+
+    grid = cs.GridSpec(64, 0.5, 1.5)
+    return {
+        "a": synth.SimSpec(truth=synth.make_phantom("helix", 12, 0), num_particles=5, grid=grid,
+                           ctf_distribution=synth.DefocusRange(1e4, 2.5e4), noise=synth.NoiseModel(snr=0.5, seed=7),
+                           seed=3),
+        "b": synth.SimSpec(truth=synth.make_phantom("blob-cluster", 10, 1), num_particles=4, grid=grid,
+                           ctf_distribution=[cs.CtfParams(12000.0, 15000.0, 0.7),
+                                             cs.CtfParams(20000.0, 18000.0, -0.3, phase_shift=0.4)],
+                           noise=synth.NoiseModel(snr=math.inf), translation_range=3.0, pose_jitter_deg=2.0, seed=11),
+        "c": synth.SimSpec(truth=synth.make_phantom("two-lobe", 8, 2), num_particles=3, grid=grid,
+                           ctf_distribution=synth.DefocusRange(1.5e4, 2e4), noise=synth.NoiseModel(snr=2.0, seed=1),
+                           translation_range=2.0, integer_translations=True, seed=5),
+    }
+
+
+def test_simulate_host_draws_match_reference():
+    """Per-particle pose / CTF / translation / jitter draws of simulate (simulate.py:224-239)
+    are the reference's, bit for bit (tests/golden/simulate.npz from the reference itself)."""
+    from paper_2508_04929_b200 import synth
+
+    g = load_golden("simulate")
+    for k, spec in _simulate_specs().items():
+        true_q, rec_q, ctfs, trans = synth._draws(spec)
+        assert np.array_equal(rec_q, g[f"{k}_quaternions"])
+        assert np.array_equal(trans, g[f"{k}_translations"])
+        d = np.array([[c.defocus_u, c.defocus_v, c.astigmatism_angle, c.phase_shift] for c in ctfs])
+        assert np.array_equal(d, g[f"{k}_defocus"])
+        rot = np.stack([cs.Pose.from_quaternion(q).rotation for q in rec_q])
+        np.testing.assert_allclose(rot, g[f"{k}_rotations"], rtol=0, atol=1e-15)
