@@ -267,6 +267,32 @@ def simulate_cases():
     print("simulate", sorted(out))
 
 
+def io_cases():
+    """Files written by the reference's io.py (MRC stack + volume, metadata table)."""
+    import tempfile
+
+    from cryosplat import io as rio
+
+    rng = np.random.default_rng(21)
+    stack = rng.standard_normal((3, 16, 16)).astype(np.float32)
+    vol = rng.standard_normal((8, 8, 8)).astype(np.float32)
+    quats = rng.standard_normal((3, 4))
+    trans = rng.uniform(-2, 2, (3, 2))
+    ctfs = [cs.CtfParams(12000.0 + 1000 * i, 15000.0 - 500 * i, 0.1 * i, phase_shift=0.05 * i, b_factor=10.0 * i)
+            for i in range(3)]
+    out = {"stack": stack, "volume": vol, "quats": quats, "trans": trans,
+           "ctf_rows": np.array([[c.defocus_u, c.defocus_v, c.astigmatism_angle, c.voltage, c.spherical_aberration,
+                                  c.amplitude_contrast, c.phase_shift, c.b_factor] for c in ctfs])}
+    with tempfile.TemporaryDirectory() as d:
+        rio.write_mrc(os.path.join(d, "s.mrcs"), stack, 1.37, volume=False)
+        rio.write_mrc(os.path.join(d, "v.mrc"), vol, 2.5)
+        rio.write_meta(os.path.join(d, "m.txt"), quats, trans, ctfs)
+        for k, f in (("stack_bytes", "s.mrcs"), ("volume_bytes", "v.mrc"), ("meta_bytes", "m.txt")):
+            out[k] = np.frombuffer(open(os.path.join(d, f), "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "io.npz"), **out)
+    print("io", sorted(out))
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     for name in sys.argv[1:]:
         globals()[name]()

@@ -175,3 +175,49 @@ def test_simulate_host_draws_match_reference():
         assert np.array_equal(d, g[f"{k}_defocus"])
         rot = np.stack([cs.Pose.from_quaternion(q).rotation for q in rec_q])
         np.testing.assert_allclose(rot, g[f"{k}_rotations"], rtol=0, atol=1e-15)
+
+
+def test_io_files_match_reference_bytes(tmp_path):
+    """MRC stack / volume and the metadata table are written byte-identically to the
+    reference's io.py, and the reference's files read back exactly (tests/golden/io.npz)."""
+    from paper_2508_04929_b200 import io as cio
+
+    g = load_golden("io")
+    ctfs = [cs.CtfParams(*row) for row in g["ctf_rows"]]
+    cio.write_mrc(tmp_path / "s.mrcs", g["stack"], 1.37, volume=False)
+    cio.write_mrc(tmp_path / "v.mrc", g["volume"], 2.5)
+    cio.write_meta(tmp_path / "m.txt", g["quats"], g["trans"], ctfs)
+    for name, key in (("s.mrcs", "stack_bytes"), ("v.mrc", "volume_bytes"), ("m.txt", "meta_bytes")):
+        assert (tmp_path / name).read_bytes() == g[key].tobytes(), name
+    ref = tmp_path / "ref.mrcs"
+    ref.write_bytes(g["stack_bytes"].tobytes())
+    data, apix = cio.read_mrc(ref)
+    assert np.array_equal(data, g["stack"]) and apix == pytest.approx(1.37, rel=1e-7)
+    (tmp_path / "ref.txt").write_bytes(g["meta_bytes"].tobytes())
+    rows = cio.read_meta(tmp_path / "ref.txt")
+    assert np.array_equal(rows[:, 1:5], g["quats"]) and np.array_equal(rows[:, 5:7], g["trans"])
+    ds = cio.load_dataset(ref, tmp_path / "ref.txt")
+    assert len(ds) == 3 and ds.grid.size == 16
+    assert np.array_equal(ds.records[1].translation, g["trans"][1])
+    assert ds.records[2].ctf.b_factor == g["ctf_rows"][2][7]
+
+
+def test_io_errors(tmp_path):
+    from paper_2508_04929_b200 import io as cio
+
+    bad = tmp_path / "bad.mrc"
+    bad.write_bytes(b"\0" * 100)
+    with pytest.raises(cs.DataError):
+        cio.read_mrc(bad)
+    cio.write_mrc(tmp_path / "ok.mrcs", np.zeros((2, 4, 4), np.float32), 1.0)
+    blob = bytearray((tmp_path / "ok.mrcs").read_bytes())
+    blob[12] = 1  # mode 1
+    (tmp_path / "m1.mrc").write_bytes(bytes(blob))
+    with pytest.raises(cs.UnsupportedModeError):
+        cio.read_mrc(tmp_path / "m1.mrc")
+    (tmp_path / "short.mrc").write_bytes((tmp_path / "ok.mrcs").read_bytes()[:-4])
+    with pytest.raises(cs.DataError):
+        cio.read_mrc(tmp_path / "short.mrc")
+    (tmp_path / "meta.txt").write_text("# x\n1 0 0 0 0 0 0 1 1 0 300 2.7 0.1 0 0\n")
+    with pytest.raises(cs.DataError):
+        cio.read_meta(tmp_path / "meta.txt")
