@@ -181,6 +181,16 @@ int cgs_ctf_mse(void *plan, const float *render, const float *obs, int32_t B, cg
 int cgs_fourier_filter(const float *in, float *out, int32_t B, cgs_grid grid, const double *ctf,
                        const double *shifts, void *stream);
 
+/* ---- K8: voxelize (evaluate.voxelize, evaluate.py:76-122, and
+ * voxelize_gaussians, _kernels.py:193-235) ----------------------------------
+ * Samples the mixture params f64 [n][11] at the D^3 voxel centres, culled on
+ * q < 6.5^2 like the rasterizer: out f64 [D][D][D] indexed [z][y][x].
+ * Deterministic (int64 fixed-point accumulation).  ws: cgs_voxelize_workspace_bytes(n)
+ * bytes; status gets CGS_STATUS_DEGENERATE_ROTATION (may be NULL). */
+size_t cgs_voxelize_workspace_bytes(int64_t n);
+int cgs_voxelize(const double *params, int64_t n, cgs_grid grid, double *out, void *ws, int32_t *status,
+                 void *stream);
+
 /* ---- K5: fused backward (backward_pixels, _kernels.py:128-190, plus the
  * per-image part of rasterize_backward, splat.py:332-349) ------------------
  * Gaussian-major: each CTA owns a chunk of Gaussians and a group of images,

@@ -29,6 +29,7 @@ from .exceptions import (
     DivergenceError,
     UnsupportedModeError,
 )
+from .evaluate import FscCurve, VoxelVolume, fsc, gold_standard_fsc, voxelize
 from .mixture import (
     GaussianMixture,
     GaussianParams,

@@ -293,6 +293,23 @@ def io_cases():
     print("io", sorted(out))
 
 
+def evaluate_cases():
+    """evaluate.voxelize and fsc (evaluate.py:76-179) on small mixtures."""
+    from cryosplat.evaluate import fsc, fsc_table, voxelize
+
+    grid = cs.GridSpec(32, 0.5, 2.0)
+    rng = np.random.default_rng(5)
+    a = random_mixture(rng, 12, grid, scale_px=(0.6, 2.5), mean_range=0.35)
+    b = cs.GaussianMixture(a.params + np.concatenate([rng.normal(0, 0.01, (12, 3)), rng.normal(0, 0.1, (12, 8))], 1))
+    va, vb = voxelize(a, grid), voxelize(b, grid)
+    c = fsc(va, vb)
+    out = {"a_params": a.params, "b_params": b.params, "va": va.voxels, "vb": vb.voxels,
+           "corr": c.correlations, "res": np.array([c.resolution_0143 or np.nan, c.resolution_05 or np.nan]),
+           "table": np.array(fsc_table(c))}
+    np.savez_compressed(os.path.join(OUT, "evaluate.npz"), **out)
+    print("evaluate", sorted(out), c.resolution_0143, c.resolution_05)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     for name in sys.argv[1:]:
         globals()[name]()

@@ -470,3 +470,22 @@ def test_dataset_ingest_to_device(oracle, tmp_path):
         assert rel_l2(o[i], ref) < 1e-5
         assert np.allclose(poses[i, :9].reshape(3, 3), r.pose.rotation, atol=1e-15)
     assert np.array_equal(cs.load_checkpoint(truth_path).params, truth.params)
+
+
+def test_voxelize_and_fsc_match_reference():
+    """K8 voxelize and the GPU FSC against the reference's evaluate.py outputs
+    (tests/golden/evaluate.npz): volumes to fp64 rounding, curves and resolutions."""
+    g = load_golden("evaluate")
+    grid = cs.GridSpec(32, 0.5, 2.0)
+    va = cs.voxelize(cs.GaussianMixture(g["a_params"]), grid)
+    vb = cs.voxelize(cs.GaussianMixture(g["b_params"]), grid)
+    for v, ref in ((va, g["va"]), (vb, g["vb"])):
+        assert np.max(np.abs(v.voxels - ref)) <= 1e-12 * np.max(np.abs(ref))
+        assert np.array_equal(v.voxels == 0, ref == 0)  # the same culled voxel set
+    c = cs.fsc(va, vb)
+    np.testing.assert_allclose(c.correlations, g["corr"], rtol=0, atol=1e-10)
+    np.testing.assert_allclose([c.resolution_0143 or np.nan, c.resolution_05 or np.nan], g["res"], rtol=1e-9)
+    # deterministic volume and curve
+    va2 = cs.voxelize(cs.GaussianMixture(g["a_params"]), grid)
+    assert np.array_equal(va.voxels, va2.voxels)
+    assert np.array_equal(cs.fsc(va, vb).correlations, c.correlations)
