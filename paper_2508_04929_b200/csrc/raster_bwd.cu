@@ -133,6 +133,13 @@ __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, 
 //
 // Along a row e_{k+1} = e_k g_k, g_{k+1} = g_k c (c = 2^(2A)), restarted
 // exactly every 32 columns (relative error < 2e-5).
+//
+// sum g (the -sub sum g part of sA = sum g (e - sub)) is not accumulated: it
+// is at most sub sum |g| = 6.7e-10 sum |g|, while the fp32 rounding already
+// in sum g e is ~6e-8 sum |g| e with mean e ~0.05 over a footprint, so the term
+// is below a quarter of that rounding (1e-8 of the gradient; tolerance 1e-3)
+// and costs one packed add per column on the FMA pipe that bounds this loop
+// (-6% kernel time).  -DCGS_BWD_EXACT_SUB restores it.
 constexpr int kChunk = 32;
 constexpr float kMinSeedLog2 = -100.f;  // joint row-pair walks need every live seed e >= 2^-100
 
@@ -176,7 +183,9 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
             float2 C = {0.f, 0.f}, S1 = {0.f, 0.f}, S2 = {0.f, 0.f}, SG = {0.f, 0.f};
             auto column = [&](float2 V) {
                 f2acc_fma(C, V, E);
+#ifdef CGS_BWD_EXACT_SUB
                 f2acc_add(SG, V);
+#endif
                 f2acc_add(S1, C);
                 f2acc_add(S2, S1);
                 f2scale(E, G);
