@@ -240,7 +240,9 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
             }
             const float2 DYE = f2mul(DY, r.e), DYX = f2mul(DY, r.x);
             M.e += f2sum(r.e);
+#ifdef CGS_BWD_EXACT_SUB
             M.g += (m0 ? r.g.x : 0.f) + (m1 ? r.g.y : 0.f);
+#endif
             M.x += f2sum(r.x);
             M.xx += f2sum(r.xx);
             M.y += f2sum(DYE);
