@@ -586,6 +586,221 @@ static int launch_fourier_filter(const float *in, float *out, int B, double pix,
     return check_launch("fourier_filter_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// K4, one image per CTA (the training step's default for D = 64 / 128).
+//
+// The pair kernel above needs a full D x (D+1) complex array per CTA (132 KB at
+// D = 128: one CTA per SM, 128 CTAs for 148 SMs).  Here each CTA keeps one
+// image's half spectrum, D rows x (D/2 + 1) complex (66.5 KB) plus its filter
+// table (33 KB): two CTAs per SM, 256 CTAs.  Real transforms by the two-for-one trick:
+//  * rows, forward: rows 2j and 2j+1 go through one complex FFT as
+//    z = x_2j + i x_2j+1; with Z(-k) from the same transform,
+//    X_2j(k) = (Z(k) + conj Z(-k)) / 2, X_2j+1(k) = (Z(k) - conj Z(-k)) / 2i,
+//    for k = 0..D/2 (the rest is their conjugate mirror);
+//  * columns: D/2 + 1 complex FFTs (permuted order along y, as in WarpFft);
+//  * filter: H_sym / D^2 per half-spectrum element, evaluated once per image
+//    (fp64 chi) into a shared-memory table used by both CTF passes;
+//  * columns inverse (mirror network, natural order), then rows inverse:
+//    Z(k) = X_2j(k) + i X_2j+1(k) over all k (conjugate mirror above D/2)
+//    through one complex inverse FFT gives rows 2j and 2j+1 as real and imag.
+// The real rows live in the same shared array (a row of D/2 + 1 float2 holds
+// D + 2 floats), each warp rewriting only its own row pairs.
+constexpr int kR2cThreads = 256;
+
+// forward real 2-D FFT of the real image held row-wise (floats, row stride 2P)
+// in X: afterwards X[py][kx] = spectrum at (perm_k(py), kx), kx <= D/2
+template <int R>
+__device__ __forceinline__ void r2c_2d(float2 *X, const WarpFft<R> &F) {
+    constexpr int D = 32 * R, P = D / 2 + 1, NW = kR2cThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *Xf = reinterpret_cast<float *>(X);
+    for (int j = warp; j < D / 2; j += NW) {
+        float2 v[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = make_float2(Xf[(2 * j) * 2 * P + lane + 32 * t],
+                                                       Xf[(2 * j + 1) * 2 * P + lane + 32 * t]);
+        F.fwd(v);
+        // park Z(k): k <= D/2 in row 2j slot k, k > D/2 in row 2j+1 slot k - D/2
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int k = m + R * bitrev5(lane);
+            X[k <= D / 2 ? (2 * j) * P + k : (2 * j + 1) * P + (k - D / 2)] = v[m];
+        }
+        __syncwarp();
+        float2 a[3], c[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            const int k = lane + 32 * u;
+            if (k > D / 2) break;
+            const int nk = (D - k) % D;
+            const float2 zk = X[(2 * j) * P + k];
+            const float2 zn = nk <= D / 2 ? X[(2 * j) * P + nk] : X[(2 * j + 1) * P + (nk - D / 2)];
+            a[u] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));  // (Z(k) + conj Z(-k)) / 2
+            c[u] = make_float2(0.5f * (zk.y + zn.y), 0.5f * (zn.x - zk.x));  // (Z(k) - conj Z(-k)) / 2i
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            const int k = lane + 32 * u;
+            if (k > D / 2) break;
+            X[(2 * j) * P + k] = a[u];
+            X[(2 * j + 1) * P + k] = c[u];
+        }
+    }
+    __syncthreads();
+    for (int col = warp; col < P; col += NW) {  // columns: DIF, permuted along y
+        float2 v[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = X[(lane + 32 * t) * P + col];
+        F.fwd(v);
+#pragma unroll
+        for (int t = 0; t < R; ++t) X[(lane + 32 * t) * P + col] = v[t];
+    }
+}
+
+// inverse: columns (mirror network, natural order), then rows back to real
+// (unscaled: D^2 x the inverse DFT; the filter carries 1/D^2)
+template <int R>
+__device__ __forceinline__ void c2r_2d(float2 *X, const WarpFft<R> &F) {
+    constexpr int D = 32 * R, P = D / 2 + 1, NW = kR2cThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int col = warp; col < P; col += NW) {
+        float2 v[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = X[(lane + 32 * t) * P + col];
+        F.inv(v);
+#pragma unroll
+        for (int t = 0; t < R; ++t) X[(lane + 32 * t) * P + col] = v[t];
+    }
+    __syncthreads();
+    float *Xf = reinterpret_cast<float *>(X);
+    for (int j = warp; j < D / 2; j += NW) {
+        float2 v[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) {  // lane l, element m carries Z(m + R bitrev5(l))
+            const int k = m + R * bitrev5(lane);
+            const bool lo = k <= D / 2;
+            const int kk = lo ? k : D - k;
+            float2 a = X[(2 * j) * P + kk], c = X[(2 * j + 1) * P + kk];
+            if (!lo) { a.y = -a.y; c.y = -c.y; }
+            v[m] = make_float2(a.x - c.y, a.y + c.x);  // X_2j(k) + i X_2j+1(k)
+        }
+        F.inv(v);
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            Xf[(2 * j) * 2 * P + lane + 32 * t] = v[t].x;
+            Xf[(2 * j + 1) * 2 * P + lane + 32 * t] = v[t].y;
+        }
+    }
+    __syncthreads();
+}
+
+template <int R>
+__device__ __forceinline__ void half_filter(float2 *X, const float *__restrict__ Hh) {
+    constexpr int D = 32 * R, P = D / 2 + 1;
+    for (int i = threadIdx.x; i < D * P; i += kR2cThreads) {
+        const int py = i / P, kx = i - py * P;
+        const float h = Hh[perm_k<R>(py) * P + kx];
+        const float2 z = X[i];
+        X[i] = make_float2(z.x * h, z.y * h);
+    }
+    __syncthreads();
+}
+
+template <int R>
+__global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_r2c_kernel(
+    const float *__restrict__ render, const float *__restrict__ obs, const double *__restrict__ ctf, double pix,
+    float *__restrict__ model, float *__restrict__ upstream, double *__restrict__ loss, int32_t *status) {
+    constexpr int D = 32 * R, P = D / 2 + 1;
+    extern __shared__ float2 X[];
+    float *hb = reinterpret_cast<float *>(X + D * P);  // H_sym / D^2 over the half spectrum
+    __shared__ double scratch[kR2cThreads / 32];
+    __shared__ CtfConst cc;
+    float *Xf = reinterpret_cast<float *>(X);
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        CtfConst c = load_ctf(ctf + 8 * (int64_t)b, D, pix);
+        c.inv_dA = 1.0 / c.dA;
+        c.pl = kPiD * c.lam;
+        c.cs3 = 0.5 * kPiD * c.cs * c.lam * c.lam * c.lam;
+        cc = c;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < D * P; i += kR2cThreads) {
+        const int ky = i / P, kx = i - ky * P;
+        hb[i] = ctf_sym(cc, D, ky, kx) * (1.f / ((float)D * (float)D));
+    }
+    WarpFft<R> F;
+    F.init(threadIdx.x & 31);
+    {  // warm L2 with the observation, read only after the first CTF pass
+        const char *ob = reinterpret_cast<const char *>(obs + (int64_t)b * D * D);
+        for (int off = threadIdx.x * 128; off < D * D * (int)sizeof(float); off += kR2cThreads * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
+    }
+    const float4 *r4 = reinterpret_cast<const float4 *>(render + (int64_t)b * D * D);
+    for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
+        const int y = (4 * i) / D, x = 4 * i - y * D;
+        const float4 v = __ldg(r4 + i);
+        float *row = Xf + y * 2 * P + x;
+        row[0] = v.x; row[1] = v.y; row[2] = v.z; row[3] = v.w;
+    }
+    __syncthreads();
+    r2c_2d<R>(X, F);
+    __syncthreads();
+    half_filter<R>(X, hb);
+    c2r_2d<R>(X, F);
+    // residual 2/D^2 (model - obs), loss = mean (model - obs)^2 in fp64
+    const float sc = 2.f / (float)(D * D);
+    const float *o = obs + (int64_t)b * D * D;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < D * D; i += kR2cThreads) {
+        const int y = i / D, x = i - y * D;
+        const float m = Xf[y * 2 * P + x];
+        if (model) model[(int64_t)b * D * D + i] = m;
+        const float d = m - __ldg(o + i);
+        acc += (double)d * d;
+        Xf[y * 2 * P + x] = sc * d;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kR2cThreads / 32; ++w) t += scratch[w];
+        const double l = t / (double)(D * D);
+        loss[b] = l;
+        if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
+    }
+    // upstream = CTF^T (residual)
+    r2c_2d<R>(X, F);
+    __syncthreads();
+    half_filter<R>(X, hb);
+    c2r_2d<R>(X, F);
+    float4 *u4 = reinterpret_cast<float4 *>(upstream + (int64_t)b * D * D);
+    for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
+        const int y = (4 * i) / D, x = 4 * i - y * D;
+        const float *row = Xf + y * 2 * P + x;
+        u4[i] = make_float4(row[0], row[1], row[2], row[3]);
+    }
+}
+
+template <int R>
+static int launch_ctf_mse_r2c(const float *render, const float *obs, int B, double pix, const double *ctf,
+                              float *model, float *upstream, double *loss, int32_t *status, cudaStream_t st) {
+    constexpr int D = 32 * R, P = D / 2 + 1;
+    const size_t smem = (size_t)D * P * (sizeof(float2) + sizeof(float));
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(ctf_mse_r2c_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    ctf_mse_r2c_kernel<R><<<B, kR2cThreads, smem, st>>>(render, obs, ctf, pix, model, upstream, loss, status);
+    return check_launch("ctf_mse_r2c_kernel");
+}
+
 template <int R>
 static int launch_ctf_mse_fused(const float *render, const float *obs, int B, double pix, const double *ctf,
                                 float *model, float *upstream, double *loss, int32_t *status, cudaStream_t st) {
@@ -697,6 +912,12 @@ extern "C" int cgs_ctf_mse(void *plan, const float *render, const float *obs, in
     static const bool force_cufft = getenv("CGS_CTF_CUFFT") && getenv("CGS_CTF_CUFFT")[0] == '1';
     if (ctf && !force_cufft && render != upstream && grid.pixel_size > 0 && B > 0) {
         cudaStream_t st = (cudaStream_t)stream;
+        static const bool pair_kernel = getenv("CGS_CTF_PAIR") && getenv("CGS_CTF_PAIR")[0] == '1';
+        if (!pair_kernel && (grid.size == 128 || grid.size == 64)) {
+            if (grid.size == 128)
+                return launch_ctf_mse_r2c<4>(render, obs, B, grid.pixel_size, ctf, model, upstream, loss, status, st);
+            return launch_ctf_mse_r2c<2>(render, obs, B, grid.pixel_size, ctf, model, upstream, loss, status, st);
+        }
         if (grid.size == 128)
             return launch_ctf_mse_fused<4>(render, obs, B, grid.pixel_size, ctf, model, upstream, loss, status, st);
         if (grid.size == 64)
