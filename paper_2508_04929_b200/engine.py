@@ -30,7 +30,9 @@ except ImportError:  # pragma: no cover - torch is in the image
     torch = None
 
 DEFAULT_TILE = 32
-DEFAULT_IMAGES_PER_GROUP = 16
+# images per backward CTA (K5 partial groups): 8 balances the 3k-CTA grid against the partials
+# the epilogue reads (measured 4..64 on C2; CGS_IMAGES_PER_GROUP overrides for A/B)
+DEFAULT_IMAGES_PER_GROUP = int(os.environ.get("CGS_IMAGES_PER_GROUP", "8"))
 
 
 def require_cuda():
