@@ -32,7 +32,10 @@
 namespace cgs {
 
 constexpr int kRThreads = 256;
-constexpr int kRChunk = 4096;              // Gaussians per CTA
+#ifndef CGS_FWD_CHUNK
+#define CGS_FWD_CHUNK 4096
+#endif
+constexpr int kRChunk = CGS_FWD_CHUNK;     // Gaussians per CTA
 constexpr int kRBandBytes = 64 * 1024;     // int32 accumulator rows per CTA
 constexpr int kWbBlock = 1024;
 constexpr float kFixedRange = 1073741824.f;  // 2^30
