@@ -31,7 +31,13 @@
 
 namespace cgs {
 
-constexpr int kRThreads = 256;
+#ifndef CGS_FWD_THREADS
+#define CGS_FWD_THREADS 512
+#endif
+#ifndef CGS_FWD_MINB
+#define CGS_FWD_MINB 2
+#endif
+constexpr int kRThreads = CGS_FWD_THREADS;
 #ifndef CGS_FWD_CHUNK
 #define CGS_FWD_CHUNK 4096
 #endif
@@ -165,7 +171,7 @@ __device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, 
 // Gaussians is spatial (Morton, chosen for the backward's region staging), so
 // the chunk visits Gaussians in a scrambled order: logical index i maps to
 // g = (i * A) mod n with gcd(A, n) = 1, stepped incrementally.
-__global__ void __launch_bounds__(kRThreads, 3) raster_fwd_atomic_kernel(
+__global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, GridF G,
     const float *__restrict__ scale_ptr, int HB, int64_t mulA, int *__restrict__ out) {
     extern __shared__ int band[];
