@@ -438,7 +438,10 @@ __global__ void __launch_bounds__(kBwdThreadsBand, 3) raster_bwd_band_kernel(
 #endif
 constexpr int kRegThreads = CGS_BWD_REG_THREADS;
 constexpr int kMaxPoseImages = 64;  // image groups up to this size keep fp32 poses in shared memory
-constexpr int kRegFloats = 4096;  // 16 KB per band
+#ifndef CGS_BWD_REG_FLOATS
+#define CGS_BWD_REG_FLOATS 6144
+#endif
+constexpr int kRegFloats = CGS_BWD_REG_FLOATS;  // 24 KB per band (measured 8..32 KB)
 
 template <bool kPoseSmem>
 __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_kernel(
