@@ -221,6 +221,7 @@ class Reconstructor:
         self.tile = tile
         self._pipes: dict = {}
         self._copy_stream = None  # H2D stream of step_host
+        self._h2d_slots: dict = {}  # step_host's double-buffered device inputs
 
     # -- helpers -------------------------------------------------------------
     def local_slice(self, indices: np.ndarray) -> np.ndarray:
@@ -269,15 +270,33 @@ class Reconstructor:
         compute = torch.cuda.current_stream(dev)
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(dev)
-        with torch.cuda.stream(self._copy_stream):
-            o = obs.to(dev, non_blocking=True)
-            p = poses.to(dev, non_blocking=True)
-            c = None if ctfs is None else ctfs.to(dev, non_blocking=True)
-        compute.wait_stream(self._copy_stream)
-        for t in (o, p, c):  # allocated on the copy stream, consumed on the compute stream
-            if t is not None:
-                t.record_stream(compute)
+        # two preallocated device slots per batch shape, alternating: no allocator
+        # traffic per step; a slot is refilled only after the step that read it
+        key = (tuple(obs.shape), ctfs is None)
+        slots = self._h2d_slots.get(key)
+        if slots is None:
+            def slot():
+                return {"o": torch.empty(obs.shape, dtype=obs.dtype, device=dev),
+                        "p": torch.empty(poses.shape, dtype=poses.dtype, device=dev),
+                        "c": None if ctfs is None else torch.empty(ctfs.shape, dtype=ctfs.dtype, device=dev),
+                        "done": None}
+            slots = self._h2d_slots[key] = [slot(), slot(), 0]
+        sl = slots[slots[2]]
+        slots[2] ^= 1
+        cs = self._copy_stream
+        if sl["done"] is not None:
+            cs.wait_event(sl["done"])
+        with torch.cuda.stream(cs):
+            sl["o"].copy_(obs, non_blocking=True)
+            sl["p"].copy_(poses, non_blocking=True)
+            if ctfs is not None:
+                sl["c"].copy_(ctfs, non_blocking=True)
+        compute.wait_stream(cs)
+        o, p, c = sl["o"], sl["p"], sl["c"]
         loss = self.step_batch(o, p, c, lr, global_batch=global_batch)
+        if sl["done"] is None:
+            sl["done"] = torch.cuda.Event()
+        sl["done"].record(compute)
         if loss_out is not None:
             loss_out.copy_(loss, non_blocking=True)
         del torch
