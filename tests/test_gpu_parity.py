@@ -489,3 +489,25 @@ def test_voxelize_and_fsc_match_reference():
     va2 = cs.voxelize(cs.GaussianMixture(g["a_params"]), grid)
     assert np.array_equal(va.voxels, va2.voxels)
     assert np.array_equal(cs.fsc(va, vb).correlations, c.correlations)
+
+
+@pytest.mark.parametrize("D,ctf", [(33, True), (96, True), (64, False), (48, True)])
+def test_full_step_other_sizes(oracle, D, ctf):
+    """The fused step on sizes outside the fast paths: odd D (the reference's D = 33 KAT
+    size, origin D // 2), D = 96 / 48 (cuFFT K4, not a 32 R size), no CTF; B = 3 (odd image
+    groups), random observations; losses and gradients against the oracle."""
+    grid = oracle.Grid(D, 0.5, 1.5)
+    params = oracle.init_random(400, 7, grid)
+    params[:, 3:6] += np.random.default_rng(D).normal(0.0, 0.5, (400, 3))  # mixed footprint sizes
+    poses = [oracle.sample_pose(np.random.default_rng(50 + i)) for i in range(3)]
+    obs = np.random.default_rng(D + 1).standard_normal((3, D, D)).astype(np.float32) * 1e-3
+    ctfs = None
+    Hs = None
+    if ctf:
+        cp = [oracle.Ctf(12000.0 + 3000 * i, 14000.0, 0.3 * i) for i in range(3)]
+        ctfs = np.stack([c.as_array() for c in cp])
+        Hs = [oracle.ctf_evaluate(c, grid) for c in cp]
+    losses, grads, _ = _full_step_device(params, poses, grid, obs, ctfs)
+    ref_losses, ref_grads = oracle.batch_step(params, poses, grid, Hs, obs)
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
