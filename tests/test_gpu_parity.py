@@ -529,3 +529,21 @@ def test_readme_pipeline_end_to_end():
     assert np.mean(losses[-1]) < np.mean(losses[0])
     curve = cs.fsc(cs.voxelize(mix, grid), cs.voxelize(truth, grid))
     assert curve.correlations[0] > 0.5
+
+
+def test_full_step_large_footprints_d256(oracle):
+    """D = 256 with a few large Gaussians (footprints of ~100 px): the backward's staged
+    region exceeds one 24 KB band (several bands per image), rows run past 32 pixels
+    (exact restarts), and the forward walks long spans; against the oracle."""
+    grid = oracle.Grid(256, 0.5, 1.5)
+    rng = np.random.default_rng(256)
+    params = oracle.init_random(60, 3, grid)
+    params[:, 3:6] = oracle.inverse_activate(rng.uniform(0.01, 0.04, (60, 3)))  # 5..20 px sigma
+    params[:, 6:10] = rng.standard_normal((60, 4))
+    poses = [oracle.sample_pose(np.random.default_rng(70 + i)) for i in range(2)]
+    obs = rng.standard_normal((2, 256, 256)).astype(np.float32) * 1e-2
+    cp = [oracle.Ctf(15000.0, 15000.0), oracle.Ctf(20000.0, 17000.0, 0.4)]
+    losses, grads, _ = _full_step_device(params, poses, grid, obs, np.stack([c.as_array() for c in cp]))
+    ref_losses, ref_grads = oracle.batch_step(params, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs)
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
