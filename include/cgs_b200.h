@@ -226,6 +226,11 @@ int cgs_adam(double *params, const double *grads, double *m, double *v, int64_t 
 int cgs_epilogue_adam(const float *acc, int32_t G, int64_t n, double *params, double *m, double *v,
                       int32_t mode, double scale, double lr, double beta1, double beta2, double eps,
                       double bc1, double bc2, const int32_t *skip_if_status, void *stream);
+/* cgs_epilogue_adam with (lr, bc1, bc2) read from device memory hyper f64 [3],
+ * so a CUDA graph holding the step replays unchanged from step to step. */
+int cgs_epilogue_adam_dev(const float *acc, int32_t G, int64_t n, double *params, double *m, double *v,
+                          int32_t mode, double scale, double beta1, double beta2, double eps, const double *hyper,
+                          const int32_t *skip_if_status, void *stream);
 
 /* ---- measurement ----------------------------------------------------------
  * In-ellipse (image, Gaussian, pixel) pairs q < 6.5^2: the algorithmic work

@@ -80,6 +80,7 @@ PROTOTYPES = {
     "cgs_epilogue_grads": (ctypes.c_int, [P, I32, I64, P, I32, F64, P, P]),
     "cgs_adam": (ctypes.c_int, [P, P, P, P, I64, F64, F64, F64, F64, F64, F64, P]),
     "cgs_epilogue_adam": (ctypes.c_int, [P, I32, I64, P, P, P, I32, F64, F64, F64, F64, F64, F64, F64, P, P]),
+    "cgs_epilogue_adam_dev": (ctypes.c_int, [P, I32, I64, P, P, P, I32, F64, F64, F64, F64, P, P, P]),
     "cgs_count_pairs": (ctypes.c_int, [P, I64, P, I32, G, P, P]),
 }
 

@@ -134,8 +134,13 @@ __global__ void epilogue_adam_kernel(const float *__restrict__ part, int G, int6
                                      double *__restrict__ params, double *__restrict__ m,
                                      double *__restrict__ v, int mode, double scale, double lr,
                                      double b1, double b2, double eps, double bc1, double bc2,
-                                     const int32_t *__restrict__ skip) {
+                                     const int32_t *__restrict__ skip, const double *__restrict__ hyper) {
     if (skip && (*skip & (CGS_STATUS_BIN_OVERFLOW | CGS_STATUS_NONFINITE_LOSS))) return;
+    if (hyper) {  // device-resident (lr, bc1, bc2): one launch serves every step of a captured graph
+        lr = hyper[0];
+        bc1 = hyper[1];
+        bc2 = hyper[2];
+    }
     int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (g >= n) return;
     double acc[10], gr[11];
@@ -187,6 +192,15 @@ extern "C" int cgs_epilogue_adam(const float *acc, int32_t G, int64_t n, double 
                                  const int32_t *skip_if_status, void *stream) {
     if (G <= 0 || n <= 0 || !acc || !params || !m || !v) return CGS_ERR_ARG;
     epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        acc, G, n, params, m, v, mode, scale, lr, beta1, beta2, eps, bc1, bc2, skip_if_status);
+        acc, G, n, params, m, v, mode, scale, lr, beta1, beta2, eps, bc1, bc2, skip_if_status, nullptr);
+    return check_launch("epilogue_adam_kernel");
+}
+
+extern "C" int cgs_epilogue_adam_dev(const float *acc, int32_t G, int64_t n, double *params, double *m, double *v,
+                                     int32_t mode, double scale, double beta1, double beta2, double eps,
+                                     const double *hyper, const int32_t *skip_if_status, void *stream) {
+    if (G <= 0 || n <= 0 || !acc || !params || !m || !v || !hyper) return CGS_ERR_ARG;
+    epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        acc, G, n, params, m, v, mode, scale, 0.0, beta1, beta2, eps, 1.0, 1.0, skip_if_status, hyper);
     return check_launch("epilogue_adam_kernel");
 }

@@ -367,6 +367,12 @@ class StepPipeline:
                   float(scale), float(lr), float(beta1), float(beta2), float(eps), float(bc1), float(bc2),
                   _ptr(self.status), self.ctx.stream)
 
+    def adam_dev(self, params, m, v, hyper, *, scale, beta1, beta2, eps):
+        """K6 with (lr, bc1, bc2) read from the device tensor hyper f64 [3] (graph-capturable)."""
+        _lib.call("cgs_epilogue_adam_dev", _ptr(self.partial), self.G, self.n, _ptr(params), _ptr(m), _ptr(v),
+                  self.mode, float(scale), float(beta1), float(beta2), float(eps), _ptr(hyper), _ptr(self.status),
+                  self.ctx.stream)
+
     def overflowed(self) -> bool:
         return bool(int(self.status.item()) & _lib.CGS_STATUS_BIN_OVERFLOW)
 

@@ -222,6 +222,8 @@ class Reconstructor:
         self._pipes: dict = {}
         self._copy_stream = None  # H2D stream of step_host
         self._h2d_slots: dict = {}  # step_host's double-buffered device inputs
+        # step_host replays each slot's step as a CUDA graph (single GPU; CGS_GRAPHS=0 disables)
+        self.use_graphs = os.environ.get("CGS_GRAPHS", "1") == "1"
 
     # -- helpers -------------------------------------------------------------
     def local_slice(self, indices: np.ndarray) -> np.ndarray:
@@ -279,21 +281,30 @@ class Reconstructor:
                 return {"o": torch.empty(obs.shape, dtype=obs.dtype, device=dev),
                         "p": torch.empty(poses.shape, dtype=poses.dtype, device=dev),
                         "c": None if ctfs is None else torch.empty(ctfs.shape, dtype=ctfs.dtype, device=dev),
-                        "done": None}
+                        "hyper": torch.empty(3, dtype=torch.float64, device=dev),
+                        "graph": None, "done": None}
             slots = self._h2d_slots[key] = [slot(), slot(), 0]
         sl = slots[slots[2]]
         slots[2] ^= 1
         cs = self._copy_stream
         if sl["done"] is not None:
             cs.wait_event(sl["done"])
+        graphs = self.use_graphs and self.world == 1
         with torch.cuda.stream(cs):
+            if graphs:  # Adam's per-step scalars travel with the batch
+                cfg, t = self.config, self.t + 1
+                sl["hyper"].copy_(torch.tensor([lr, 1.0 - cfg.adam_beta1 ** t, 1.0 - cfg.adam_beta2 ** t],
+                                               dtype=torch.float64), non_blocking=True)
             sl["o"].copy_(obs, non_blocking=True)
             sl["p"].copy_(poses, non_blocking=True)
             if ctfs is not None:
                 sl["c"].copy_(ctfs, non_blocking=True)
         compute.wait_stream(cs)
         o, p, c = sl["o"], sl["p"], sl["c"]
-        loss = self.step_batch(o, p, c, lr, global_batch=global_batch)
+        if graphs:
+            loss = self._graph_step(sl, o, p, c, global_batch)
+        else:
+            loss = self.step_batch(o, p, c, lr, global_batch=global_batch)
         if sl["done"] is None:
             sl["done"] = torch.cuda.Event()
         sl["done"].record(compute)
@@ -301,6 +312,32 @@ class Reconstructor:
             loss_out.copy_(loss, non_blocking=True)
         del torch
         return loss
+
+    def _graph_step(self, sl, o, p, c, global_batch: int):
+        """One step of a step_host slot as a CUDA graph replay: the first use of a
+        slot runs eagerly and captures status clear, K0..K5 and K6 (with its
+        scalars in sl["hyper"]); later steps replay it with one launch."""
+        torch = _torch()
+        pipe = self.pipeline(o.shape[0])
+        cfg = self.config
+        scale = 1.0 / global_batch
+
+        def body():
+            pipe.clear_status()
+            pipe.forward_backward(self.params, p, o, c)
+            pipe.adam_dev(self.params, self.m, self.v, sl["hyper"], scale=scale, beta1=cfg.adam_beta1,
+                          beta2=cfg.adam_beta2, eps=cfg.adam_epsilon)
+
+        if sl["graph"] is None:
+            body()  # eager: also performs one-time kernel attribute setup outside the capture
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                body()
+            sl["graph"] = g
+        else:
+            sl["graph"].replay()
+        self.t += 1
+        return pipe.loss
 
     def step_batch(self, obs, poses, ctfs, lr: float, *, global_batch: int, events=None):
         """One step on device tensors of this rank's batch (obs f32 [b][D][D],

@@ -547,3 +547,31 @@ def test_full_step_large_footprints_d256(oracle):
     ref_losses, ref_grads = oracle.batch_step(params, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs)
     np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
     grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
+
+
+def test_step_host_graph_replay_matches_eager():
+    """step_host replays each input slot's step as a CUDA graph (Adam's lr / bias corrections
+    read from device memory); four steps must leave exactly the parameters and losses of the
+    eager step_batch path (the kernels are deterministic)."""
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    grid = cs.GridSpec(64, 0.5, 1.5)
+    rng = np.random.default_rng(9)
+    R = 24
+    rot = np.stack([cs.sample_pose(np.random.default_rng(300 + i)).rotation for i in range(R)])
+    obs = (rng.standard_normal((R, 64, 64)) * 1e-3).astype(np.float32)
+    ctfs = engine.ctf_array([cs.CtfParams(float(d), float(d)) for d in rng.uniform(1e4, 2e4, R)])
+    mix = cs.init_random(3000, 0, grid)
+    a = Reconstructor(grid, mix.params, obs, engine.pose_array(rot), ctfs, batch_size=8)
+    b = Reconstructor(grid, mix.params, obs, engine.pose_array(rot), ctfs, batch_size=8)
+    assert a.use_graphs
+    lh = torch.empty(8, dtype=torch.float64).pin_memory()
+    for k in range(4):
+        idx = torch.arange(8 * (k % 3), 8 * (k % 3) + 8, device=a.ctx.device)
+        o, p, c = (t.index_select(0, idx).contiguous() for t in (a.obs, a.poses, a.ctfs))
+        a.step_host(o.cpu().pin_memory(), p.cpu().pin_memory(), c.cpu().pin_memory(), 2e-3 * (k + 1),
+                    global_batch=8, loss_out=lh)
+        lb = b.step_batch(o, p, c, 2e-3 * (k + 1), global_batch=8)
+        torch.cuda.synchronize()
+        assert np.array_equal(lh.numpy(), lb.cpu().numpy())
+    assert torch.equal(a.params, b.params) and torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
