@@ -10,7 +10,8 @@
 // near lockstep, so no lane idles on another lane's rows and no cross-lane
 // reduction is needed.  Per pixel it accumulates moments of ge = g e in pixel
 // units (per row: sum ge, sum g, sum ge dx', sum ge dx'^2; per image the
-// dy-weighted row sums), which carry the reference's six raw sums exactly:
+// dy-weighted row sums), which carry the reference's six raw sums exactly
+// (the default kernel drops sum g, see bwd_rowpairs):
 //   sA = sum ge - sub sum g,  s_ab = 1/(2 h^2) (sum ge (Pd)_a (Pd)_b - p_ab sA),
 // with (Pd)_x = p00 dx', (Pd)_y = p01 dx' + k dy.  They are converted in
 // registers to the image-summable 10-float world-frame accumulator
@@ -18,10 +19,16 @@
 // summed over the CTA's images.  The CTA writes its image group's partial
 // once; the epilogue sums groups in a fixed order: bitwise reproducible.
 //
-// Staging: for D <= 160 each CTA double-buffers whole upstream images in
-// shared memory with 1-D bulk async copies (TMA engine, mbarrier completion),
-// so image b+1 streams in while image b is processed; larger D falls back to
-// synchronous row bands.
+// Kernels:
+//  * raster_bwd_region_kernel (default, natural layout): per image the CTA
+//    stages only the union of its Gaussians' footprint boxes (Morton order
+//    keeps it small), row-pair interleaved, and walks two rows per packed step
+//    (bwd_rowpairs); 256 threads, 64 registers, 4 CTAs per SM.
+//  * raster_bwd_db_kernel (CGS_BWD_KERNEL=db, D <= 160): whole upstream images
+//    double-buffered with 1-D bulk async copies (TMA engine, mbarrier), one row
+//    per step (bwd_rows).
+//  * raster_bwd_band_kernel (FFT layout, or D beyond the region band):
+//    synchronous row bands, one row per step.
 #include <cstdlib>
 
 #include "common.cuh"
