@@ -605,7 +605,10 @@ static int launch_fourier_filter(const float *in, float *out, int B, double pix,
 //    through one complex inverse FFT gives rows 2j and 2j+1 as real and imag.
 // The real rows live in the same shared array (a row of D/2 + 1 float2 holds
 // D + 2 floats), each warp rewriting only its own row pairs.
-constexpr int kR2cThreads = 256;
+#ifndef CGS_R2C_THREADS
+#define CGS_R2C_THREADS 384
+#endif
+constexpr int kR2cThreads = CGS_R2C_THREADS;
 
 // forward real 2-D FFT of the real image held row-wise (floats, row stride 2P)
 // in X: afterwards X[py][kx] = spectrum at (perm_k(py), kx), kx <= D/2
