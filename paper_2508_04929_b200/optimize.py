@@ -28,7 +28,7 @@ import numpy as np
 from . import _lib, engine, parallel
 from .ctf import CtfParams, phase_shift_translate
 from .exceptions import DegenerateRotationError, DivergenceError
-from .mixture import COL_RAW_SCALE, MODES, GaussianMixture, GridSpec, init_random, save_checkpoint
+from .mixture import MODES, GaussianMixture, GridSpec, init_random, save_checkpoint
 from .render import Pose, RenderedImage
 
 DIVERGENCE_FACTOR = 1e3

@@ -1,4 +1,4 @@
-import time, torch, numpy as np, sys
+import time, torch, sys
 sys.path.insert(0, '.')
 import bench
 from paper_2508_04929_b200.optimize import Reconstructor
