@@ -212,29 +212,31 @@ __device__ __forceinline__ Box footprint_box(const Splat2 &s, bool live, int ylo
     return b;
 }
 
-// Union of every thread's box.  red is shared scratch of 8 x (blockDim/32)
-// ints used in two halves by call parity, so one barrier per call suffices:
+// Union of every thread's box.  red is shared scratch [2][4][warps] used in
+// two halves by call parity, so one barrier per call suffices:
 // the half written now was last read two calls ago, before the previous call's
 // barrier.  That barrier also orders everything each thread did before the
 // call ahead of everything after it (callers rely on it).  Needs blockDim <= 1024.
-__device__ __forceinline__ Box block_union(const Box &b, int *red, int parity) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+template <int NW>  // warps per CTA
+__device__ __forceinline__ Box block_union(const Box &b, int (&red)[2][4][NW], int parity) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = __reduce_min_sync(0xffffffffu, b.x0), y0 = __reduce_min_sync(0xffffffffu, b.y0);
     const int x1 = __reduce_max_sync(0xffffffffu, b.x1), y1 = __reduce_max_sync(0xffffffffu, b.y1);
-    int *rr = red + (parity & 1) * 4 * nw;
+    int (&rr)[4][NW] = red[parity & 1];
     if (lane == 0) {
-        rr[warp] = x0;
-        rr[nw + warp] = x1;
-        rr[2 * nw + warp] = y0;
-        rr[3 * nw + warp] = y1;
+        rr[0][warp] = x0;
+        rr[1][warp] = x1;
+        rr[2][warp] = y0;
+        rr[3][warp] = y1;
     }
     __syncthreads();
-    const bool in = lane < nw;
+    const bool in = lane < NW;
+    const int l = in ? lane : 0;
     Box r;
-    r.x0 = __reduce_min_sync(0xffffffffu, in ? rr[lane] : 0x7fffffff);
-    r.x1 = __reduce_max_sync(0xffffffffu, in ? rr[nw + lane] : -1);
-    r.y0 = __reduce_min_sync(0xffffffffu, in ? rr[2 * nw + lane] : 0x7fffffff);
-    r.y1 = __reduce_max_sync(0xffffffffu, in ? rr[3 * nw + lane] : -1);
+    r.x0 = __reduce_min_sync(0xffffffffu, in ? rr[0][l] : 0x7fffffff);
+    r.x1 = __reduce_max_sync(0xffffffffu, in ? rr[1][l] : -1);
+    r.y0 = __reduce_min_sync(0xffffffffu, in ? rr[2][l] : 0x7fffffff);
+    r.y1 = __reduce_max_sync(0xffffffffu, in ? rr[3][l] : -1);
     return r;
 }
 

@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
     __shared__ __align__(16) float reg[kRegFloats + kRowPad];  // row-pair interleaved (bwd_rowpairs)
-    __shared__ int red[8 * (kRegThreads / 32)];
+    __shared__ int red[2][4][kRegThreads / 32];
     // Register budget: the walk needs ~40 registers, so per-thread state that
     // is touched once per image lives outside the register file: the world
     // accumulator in shared memory (column-major: conflict-free), poses as fp32
