@@ -42,7 +42,10 @@ constexpr int kRThreads = CGS_FWD_THREADS;
 #define CGS_FWD_CHUNK 4096
 #endif
 constexpr int kRChunk = CGS_FWD_CHUNK;     // Gaussians per CTA
-constexpr int kRBandBytes = 64 * 1024;     // int32 accumulator rows per CTA
+#ifndef CGS_FWD_BAND_KB
+#define CGS_FWD_BAND_KB 64
+#endif
+constexpr int kRBandBytes = CGS_FWD_BAND_KB * 1024;  // int32 accumulator rows per CTA
 constexpr int kWbBlock = 1024;
 constexpr float kFixedRange = 1073741824.f;  // 2^30
 constexpr float kContribRange = 4194304.f;   // 2^22
