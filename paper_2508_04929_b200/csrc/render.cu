@@ -25,6 +25,7 @@
 // c = 2^(2A): two FMULs per pixel instead of an MUFU.EX2, restarted every 32
 // pixels so the recurrence error stays below 2e-5.  Rounding to int uses the
 // FMA-pipe magic-number trick (common.cuh fast_rint) instead of F2I on the XU.
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -39,9 +40,10 @@ namespace cgs {
 #endif
 constexpr int kRThreads = CGS_FWD_THREADS;
 #ifndef CGS_FWD_CHUNK
-#define CGS_FWD_CHUNK 4096
+#define CGS_FWD_CHUNK 8192
 #endif
-constexpr int kRChunk = CGS_FWD_CHUNK;     // Gaussians per CTA
+constexpr int kRChunk = CGS_FWD_CHUNK;     // max Gaussians per CTA (fwd_chunks picks the split)
+constexpr int kRChunkMin = 512;
 #ifndef CGS_FWD_BAND_KB
 #define CGS_FWD_BAND_KB 64
 #endif
@@ -119,36 +121,46 @@ __global__ void __launch_bounds__(256) wbound_scale_kernel(float *part, int npar
     }
 }
 
-// Add one footprint's rows [ya, yb] into the int32 block at acc (pixel (r0, 0),
-// row stride ld), columns clipped to [xlo, xhi].
-__device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, int xlo, int xhi, int ya, int yb,
-                                         const Splat2 &s, float scale, float cut) {
+// One footprint's rows [ya, yb] into the int32 band at acc (pixel (r0, 0), row
+// stride ld), columns [0, xhi], with little work per row: kRecur is chosen per
+// footprint (every row shorter than 32 px -> the
+// two-pixel recurrence, else one exact exp per pixel), ceil / floor run on the
+// FMA pipe (adding 1.5*2^23 with directed rounding leaves the integer in the
+// low mantissa bits; the clamps also absorb spans beyond +-2^22 px), and the
+// row term C_k dy^2 comes from the span's own remainder,
+// -log2(e)/2 k dy^2 = log2(e)/2 (rem - cut).
+template <bool kRecur>
+__device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int ld, int xhi, int ya, int yb,
+                                              const Splat2 &s, float scale, float cut) {
+    constexpr float kM = 12582912.0f;
+    constexpr float kHalfL2e = 0.5f * 1.4426950408889634f;
     const float wS = s.w * scale, wsubS = s.w * kSub * scale;
     const float c = ex2_approx(2.f * s.A);  // g_{k+1} / g_k
-    const float c4 = (c * c) * (c * c);
+    const float c2 = c * c;
+    const float2 C13 = f2pack(c, c2 * c), C4 = f2pack(c2 * c2, c2 * c2);
+    const float A2 = 2.f * s.A, nHcut = -kHalfL2e * cut, xhiM = kM + (float)xhi;
     // v = wS e - wS sub + 1.5*2^23: the FFMA that evaluates the contribution
     // also places its rounded integer in the low mantissa bits (fast_rint)
-    const float2 WS = f2pack(wS, wS), BIAS = f2pack(12582912.0f - wsubS, 12582912.0f - wsubS);
-    const float2 C4 = f2pack(c4, c4);
+    const float2 WS = f2pack(wS, wS), BIAS = f2pack(kM - wsubS, kM - wsubS);
     float dy = (float)ya - s.mpy;
     float xcv = fmaf(-s.slope, dy, s.mpx);
     int *row = acc + (ya - r0) * ld;
-    for (int iy = ya; iy <= yb; ++iy, dy += 1.f, xcv -= s.slope, row += ld) {
+    for (int nr = yb - ya; nr >= 0; --nr, dy += 1.f, xcv -= s.slope, row += ld) {
         const float rem = fmaf(-s.k * dy, dy, cut);
         if (rem <= 0.f) continue;
-        const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
-        const int xa = max((int)ceilf(xcv - half), xlo);
-        const int xb = min((int)floorf(xcv + half), xhi);
-        if (xa > xb) continue;
-        const float dx = (float)xa - xcv;
-        const float Ckdy2 = s.Ck * dy * dy;
-        if (xb - xa < 32) {
-            // recurrence, two pixels per packed step (raster_bwd.cu bwd_rows)
+        const float sq = sqrt_approx(rem);
+        const float fa = fmaxf(__fadd_ru(fmaf(-sq, s.inv_sqrt_p00, xcv), kM), kM);
+        const float fb = fminf(__fadd_rd(fmaf(sq, s.inv_sqrt_p00, xcv), kM), xhiM);
+        if (fa > fb) continue;
+        const int xa = __float_as_int(fa) - 0x4B400000, xb = __float_as_int(fb) - 0x4B400000;
+        const float dx = (fa - kM) - xcv;
+        const float Ckdy2 = fmaf(kHalfL2e, rem, nHcut);
+        if (kRecur) {
             const float e0 = ex2_approx(fmaf(s.A * dx, dx, Ckdy2));
-            const float g0 = ex2_approx(s.A * fmaf(2.f, dx, 1.f));
-            const float g1 = g0 * c;
+            const float g0 = ex2_approx(fmaf(A2, dx, s.A));
+            const float t = g0 * g0;
             float2 E = f2pack(e0, e0 * g0);
-            float2 R = f2pack(g0 * g1, g1 * g1 * c);
+            float2 R = f2mul(f2pack(t, t), C13);
             int x = xa;
 #pragma unroll 1
             for (; x < xb; x += 2) {
@@ -159,7 +171,7 @@ __device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, 
                 f2scale(R, C4);
             }
             if (x == xb) atomicAdd(row + x, fast_rint(fmaf(wS, E.x, -wsubS)));
-        } else {  // long rows: exact exp per pixel
+        } else {
             float d = dx;
             for (int x = xa; x <= xb; ++x, d += 1.f)
                 atomicAdd(row + x, fast_rint(fmaf(wS, ex2_approx(fmaf(s.A * d, d, Ckdy2)), -wsubS)));
@@ -176,7 +188,7 @@ __device__ __forceinline__ void fwd_rows(int *__restrict__ acc, int r0, int ld, 
 // g = (i * A) mod n with gcd(A, n) = 1, stepped incrementally.
 __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, GridF G,
-    const float *__restrict__ scale_ptr, int HB, int64_t mulA, int *__restrict__ out) {
+    const float *__restrict__ scale_ptr, int HB, int64_t mulA, int chunk, int *__restrict__ out) {
     extern __shared__ int band[];
     const int D = G.D;
     const int b = blockIdx.y;
@@ -185,8 +197,8 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     for (int i = threadIdx.x; i < npx; i += kRThreads) band[i] = 0;
     const float scale = *scale_ptr;
     const PoseF P = load_pose_f(poses, b);
-    const int64_t i_begin = (int64_t)blockIdx.x * kRChunk;
-    const int64_t i_end = min(n, i_begin + kRChunk);
+    const int64_t i_begin = (int64_t)blockIdx.x * chunk;
+    const int64_t i_end = min(n, i_begin + chunk);
     const int64_t stepA = (kRThreads * mulA) % n;
     int64_t g = ((i_begin + threadIdx.x) % n) * mulA % n;
     __syncthreads();
@@ -199,13 +211,18 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
         // which is 0 wherever e < sub + 0.5 / wS.  Walk only q < cut with
         // e(cut) = sub + 0.4995 / wS (the 1e-3 margin keeps every pixel that
         // can round to >= 1 unit): the same integer image, far fewer updates.
-        const float thr = kSub + 0.4995f / (s.w * scale);
+        const float thr = fmaf(0.4995f, rcp_approx(s.w * scale), kSub);  // thr >= sub: no denormals
         if (!(thr < 1.f)) continue;
-        const float cut = fminf(kCutoffSq, -2.f * kLn2 * __log2f(thr));
+        const float cut = fminf(kCutoffSq, -2.f * kLn2 * lg2_approx(thr));
         const float hy = s.hy * sqrt_approx(cut * (1.f / kCutoffSq));
         const int ylo = max(max((int)ceilf(s.mpy - hy), 0), r0);
         const int yhi = min(min((int)floorf(s.mpy + hy), D - 1), r1 - 1);
-        if (ylo <= yhi) fwd_rows(band, r0, D, 0, D - 1, ylo, yhi, s, scale, cut);
+        if (ylo > yhi) continue;
+        // widest row = 2 sqrt(cut / p00) = 2 * 6.5 sqrt(cut / 6.5^2) / sqrt(p00)
+        if (13.f * sqrt_approx(cut * (1.f / kCutoffSq)) * s.inv_sqrt_p00 < 31.f)
+            fwd_rows_band<true>(band, r0, D, D - 1, ylo, yhi, s, scale, cut);
+        else
+            fwd_rows_band<false>(band, r0, D, D - 1, ylo, yhi, s, scale, cut);
     }
     __syncthreads();
     int *dst = out + (int64_t)b * D * D + (int64_t)r0 * D;
@@ -241,6 +258,25 @@ static int64_t scramble_multiplier(int64_t n) {
     return 1;
 }
 
+// Chunks per image: equal chunks of kRChunkMin..kRChunk Gaussians, the count
+// trading each CTA's band init + flush (~200 Gaussians' worth) against the
+// last partial wave of CTAs over the resident slots, weighted 0.3 because CTA
+// lengths vary and the tail is soft.  C2 (50k, B = 256, 296 slots): 8 chunks
+// of 6250 (6.92 waves) run 2.6% faster than 13 of <= 4096 (11.24 waves).
+static int64_t fwd_chunks(int64_t n, int64_t ctas_per_chunk, int slots) {
+    static int64_t memo[4] = {-1, -1, -1, -1};
+    if (memo[0] == n && memo[1] == ctas_per_chunk && memo[2] == slots) return memo[3];
+    int64_t best = (n + kRChunk - 1) / kRChunk;
+    double best_cost = 1e300;
+    for (int64_t nc = best; nc <= (n + kRChunkMin - 1) / kRChunkMin; ++nc) {
+        const double waves = (double)(nc * ctas_per_chunk) / slots;
+        const double cost = (waves + 0.3 * (std::ceil(waves) - waves)) * ((double)n / (double)nc + 200.0);
+        if (cost < 0.999 * best_cost) { best_cost = cost; best = nc; }
+    }
+    memo[0] = n; memo[1] = ctas_per_chunk; memo[2] = slots; memo[3] = best;
+    return best;
+}
+
 extern "C" size_t cgs_render_workspace_bytes(int64_t n) {
     int64_t parts = (n + kWbBlock - 1) / kWbBlock;
     return (size_t)(2 * parts + 1) * sizeof(float);
@@ -268,9 +304,22 @@ extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, in
     }
     const int64_t count = (int64_t)B * D * D;
     cudaMemsetAsync(out, 0, sizeof(int) * count, st);
-    dim3 g((unsigned)((n + kRChunk - 1) / kRChunk), (unsigned)B, (unsigned)bands);
+    static int slots = 0;
+    static size_t slots_smem = 0;
+    if (slots == 0 || slots_smem != smem) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_atomic_kernel, kRThreads, smem);
+        slots = std::max(1, sms * per_sm);
+        slots_smem = smem;
+    }
+    int64_t nchunks = fwd_chunks(n, (int64_t)B * bands, slots);
+    const int chunk = (int)((n + nchunks - 1) / nchunks);
+    nchunks = (n + chunk - 1) / chunk;
+    dim3 g((unsigned)nchunks, (unsigned)B, (unsigned)bands);
     raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), part + 2 * parts, HB,
-                                                         scramble_multiplier(n), reinterpret_cast<int *>(out));
+                                                         scramble_multiplier(n), chunk, reinterpret_cast<int *>(out));
     int rc = check_launch("raster_fwd_atomic_kernel");
     if (rc) return rc;
     const int64_t threads = (count + 3) / 4;
