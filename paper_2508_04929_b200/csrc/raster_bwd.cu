@@ -509,14 +509,21 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
             const int by1 = min(R.y1 | 1, by0 + HBr - 1);  // odd: whole pairs
             const int np = (by1 - by0 + 1) >> 1;
             if (by0 != (R.y0 & ~1)) __syncthreads();  // previous band fully consumed (block_union covers the first)
-            // a warp per row pair, lanes along columns: coalesced row loads,
-            // one 64-bit store of both rows per column
-            for (int j = threadIdx.x >> 5; j < np; j += kRegThreads / 32) {
-                const int row = by0 + 2 * j;  // < D; row + 1 may be D (zero)
-                const float *s0 = src + row * D + R.x0;
-                const bool two = row + 1 < D;
-                for (int x = threadIdx.x & 31; x < W; x += 32)
-                    reg2[j * W + x] = f2pack(__ldg(s0 + x), two ? __ldg(s0 + D + x) : 0.f);
+            // flat over the band's np * W float2 slots, slot i = (pair j, column x):
+            // coalesced row loads, one 64-bit store of both rows per column
+            // (row D is zero).  j = floor((i + 0.5) / W) on the FMA pipe: a
+            // round-down FFMA into the 1.5*2^23 magic; (i + 0.5) / W is >= 0.5 / W
+            // from an integer, far above the rcp error; i is tracked as an exact float
+            {
+                const float invW = rcp_approx((float)W);
+                const float *sb = src + by0 * D + R.x0;
+                const int nel = np * W;
+                float fi = (float)threadIdx.x + 0.5f;
+                for (int i = threadIdx.x; i < nel; i += kRegThreads, fi += (float)kRegThreads) {
+                    const int j = __float_as_int(__fmaf_rd(fi, invW, 12582912.0f)) - 0x4B400000;
+                    const float *p = sb + j * (2 * D) + (i - j * W);
+                    reg2[i] = f2pack(__ldg(p), by0 + 2 * j + 1 < D ? __ldg(p + D) : 0.f);
+                }
             }
             __syncthreads();
             const int ya = max(ylo, by0), yb = min(yhi, by1);

@@ -30,9 +30,10 @@ except ImportError:  # pragma: no cover - torch is in the image
     torch = None
 
 DEFAULT_TILE = 32
-# images per backward CTA (K5 partial groups): 8 balances the 3k-CTA grid against the partials
-# the epilogue reads (measured 4..64 on C2; CGS_IMAGES_PER_GROUP overrides for A/B)
-DEFAULT_IMAGES_PER_GROUP = int(os.environ.get("CGS_IMAGES_PER_GROUP", "8"))
+# images per backward CTA (K5 partial groups): 10 balances the grid (5k CTAs on C2) against the
+# partials the epilogue reads (measured 4..64 on C2, 6..12 within 1%; CGS_IMAGES_PER_GROUP
+# overrides for A/B)
+DEFAULT_IMAGES_PER_GROUP = int(os.environ.get("CGS_IMAGES_PER_GROUP", "10"))
 
 
 def require_cuda():

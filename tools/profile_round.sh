@@ -2,5 +2,5 @@ set -x
 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"raster_bwd|raster_fwd_atomic|ctf_mse_fused" -s 9 -c 3 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"raster_bwd|raster_fwd_atomic|ctf_mse" -s 9 -c 3 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 tail -c 300 gpurun_out/bench_full.json
