@@ -264,7 +264,7 @@ static int64_t scramble_multiplier(int64_t n) {
 // lengths vary and the tail is soft.  C2 (50k, B = 256, 296 slots): 8 chunks
 // of 6250 (6.92 waves) run 2.6% faster than 13 of <= 4096 (11.24 waves).
 static int64_t fwd_chunks(int64_t n, int64_t ctas_per_chunk, int slots) {
-    static int64_t memo[4] = {-1, -1, -1, -1};
+    thread_local int64_t memo[4] = {-1, -1, -1, -1};
     if (memo[0] == n && memo[1] == ctas_per_chunk && memo[2] == slots) return memo[3];
     int64_t best = (n + kRChunk - 1) / kRChunk;
     double best_cost = 1e300;
@@ -304,8 +304,8 @@ extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, in
     }
     const int64_t count = (int64_t)B * D * D;
     cudaMemsetAsync(out, 0, sizeof(int) * count, st);
-    static int slots = 0;
-    static size_t slots_smem = 0;
+    thread_local int slots = 0;
+    thread_local size_t slots_smem = 0;
     if (slots == 0 || slots_smem != smem) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
