@@ -575,3 +575,39 @@ def test_step_host_graph_replay_matches_eager():
         torch.cuda.synchronize()
         assert np.array_equal(lh.numpy(), lb.cpu().numpy())
     assert torch.equal(a.params, b.params) and torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
+
+
+def test_full_size_c2_properties(oracle):
+    """BASELINE configs[1] at full size (50k Gaussians, 128^2, B = 256) through properties that hold
+    at any size.  (1) A batch render equals the renders of its images alone, bitwise: the
+    fixed-point sums are order-free and the scale belongs to the mixture, whatever the chunk split.
+    (2) The backward is linear in the upstream: 2g gives exactly twice the partial accumulators
+    (every operation scales exactly by a power of two).  (3) Images of the batch match the oracle."""
+    grid = oracle.Grid(128, 0.5, 1.5)
+    n, B, D = 50000, 256, 128
+    params = oracle.init_random(n, 0, grid)
+    poses = [oracle.sample_pose(np.random.default_rng(1000 + i)) for i in range(B)]
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(D, 0.5, 1.5)
+    p = _dev(params, torch.float64)
+    P = _dev(engine.pose_array([W for W, _ in poses], [t for _, t in poses]), torch.float64)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    splat = engine.prepare(ctx, p, status)
+    full = torch.empty((B, D, D), dtype=torch.float32, device="cuda")
+    engine.render_direct(ctx, splat, n, P, gs, full)
+    for k in (0, 101, 255):
+        one = torch.empty((1, D, D), dtype=torch.float32, device="cuda")
+        engine.render_direct(ctx, splat, n, P[k:k + 1].contiguous(), gs, one)
+        assert torch.equal(one[0], full[k])
+    for k in (0, 255):
+        ref, _ = oracle.rasterize(params, poses[k][0], poses[k][1], grid)
+        assert rel_l2(full[k].cpu().numpy(), ref) < RENDER_TOL
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    up = torch.randn((B, D, D), generator=gen, device="cuda", dtype=torch.float32) * 1e-3
+    G = int(ctx.lib.cgs_bwd_groups(B, engine.DEFAULT_IMAGES_PER_GROUP))
+    part1 = torch.empty(G * n * 10, dtype=torch.float32, device="cuda")
+    part2 = torch.empty_like(part1)
+    engine.raster_bwd(ctx, splat, n, P, gs, up, out=part1)
+    engine.raster_bwd(ctx, splat, n, P, gs, up * 2, out=part2)
+    assert torch.equal(part2, part1 * 2)
+    assert int(status.item()) == 0
