@@ -264,7 +264,8 @@ class StepPipeline:
         self.loss = torch.empty(self.B, dtype=torch.float64, device=dev)
         self.G = int(ctx.lib.cgs_bwd_groups(self.B, self.ipg))
         self.partial = torch.empty(self.G * n * 10, dtype=torch.float32, device=dev)
-        self.acc = torch.empty(n * 10, dtype=torch.float32, device=dev)
+        # summed accumulator + one slot for the rank's skip flag (parallel.allreduce_accumulator)
+        self.acc = torch.zeros(n * 10 + 1, dtype=torch.float32, device=dev)
         self.plan = ctx.plan(D, self.B)
         self.render_ws = torch.empty(ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, dtype=torch.float32, device=dev)
         self.T = int(ctx.lib.cgs_bin_tiles(D, tile))
@@ -358,15 +359,16 @@ class StepPipeline:
         _lib.call("cgs_reduce_partials", _ptr(self.partial), self.G, self.n, _ptr(self.acc), self.ctx.stream)
         return self.acc
 
-    def adam(self, params, m, v, *, scale, lr, beta1, beta2, eps, t, acc=None, groups=None):
-        """K6 fused epilogue + Adam; acc defaults to this step's partials."""
+    def adam(self, params, m, v, *, scale, lr, beta1, beta2, eps, t, acc=None, groups=None, skip=None):
+        """K6 fused epilogue + Adam; acc defaults to this step's partials.  ``skip`` (int32 device
+        status) decides whether the update is skipped; default: this pipeline's own status."""
         src = self.partial if acc is None else acc
         G = self.G if acc is None else (groups or 1)
         bc1 = 1.0 - beta1 ** t
         bc2 = 1.0 - beta2 ** t
         _lib.call("cgs_epilogue_adam", _ptr(src), G, self.n, _ptr(params), _ptr(m), _ptr(v), self.mode,
                   float(scale), float(lr), float(beta1), float(beta2), float(eps), float(bc1), float(bc2),
-                  _ptr(self.status), self.ctx.stream)
+                  _ptr(self.status if skip is None else skip), self.ctx.stream)
 
     def adam_dev(self, params, m, v, hyper, *, scale, beta1, beta2, eps):
         """K6 with (lr, bc1, bc2) read from the device tensor hyper f64 [3] (graph-capturable)."""

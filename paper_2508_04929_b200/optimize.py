@@ -350,9 +350,10 @@ class Reconstructor:
         scale = 1.0 / global_batch
         self.t += 1
         if self.world > 1:
-            acc = parallel.allreduce_accumulator(pipe.reduce(), self.pg)
+            acc = pipe.reduce()
+            skip = parallel.allreduce_accumulator(acc, self.pg, status=pipe.status)
             pipe.adam(self.params, self.m, self.v, scale=scale, lr=lr, beta1=cfg.adam_beta1,
-                      beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t, acc=acc, groups=1)
+                      beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t, acc=acc, groups=1, skip=skip)
         else:
             pipe.adam(self.params, self.m, self.v, scale=scale, lr=lr, beta1=cfg.adam_beta1,
                       beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t)

@@ -611,3 +611,73 @@ def test_full_size_c2_properties(oracle):
     engine.raster_bwd(ctx, splat, n, P, gs, up * 2, out=part2)
     assert torch.equal(part2, part1 * 2)
     assert int(status.item()) == 0
+
+
+def _dp_gpu_worker(rank, world, port, out_path, poison):
+    import os
+    import sys
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    from conftest import ROOT
+
+    sys.path.insert(0, ROOT)
+    import paper_2508_04929_b200 as cs2
+    from paper_2508_04929_b200 import engine as eng
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    params, obs, poses, ctfs, grid = _dp_inputs(cs2, eng)
+    if poison and rank == 1:
+        obs = obs.copy()
+        obs[5, 0, 0] = np.nan  # image 5 is in rank 1's half of the batch
+    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=8, process_group=dist.group.WORLD)
+    idx = rec.local_slice(np.arange(8))
+    dev = rec.ctx.device
+    sel = torch.as_tensor(idx, device=dev)
+    rec.step_batch(rec.obs.index_select(0, sel).contiguous(), rec.poses.index_select(0, sel).contiguous(),
+                   rec.ctfs.index_select(0, sel).contiguous(), 1e-3, global_batch=8)
+    torch.cuda.synchronize()
+    if rank == 0:
+        np.save(out_path, rec.params_host())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _dp_inputs(cs2, eng):
+    grid = cs2.GridSpec(64, 0.5, 1.5)
+    rng = np.random.default_rng(21)
+    params = cs2.init_random(2000, 0, grid).params
+    rot = np.stack([cs2.sample_pose(np.random.default_rng(700 + i)).rotation for i in range(8)])
+    obs = (rng.standard_normal((8, 64, 64)) * 1e-3).astype(np.float32)
+    ctfs = eng.ctf_array([cs2.CtfParams(12000.0 + 500 * i, 12500.0 + 500 * i) for i in range(8)])
+    return params, obs, eng.pose_array(rot), ctfs, grid
+
+
+@pytest.mark.parametrize("poison", [False, True])
+def test_data_parallel_step_two_ranks(tmp_path, poison):
+    """Reconstructor.step_batch with a 2-rank process group (gloo; both ranks on this GPU, host-level
+    collectives only, no kernel waits on another rank) equals the single-process full-batch step;
+    a NaN observation on one rank makes both ranks skip the update."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = str(tmp_path / "dp.npy")
+    mp.spawn(_dp_gpu_worker, args=(2, port, out, poison), nprocs=2, join=True)
+    got = np.load(out)
+    params, obs, poses, ctfs, grid = _dp_inputs(cs, engine)
+    if poison:
+        np.testing.assert_array_equal(got, params)
+        return
+    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=8)
+    rec.step_batch(rec.obs, rec.poses, rec.ctfs, 1e-3, global_batch=8)
+    ref = rec.params_host()
+    assert rel_l2(got - params, ref - params) < 1e-5

@@ -106,3 +106,36 @@ def test_allreduce_is_noop_without_process_group():
 
     t = torch.ones(5)
     assert parallel.allreduce_accumulator(t) is t and torch.equal(t, torch.ones(5))
+
+
+def _skip_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_2508_04929_b200 import parallel
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    acc = torch.full((2 * 10 + 1,), float(rank + 1))
+    status = torch.tensor([4 if rank == 1 else 1], dtype=torch.int32)  # rank 1: non-finite loss
+    skip = parallel.allreduce_accumulator(acc, status=status)
+    clean = parallel.allreduce_accumulator(torch.zeros(21), status=torch.tensor([1], dtype=torch.int32))
+    out = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(out, torch.tensor([float(skip.item()), float(acc[0]), float(clean.item())], dtype=torch.float64))
+    if rank == 0:
+        np.save(out_path, torch.stack(out).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_skip_decision_is_shared_by_all_ranks(tmp_path):
+    """A non-finite loss on one rank makes every rank skip the Adam update (the flag travels in
+    the accumulator all-reduce), so replicated parameters cannot diverge; a degenerate-rotation
+    bit alone does not skip."""
+    out = str(tmp_path / "skip.npy")
+    mp.spawn(_skip_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    res = np.load(out)
+    assert res[:, 0].tolist() == [6.0, 6.0]  # SKIP_BITS on both ranks
+    assert res[:, 1].tolist() == [3.0, 3.0]  # the accumulator itself is summed
+    assert res[:, 2].tolist() == [0.0, 0.0]
