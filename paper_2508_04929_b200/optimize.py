@@ -80,6 +80,14 @@ class ParticleRecord:
         if not np.all(np.isfinite(self.image)):
             raise ValueError("particle image contains non-finite values")
 
+    @classmethod
+    def prevalidated(cls, image: np.ndarray, pose: Pose, ctf: CtfParams, translation: np.ndarray):
+        """A record whose fields the caller has already checked in bulk (square finite f32
+        image, f64 [2] translation), e.g. a whole simulated stack at once."""
+        r = object.__new__(cls)
+        r.image, r.pose, r.ctf, r.translation = image, pose, ctf, translation
+        return r
+
 
 @dataclass
 class Dataset:

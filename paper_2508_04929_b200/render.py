@@ -71,6 +71,22 @@ class Pose:
     def from_quaternion(cls, q, translation=(0.0, 0.0)) -> "Pose":
         return cls(quaternion_to_matrix(normalize_quaternion(q)), np.asarray(translation, float))
 
+    @classmethod
+    def from_quaternions(cls, qs) -> list:
+        """Poses of many quaternions (K, 4) at zero translation: the same matrices as
+        from_quaternion, validated in one vectorised check instead of one per pose."""
+        R = quaternion_to_matrix(normalize_quaternion(np.asarray(qs, dtype=np.float64).reshape(-1, 4)))
+        ortho = np.abs(np.einsum("kji,kjl->kil", R, R) - np.eye(3)).max(axis=(1, 2)) if len(R) else np.zeros(0)
+        if np.any(ortho > 1e-9) or np.any(np.abs(np.linalg.det(R) - 1.0) > 1e-9):
+            raise ValueError("pose rotation is not a proper rotation (orthonormal, det +1)")
+        out = []
+        for Rk in R:
+            p = object.__new__(cls)
+            p.rotation = Rk
+            p.translation = np.zeros(2)
+            out.append(p)
+        return out
+
     @property
     def translation3(self) -> np.ndarray:
         return np.array([self.translation[0], self.translation[1], 0.0])

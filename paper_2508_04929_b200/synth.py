@@ -252,7 +252,7 @@ def simulate(spec: SimSpec, *, noise: str = "numpy", chunk: int = 1024, keep_on_
     grid = spec.grid
     n, D = spec.num_particles, grid.size
     true_q, rec_q, ctfs, trans = _draws(spec)
-    R = np.stack([Pose.from_quaternion(q).rotation for q in true_q])
+    R = np.stack([p.rotation for p in Pose.from_quaternions(true_q)])
     ctx = engine.DeviceContext.get()
     clean = torch.empty((n, D, D), dtype=torch.float32, device=ctx.device)
     carr = engine.ctf_array(ctfs)
@@ -267,15 +267,18 @@ def simulate(spec: SimSpec, *, noise: str = "numpy", chunk: int = 1024, keep_on_
         gen = torch.Generator(device=ctx.device)
         gen.manual_seed(int(spec.noise.seed))
         clean += sigma * torch.randn(clean.shape, generator=gen, device=ctx.device, dtype=torch.float32)
+    if not bool(torch.isfinite(clean).all()):
+        raise ValueError("simulated particle images contain non-finite values")
     host = clean.cpu().numpy()
+    poses = Pose.from_quaternions(rec_q)
+    trans = np.asarray(trans, dtype=np.float64)
     records = []
     for i in range(n):
         img = host[i]
         if sigma > 0.0 and noise == "numpy":
             img = (img.astype(np.float64)
                    + np.random.default_rng(spec.noise.seed + i).normal(0.0, sigma, size=img.shape)).astype(np.float32)
-        records.append(ParticleRecord(image=img, pose=Pose.from_quaternion(rec_q[i]), ctf=ctfs[i],
-                                      translation=trans[i]))
+        records.append(ParticleRecord.prevalidated(img, poses[i], ctfs[i], trans[i]))
     images = None
     if keep_on_device:
         images = torch.as_tensor(np.stack([r.image for r in records])).to(ctx.device) if noise == "numpy" else clean
