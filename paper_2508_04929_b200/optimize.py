@@ -230,6 +230,7 @@ class Reconstructor:
         self._pipes: dict = {}
         self._copy_stream = None  # H2D stream of step_host
         self._h2d_slots: dict = {}  # step_host's double-buffered device inputs
+        self._idx_slots: dict = {}  # step's graph inputs (batch indices, gathered batch, Adam scalars)
         # step_host replays each slot's step as a CUDA graph (single GPU; CGS_GRAPHS=0 disables)
         self.use_graphs = os.environ.get("CGS_GRAPHS", "1") == "1"
 
@@ -260,11 +261,59 @@ class Reconstructor:
             pipe.grow(pipe.measure_items(self.params, poses))
 
     def step(self, indices, lr: float):
-        """One step over the global batch ``indices``; returns per-image losses (device)."""
+        """One step over the global batch ``indices``; returns per-image losses (device).
+
+        On one GPU the step (batch gather from the HBM-resident stack, status clear,
+        K0..K6) is a CUDA graph per batch size, replayed with this step's indices and
+        Adam scalars written into its static inputs (CGS_GRAPHS=0: eager)."""
         indices = np.asarray(indices)
         local = self.local_slice(indices)
+        if self.use_graphs and self.world == 1:
+            return self._graph_step_indexed(local, lr, global_batch=len(indices))
         obs, poses, ctfs = self._batch(local)
         return self.step_batch(obs, poses, ctfs, lr, global_batch=len(indices))
+
+    def _graph_step_indexed(self, local: np.ndarray, lr: float, *, global_batch: int):
+        torch = _torch()
+        dev = self.ctx.device
+        b = len(local)
+        key = (b, global_batch)
+        sl = self._idx_slots.get(key)
+        if sl is None:
+            D = self.grid.size
+            sl = self._idx_slots[key] = {
+                "idx": torch.empty(b, dtype=torch.int64, device=dev),
+                "o": torch.empty((b, D, D), dtype=torch.float32, device=dev),
+                "p": torch.empty((b, 12), dtype=torch.float64, device=dev),
+                "c": None if self.ctfs is None else torch.empty((b, 8), dtype=torch.float64, device=dev),
+                "hyper": torch.empty(3, dtype=torch.float64, device=dev), "graph": None}
+        cfg, t = self.config, self.t + 1
+        sl["idx"].copy_(torch.as_tensor(np.asarray(local, dtype=np.int64)), non_blocking=True)
+        sl["hyper"].copy_(torch.tensor([lr, 1.0 - cfg.adam_beta1 ** t, 1.0 - cfg.adam_beta2 ** t],
+                                       dtype=torch.float64), non_blocking=True)
+        pipe = self.pipeline(b)
+        scale = 1.0 / global_batch
+
+        def body():
+            torch.index_select(self.obs, 0, sl["idx"], out=sl["o"])
+            torch.index_select(self.poses, 0, sl["idx"], out=sl["p"])
+            if sl["c"] is not None:
+                torch.index_select(self.ctfs, 0, sl["idx"], out=sl["c"])
+            pipe.clear_status()
+            pipe.forward_backward(self.params, sl["p"], sl["o"], sl["c"])
+            pipe.adam_dev(self.params, self.m, self.v, sl["hyper"], scale=scale, beta1=cfg.adam_beta1,
+                          beta2=cfg.adam_beta2, eps=cfg.adam_epsilon)
+
+        if sl["graph"] is None:
+            body()  # eager first use (one-time kernel attribute setup outside the capture)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                body()
+            sl["graph"] = g
+        else:
+            sl["graph"].replay()
+        self.t = t
+        return pipe.loss
 
     def step_host(self, obs, poses, ctfs, lr: float, *, global_batch: int, loss_out=None):
         """Public end-to-end step from (pinned) HOST buffers of this rank's batch.
@@ -384,9 +433,10 @@ class Reconstructor:
         torch = _torch()
         local = morton_order(self.params[:, :3].cpu().numpy(), self.grid.extent)
         idx = torch.as_tensor(local, device=self.params.device)
-        self.params = self.params.index_select(0, idx).contiguous()
-        self.m = self.m.index_select(0, idx).contiguous()
-        self.v = self.v.index_select(0, idx).contiguous()
+        # in place: captured step graphs keep pointing at these buffers
+        self.params.copy_(self.params.index_select(0, idx))
+        self.m.copy_(self.m.index_select(0, idx))
+        self.v.copy_(self.v.index_select(0, idx))
         self.perm = self.perm[local]
 
 

@@ -67,7 +67,7 @@ def main():
     losses = []
     a.record()
     for b in batches:
-        losses.append(rec.step(b, args.lr))
+        losses.append(rec.step(b, args.lr).clone())
     e.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(e)
