@@ -577,6 +577,38 @@ def test_step_host_graph_replay_matches_eager():
     assert torch.equal(a.params, b.params) and torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
 
 
+def test_indexed_step_graph_matches_eager_across_reorder():
+    """Reconstructor.step replays a CUDA graph per batch size (gather by a device index buffer,
+    K0..K6); with shuffled batches, a ragged last batch and an in-place Morton reorder between
+    steps it must leave exactly the parameters and losses of the eager path."""
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    grid = cs.GridSpec(64, 0.5, 1.5)
+    rng = np.random.default_rng(19)
+    R = 30
+    rot = np.stack([cs.sample_pose(np.random.default_rng(500 + i)).rotation for i in range(R)])
+    obs = (rng.standard_normal((R, 64, 64)) * 1e-3).astype(np.float32)
+    ctfs = engine.ctf_array([cs.CtfParams(float(d), float(d)) for d in rng.uniform(1e4, 2e4, R)])
+    mix = cs.init_random(3000, 0, grid)
+    a = Reconstructor(grid, mix.params, obs, engine.pose_array(rot), ctfs, batch_size=8)
+    b = Reconstructor(grid, mix.params, obs, engine.pose_array(rot), ctfs, batch_size=8)
+    b.use_graphs = False
+    assert a.use_graphs
+    order = rng.permutation(R)
+    batches = [order[i:i + 8] for i in range(0, R, 8)] * 2  # 8, 8, 8, 6, then again
+    for k, bi in enumerate(batches):
+        if k == 4:
+            for r in (a, b):
+                r.params[:, :3] += 0.01  # move the means, then re-sort in place
+                r.reorder()
+        la = a.step(bi, 1e-3 * (1 + k)).clone()
+        lb = b.step(bi, 1e-3 * (1 + k)).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(la, lb)
+    assert torch.equal(a.params, b.params) and torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
+    assert np.array_equal(a.params_host(), b.params_host())
+
+
 def test_full_size_c2_properties(oracle):
     """BASELINE configs[1] at full size (50k Gaussians, 128^2, B = 256) through properties that hold
     at any size.  (1) A batch render equals the renders of its images alone, bitwise: the
