@@ -210,7 +210,8 @@ int cgs_reduce_partials(const float *partial, int32_t G, int64_t n, float *acc, 
 
 /* ---- K6: epilogue + Adam (splat.py:344-381, train.py:157-159, train.py:101-111)
  * grads f64 [n][11] = scale * chain(acc) for the raw parameters; mode
- * isotropic sums the three raw-scale gradients (train.py:157-159). */
+ * isotropic sums the three raw-scale gradients (train.py:157-159).
+ * acc [G][n][10] must be 8-byte aligned (read as float pairs); else CGS_ERR_ARG. */
 int cgs_epilogue_grads(const float *acc, int32_t G, int64_t n, const double *params, int32_t mode,
                        double scale, double *grads, void *stream);
 

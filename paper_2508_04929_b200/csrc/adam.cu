@@ -8,6 +8,7 @@
 // once per (image, Gaussian).  fp64 throughout (parameters and moments are
 // fp64 master copies, so tiny late-epoch updates survive as in the reference).
 #include <cmath>
+#include <cstdint>
 
 #include "common.cuh"
 
@@ -80,11 +81,32 @@ __device__ __forceinline__ void sum_groups(const float *__restrict__ part, int G
                                            int64_t g, double acc[10]) {
 #pragma unroll
     for (int c = 0; c < 10; ++c) acc[c] = 0.0;
-    for (int k = 0; k < G; ++k) {
-        const float *p = part + ((int64_t)k * n + g) * CGS_ACC_STRIDE;
+    // groups in order (fixed fp64 summation order), loads issued 4 groups ahead as
+    // 8-byte vectors: the kernel is bound by the latency of these 52 MB of reads
+    const float2 *base = reinterpret_cast<const float2 *>(part + g * CGS_ACC_STRIDE);
+    const int64_t gstride = n * (CGS_ACC_STRIDE / 2);
+    int k = 0;
+    for (; k + 4 <= G; k += 4) {
+        float2 v[4][5];
 #pragma unroll
-        for (int c = 0; c < 10; ++c) acc[c] += (double)p[c];
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) v[u][c] = __ldg(base + (k + u) * gstride + c);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                acc[2 * c] += (double)v[u][c].x;
+                acc[2 * c + 1] += (double)v[u][c].y;
+            }
     }
+    for (; k < G; ++k)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            const float2 w = __ldg(base + k * gstride + c);
+            acc[2 * c] += (double)w.x;
+            acc[2 * c + 1] += (double)w.y;
+        }
 }
 
 // AdamState.update for one element, operation order as train.py:103-111
@@ -171,7 +193,7 @@ extern "C" int cgs_reduce_partials(const float *partial, int32_t G, int64_t n, f
 
 extern "C" int cgs_epilogue_grads(const float *acc, int32_t G, int64_t n, const double *params,
                                   int32_t mode, double scale, double *grads, void *stream) {
-    if (G <= 0 || n <= 0 || !acc || !params || !grads) return CGS_ERR_ARG;
+    if (G <= 0 || n <= 0 || !acc || !params || !grads || (reinterpret_cast<uintptr_t>(acc) & 7)) return CGS_ERR_ARG;
     epilogue_grads_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         acc, G, n, params, mode, scale, grads);
     return check_launch("epilogue_grads_kernel");
@@ -190,7 +212,7 @@ extern "C" int cgs_epilogue_adam(const float *acc, int32_t G, int64_t n, double 
                                  double *v, int32_t mode, double scale, double lr, double beta1,
                                  double beta2, double eps, double bc1, double bc2,
                                  const int32_t *skip_if_status, void *stream) {
-    if (G <= 0 || n <= 0 || !acc || !params || !m || !v) return CGS_ERR_ARG;
+    if (G <= 0 || n <= 0 || !acc || !params || !m || !v || (reinterpret_cast<uintptr_t>(acc) & 7)) return CGS_ERR_ARG;
     epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         acc, G, n, params, m, v, mode, scale, lr, beta1, beta2, eps, bc1, bc2, skip_if_status, nullptr);
     return check_launch("epilogue_adam_kernel");
@@ -199,7 +221,8 @@ extern "C" int cgs_epilogue_adam(const float *acc, int32_t G, int64_t n, double 
 extern "C" int cgs_epilogue_adam_dev(const float *acc, int32_t G, int64_t n, double *params, double *m, double *v,
                                      int32_t mode, double scale, double beta1, double beta2, double eps,
                                      const double *hyper, const int32_t *skip_if_status, void *stream) {
-    if (G <= 0 || n <= 0 || !acc || !params || !m || !v || !hyper) return CGS_ERR_ARG;
+    if (G <= 0 || n <= 0 || !acc || !params || !m || !v || !hyper || (reinterpret_cast<uintptr_t>(acc) & 7))
+        return CGS_ERR_ARG;
     epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         acc, G, n, params, m, v, mode, scale, 0.0, beta1, beta2, eps, 1.0, 1.0, skip_if_status, hyper);
     return check_launch("epilogue_adam_kernel");

@@ -50,6 +50,10 @@ def test_invalid_arguments_are_rejected_without_touching_the_device():
     assert lib.cgs_prepare(None, 0, None, None, None) == 1
     assert lib.cgs_raster_fwd(None, 10, None, 1, g, 12, None, None, 0, None, 0, None) == 1
     assert lib.cgs_bin_count_bbox(None, 10, 1, 64, 16, None, None, None) == 1
+    # K6 reads the accumulator as float pairs: a 4-byte-aligned pointer is refused up front
+    assert lib.cgs_epilogue_grads(0x1004, 1, 10, 0x2000, 0, 1.0, 0x3000, None) == 1
+    assert lib.cgs_epilogue_adam(0x1004, 1, 10, 0x2000, 0x3000, 0x4000, 0, 1.0, 1e-3, 0.9, 0.999, 1e-8,
+                                 0.1, 0.001, None, None) == 1
 
 
 def test_product_path_fails_loudly_without_gpu():
