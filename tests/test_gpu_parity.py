@@ -513,6 +513,26 @@ def test_full_step_other_sizes(oracle, D, ctf):
     grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
 
 
+@pytest.mark.parametrize("n,B,D,ctf", [(1, 1, 16, True), (7, 3, 17, True), (300, 11, 32, True),
+                                        (257, 13, 64, True), (1000, 21, 128, True)])
+def test_full_step_edge_shapes(oracle, n, B, D, ctf):
+    """Edge shapes against the oracle: a single Gaussian and image, tiny odd grids, one Gaussian
+    past a full backward CTA (257), batches that leave a short last image group (11, 13, 21)
+    and odd batches through the paired K4 kernel (D = 32)."""
+    grid = oracle.Grid(D, 0.5, 1.5)
+    params = oracle.init_random(n, 3, grid)
+    params[:, 3:6] += np.random.default_rng(n).normal(0.0, 0.4, (n, 3))
+    poses = [oracle.sample_pose(np.random.default_rng(900 + i)) for i in range(B)]
+    obs = np.random.default_rng(D + B).standard_normal((B, D, D)).astype(np.float32) * 1e-3
+    cp = [oracle.Ctf(11000.0 + 700 * i, 13000.0, 0.2 * i) for i in range(B)]
+    ctfs = np.stack([c.as_array() for c in cp]) if ctf else None
+    Hs = [oracle.ctf_evaluate(c, grid) for c in cp] if ctf else None
+    losses, grads, _ = _full_step_device(params, poses, grid, obs, ctfs)
+    ref_losses, ref_grads = oracle.batch_step(params, poses, grid, Hs, obs)
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
+
+
 def test_readme_pipeline_end_to_end():
     """The README's simulate -> train -> voxelize -> FSC pipeline at toy size: it runs,
     the loss falls, and the reconstruction correlates with the truth at low resolution."""
