@@ -198,22 +198,15 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
                 f2scale(E, G);
                 f2scale(G, f2pack(c, c));
             };
-            // two columns per trip, loads one trip ahead (they may read one
-            // float2 past the span: every staging buffer carries kRowPad floats
-            // of slack); an odd column count peels one column first
+            // two columns per trip, both loaded at the top of the trip (no value
+            // carried across trips: a software-pipelined load costs register
+            // moves in the loop); an odd column count peels one column first
             const float2 *qe = q + (n - 1);
-            float2 GP = q[0];
-            if (n & 1) {
-                const float2 V1 = q[1];
-                column(GP);
-                GP = V1;
-                ++q;
-            }
+            if (n & 1) column(*q++);
 #pragma unroll 1
             for (; q < qe; q += 2) {
-                const float2 V1 = q[1];
-                column(GP);
-                GP = q[2];
+                const float2 V0 = q[0], V1 = q[1];
+                column(V0);
                 column(V1);
             }
             const float nf = (float)n;
