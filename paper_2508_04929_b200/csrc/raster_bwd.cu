@@ -161,11 +161,14 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
     for (; y <= yb; y += 2, DY = f2add(DY, f2pack(2.f, 2.f)), XC = f2add(XC, f2pack(m2s, m2s)), prow += W) {
         const bool v0 = y >= ya, v1 = y + 1 <= yb;
         const float2 REM = f2fma(f2mul(DY, f2pack(nk, nk)), DY, f2pack(kCutoffSq, kCutoffSq));
-        const float2 H = f2mul(f2pack(sqrt_approx(fmaxf(REM.x, 0.f)), sqrt_approx(fmaxf(REM.y, 0.f))),
-                               f2pack(isp, isp));
+        float2 H = f2mul(f2pack(sqrt_approx(fmaxf(REM.x, 0.f)), sqrt_approx(fmaxf(REM.y, 0.f))),
+                         f2pack(isp, isp));
+        // a row outside [ya, yb] gets the empty span [~1e9, ~-1e9]: neutral in the union's min/max
+        H.x = v0 ? H.x : -1e9f;
+        H.y = v1 ? H.y : -1e9f;
         const float2 LO = f2add(XC, f2pack(-H.x, -H.y)), HI = f2add(XC, H);
-        const int xa0 = v0 ? max((int)ceilf(LO.x), xlo) : 0x7fffffff, xb0 = v0 ? min((int)floorf(HI.x), xhi) : -1;
-        const int xa1 = v1 ? max((int)ceilf(LO.y), xlo) : 0x7fffffff, xb1 = v1 ? min((int)floorf(HI.y), xhi) : -1;
+        const int xa0 = max((int)ceilf(LO.x), xlo), xb0 = min((int)floorf(HI.x), xhi);
+        const int xa1 = max((int)ceilf(LO.y), xlo), xb1 = min((int)floorf(HI.y), xhi);
         const int xa = min(xa0, xa1), xb = max(xb0, xb1);
         if (xa > xb) continue;
         const float2 KY = f2mul(f2mul(DY, f2pack(Ck, Ck)), DY);
@@ -238,16 +241,17 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
                     r.g = f2add(r.g, t.g);
                 }
             }
-            const float2 DYE = f2mul(DY, r.e), DYX = f2mul(DY, r.x);
             M.e += f2sum(r.e);
 #ifdef CGS_BWD_EXACT_SUB
             M.g += (m0 ? r.g.x : 0.f) + (m1 ? r.g.y : 0.f);
 #endif
             M.x += f2sum(r.x);
             M.xx += f2sum(r.xx);
-            M.y += f2sum(DYE);
-            M.xy += f2sum(DYX);
-            M.yy += fmaf(DY.x, DYE.x, DY.y * DYE.y);
+            // y moments as FMA chains (one rounding fewer per term than product-then-sum)
+            M.y = fmaf(DY.y, r.e.y, fmaf(DY.x, r.e.x, M.y));
+            M.xy = fmaf(DY.y, r.x.y, fmaf(DY.x, r.x.x, M.xy));
+            const float2 DY2 = f2mul(DY, DY);
+            M.yy = fmaf(DY2.y, r.e.y, fmaf(DY2.x, r.e.x, M.yy));
         };
         // The union walk seeds a lane's recurrence up to |xa0 - xa1| columns
         // before its own span.  For thin, slanted footprints that seed e can
