@@ -152,7 +152,6 @@ constexpr float kMinSeedLog2 = -100.f;  // joint row-pair walks need every live 
 
 __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int b0, int W, int xlo, int xhi,
                                              int ya, int yb, const Splat2 &s, float c, Moments &M) {
-    const float2 ONE = f2pack(1.f, 1.f);
     const float nk = -s.k, A = s.A, Ck = s.Ck, isp = s.inv_sqrt_p00, m2s = -2.f * s.slope;
     int y = ya & ~1;  // b0 is even: pairs are aligned to even rows
     float2 DY = f2pack((float)y - s.mpy, (float)(y + 1) - s.mpy);
@@ -185,8 +184,9 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
             float2 e, x, xx, g;
         };
         auto run = [&](const float2 *q, int n, float2 DX, bool m0, bool m1) -> RunSums {
-            const float2 Q = f2fma(f2mul(DX, f2pack(A, A)), DX, KY);
-            const float2 GA = f2mul(f2fma(DX, f2pack(2.f, 2.f), ONE), f2pack(A, A));
+            const float2 DXA = f2mul(DX, f2pack(A, A));
+            const float2 Q = f2fma(DXA, DX, KY);
+            const float2 GA = f2fma(DXA, f2pack(2.f, 2.f), f2pack(A, A));  // A (2 dx + 1)
             // a dead lane carries e = g = 0 (a select: its g may be inf)
             float2 E = f2pack(m0 ? ex2_approx(Q.x) : 0.f, m1 ? ex2_approx(Q.y) : 0.f);
             float2 G = f2pack(m0 ? ex2_approx(GA.x) : 0.f, m1 ? ex2_approx(GA.y) : 0.f);
