@@ -257,6 +257,24 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return _
 __device__ __forceinline__ void f2acc_add(float2 &acc, float2 a) { acc = __fadd2_rn(acc, a); }
 __device__ __forceinline__ void f2acc_fma(float2 &acc, float2 a, float2 b) { acc = __ffma2_rn(a, b, acc); }
 __device__ __forceinline__ void f2scale(float2 &a, float2 b) { a = __fmul2_rn(a, b); }
+
+// Multiplies whose results are meant to be denormal (render.cu: integer
+// contributions as denormal bit patterns): explicit non-FTZ PTX, so a -ftz=true
+// or --use_fast_math build cannot flush them to zero.
+__device__ __forceinline__ float2 f2mul_keep_denorm(float2 a, float2 b) {
+    unsigned long long ua, ub, ud;
+    memcpy(&ua, &a, 8);
+    memcpy(&ub, &b, 8);
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(ud) : "l"(ua), "l"(ub));
+    float2 d;
+    memcpy(&d, &ud, 8);
+    return d;
+}
+__device__ __forceinline__ float fmul_keep_denorm(float a, float b) {
+    float d;
+    asm("mul.rn.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
 __device__ __forceinline__ float f2sum(float2 v) { return v.x + v.y; }
 
 // float -> nearest int32 on the FMA/ALU pipes (no F2I on the XU pipe):

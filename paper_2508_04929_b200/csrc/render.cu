@@ -134,14 +134,19 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
                                               const Splat2 &s, float scale, float cut) {
     constexpr float kM = 12582912.0f;
     constexpr float kHalfL2e = 0.5f * 1.4426950408889634f;
-    const float wS = s.w * scale, wsubS = s.w * kSub * scale;
+    const float wS = s.w * scale;
     const float c = ex2_approx(2.f * s.A);  // g_{k+1} / g_k
     const float c2 = c * c;
     const float2 C13 = f2pack(c, c2 * c), C4 = f2pack(c2 * c2, c2 * c2);
-    const float A2 = 2.f * s.A, nHcut = -kHalfL2e * cut, xhiM = kM + (float)xhi;
-    // v = wS e - wS sub + 1.5*2^23: the FFMA that evaluates the contribution
-    // also places its rounded integer in the low mantissa bits (fast_rint)
-    const float2 WS = f2pack(wS, wS), BIAS = f2pack(kM - wsubS, kM - wsubS);
+    // Contributions land directly as integers: e is carried scaled by 2^-74 and
+    // wS by 2^-75, so the product wS e 2^-149 is a denormal whose bit pattern is
+    // round(wS e) (round-to-nearest-even on the 2^-149 grid, the same rounding
+    // as fast_rint; explicit non-FTZ multiplies, common.cuh).  One multiply per pixel, no bias, no
+    // integer fix-up.  The -wS sub term (< 0.003 units per contribution for
+    // wS <= 2^22) is below the rounding of each contribution and is dropped.
+    const float A2 = 2.f * s.A, nHcut = -kHalfL2e * cut - 74.f, xhiM = kM + (float)xhi;
+    const float wSd = wS * 0x1p-75f;
+    const float2 WS = f2pack(wSd, wSd);
     float dy = (float)ya - s.mpy;
     float xcv = fmaf(-s.slope, dy, s.mpx);
     int *row = acc + (ya - r0) * ld;
@@ -164,17 +169,17 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
             int x = xa;
 #pragma unroll 1
             for (; x < xb; x += 2) {
-                const float2 v = f2fma(WS, E, BIAS);
-                atomicAdd(row + x, __float_as_int(v.x) - 0x4B400000);
-                atomicAdd(row + x + 1, __float_as_int(v.y) - 0x4B400000);
+                const float2 v = f2mul_keep_denorm(WS, E);
+                atomicAdd(row + x, __float_as_int(v.x));
+                atomicAdd(row + x + 1, __float_as_int(v.y));
                 f2scale(E, R);
                 f2scale(R, C4);
             }
-            if (x == xb) atomicAdd(row + x, fast_rint(fmaf(wS, E.x, -wsubS)));
+            if (x == xb) atomicAdd(row + x, __float_as_int(fmul_keep_denorm(wSd, E.x)));
         } else {
             float d = dx;
             for (int x = xa; x <= xb; ++x, d += 1.f)
-                atomicAdd(row + x, fast_rint(fmaf(wS, ex2_approx(fmaf(s.A * d, d, Ckdy2)), -wsubS)));
+                atomicAdd(row + x, __float_as_int(fmul_keep_denorm(wSd, ex2_approx(fmaf(s.A * d, d, Ckdy2)))));
         }
     }
 }
@@ -207,11 +212,12 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
         g += stepA;
         if (g >= n) g -= n;
         if (!(s.w > 0.f)) continue;
-        // Contribution-exact footprint: a pixel adds round(wS (e - sub)) units,
-        // which is 0 wherever e < sub + 0.5 / wS.  Walk only q < cut with
-        // e(cut) = sub + 0.4995 / wS (the 1e-3 margin keeps every pixel that
-        // can round to >= 1 unit): the same integer image, far fewer updates.
-        const float thr = fmaf(0.4995f, rcp_approx(s.w * scale), kSub);  // thr >= sub: no denormals
+        // Contribution-exact footprint: a pixel adds round(wS e) units, which is
+        // 0 wherever e < 0.5 / wS.  Walk only q < cut with e(cut) = 0.4995 / wS
+        // (the 1e-3 margin keeps every pixel that can round to >= 1 unit) and
+        // q < 6.5^2: the same integer image as the whole culled ellipse, far
+        // fewer updates.
+        const float thr = fmaxf(0.4995f * rcp_approx(s.w * scale), kSub);  // >= sub: no denormals
         if (!(thr < 1.f)) continue;
         const float cut = fminf(kCutoffSq, -2.f * kLn2 * lg2_approx(thr));
         const float hy = s.hy * sqrt_approx(cut * (1.f / kCutoffSq));
