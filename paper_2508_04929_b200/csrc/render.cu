@@ -151,9 +151,10 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
     float xcv = fmaf(-s.slope, dy, s.mpx);
     int *row = acc + (ya - r0) * ld;
     for (int nr = yb - ya; nr >= 0; --nr, dy += 1.f, xcv -= s.slope, row += ld) {
+        // rem <= 0 (a row at the cut's tip) leaves an empty span or one pixel
+        // at q >= cut, whose contribution rounds to 0: no branch for it
         const float rem = fmaf(-s.k * dy, dy, cut);
-        if (rem <= 0.f) continue;
-        const float sq = sqrt_approx(rem);
+        const float sq = sqrt_approx(fmaxf(rem, 0.f));
         const float fa = fmaxf(__fadd_ru(fmaf(-sq, s.inv_sqrt_p00, xcv), kM), kM);
         const float fb = fminf(__fadd_rd(fmaf(sq, s.inv_sqrt_p00, xcv), kM), xhiM);
         if (fa > fb) continue;
