@@ -790,6 +790,142 @@ __global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_r2c_kernel(
     }
 }
 
+// K4 in the Fourier domain (the training step's default when the observation
+// spectra are available, D = 64 / 128).  With O = F(obs) computed once per
+// observation (obs_spectrum_kernel, same half-spectrum layout as r2c_2d), the
+// residual's spectrum is F(r) = H_sym F(render) - O, so
+//   loss = mean r^2 = sum_k w_k |F(r)_k|^2 / D^4      (Parseval; w = 1 on the
+//          kx = 0 and kx = D/2 columns of the half spectrum, 2 elsewhere)
+//   upstream = 2/D^2 CTF^T(r) = c2r(H_sym / D^2 * 2/D^2 * F(r))
+// One forward and one inverse 2-D transform per image instead of two of each,
+// and the model image is never formed.
+template <int R>
+__global__ void __launch_bounds__(kR2cThreads, 2) obs_spectrum_kernel(const float *__restrict__ obs,
+                                                                       float2 *__restrict__ spec) {
+    constexpr int D = 32 * R, P = D / 2 + 1;
+    extern __shared__ float2 X[];
+    float *Xf = reinterpret_cast<float *>(X);
+    const int b = blockIdx.x;
+    WarpFft<R> F;
+    F.init(threadIdx.x & 31);
+    const float4 *o4 = reinterpret_cast<const float4 *>(obs + (int64_t)b * D * D);
+    for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
+        const int y = (4 * i) / D, x = 4 * i - y * D;
+        const float4 v = __ldg(o4 + i);
+        float *row = Xf + y * 2 * P + x;
+        row[0] = v.x; row[1] = v.y; row[2] = v.z; row[3] = v.w;
+    }
+    __syncthreads();
+    r2c_2d<R>(X, F);
+    __syncthreads();
+    float2 *dst = spec + (int64_t)b * D * P;
+    for (int i = threadIdx.x; i < D * P; i += kR2cThreads) dst[i] = X[i];
+}
+
+template <int R>
+__global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_spec_kernel(
+    const float *__restrict__ render, const float2 *__restrict__ obs_spec, const double *__restrict__ ctf,
+    double pix, float *__restrict__ upstream, double *__restrict__ loss, int32_t *status) {
+    constexpr int D = 32 * R, P = D / 2 + 1;
+    extern __shared__ float2 X[];
+    float *hb = reinterpret_cast<float *>(X + D * P);  // H_sym / D^2 over the half spectrum
+    __shared__ double scratch[kR2cThreads / 32];
+    __shared__ CtfConst cc;
+    float *Xf = reinterpret_cast<float *>(X);
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        CtfConst c = load_ctf(ctf + 8 * (int64_t)b, D, pix);
+        c.inv_dA = 1.0 / c.dA;
+        c.pl = kPiD * c.lam;
+        c.cs3 = 0.5 * kPiD * c.cs * c.lam * c.lam * c.lam;
+        cc = c;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < D * P; i += kR2cThreads) {
+        const int ky = i / P, kx = i - ky * P;
+        hb[i] = ctf_sym(cc, D, ky, kx) * (1.f / ((float)D * (float)D));
+    }
+    WarpFft<R> F;
+    F.init(threadIdx.x & 31);
+    const float2 *O = obs_spec + (int64_t)b * D * P;
+    {  // warm L2 with the observation spectrum, read after the forward transform
+        const char *ob = reinterpret_cast<const char *>(O);
+        for (int off = threadIdx.x * 128; off < D * P * (int)sizeof(float2); off += kR2cThreads * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
+    }
+    const float4 *r4 = reinterpret_cast<const float4 *>(render + (int64_t)b * D * D);
+    for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
+        const int y = (4 * i) / D, x = 4 * i - y * D;
+        const float4 v = __ldg(r4 + i);
+        float *row = Xf + y * 2 * P + x;
+        row[0] = v.x; row[1] = v.y; row[2] = v.z; row[3] = v.w;
+    }
+    __syncthreads();
+    r2c_2d<R>(X, F);
+    __syncthreads();
+    // F(r) = H F(render) - O (H = hb D^2, exact: D^2 is a power of two); loss; then
+    // the CTF^T filter and the 2/D^2 residual scale in place
+    const float d2 = (float)(D * D), sc = 2.f / (float)(D * D);
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < D * P; i += kR2cThreads) {
+        const int py = i / P, kx = i - py * P;
+        const float h = hb[perm_k<R>(py) * P + kx];
+        const float2 z = X[i], o = __ldg(O + i);
+        const float hd = h * d2;
+        const float rx = fmaf(hd, z.x, -o.x), ry = fmaf(hd, z.y, -o.y);
+        const double m2 = (double)rx * rx + (double)ry * ry;
+        acc += (kx == 0 || kx == D / 2) ? m2 : 2.0 * m2;
+        const float hs = h * sc;
+        X[i] = make_float2(hs * rx, hs * ry);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kR2cThreads / 32; ++w) t += scratch[w];
+        const double l = t / ((double)D * D * (double)D * D);
+        loss[b] = l;
+        if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
+    }
+    c2r_2d<R>(X, F);
+    float4 *u4 = reinterpret_cast<float4 *>(upstream + (int64_t)b * D * D);
+    for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
+        const int y = (4 * i) / D, x = 4 * i - y * D;
+        const float *row = Xf + y * 2 * P + x;
+        u4[i] = make_float4(row[0], row[1], row[2], row[3]);
+    }
+}
+
+template <int R>
+static int launch_obs_spectrum(const float *obs, float *spec, int B, cudaStream_t st) {
+    constexpr int D = 32 * R, P = D / 2 + 1;
+    const size_t smem = (size_t)D * P * sizeof(float2);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(obs_spectrum_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    obs_spectrum_kernel<R><<<B, kR2cThreads, smem, st>>>(obs, reinterpret_cast<float2 *>(spec));
+    return check_launch("obs_spectrum_kernel");
+}
+
+template <int R>
+static int launch_ctf_mse_spec(const float *render, const float *spec, int B, double pix, const double *ctf,
+                               float *upstream, double *loss, int32_t *status, cudaStream_t st) {
+    constexpr int D = 32 * R, P = D / 2 + 1;
+    const size_t smem = (size_t)D * P * (sizeof(float2) + sizeof(float));
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(ctf_mse_spec_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    ctf_mse_spec_kernel<R><<<B, kR2cThreads, smem, st>>>(render, reinterpret_cast<const float2 *>(spec), ctf, pix,
+                                                         upstream, loss, status);
+    return check_launch("ctf_mse_spec_kernel");
+}
+
 template <int R>
 static int launch_ctf_mse_r2c(const float *render, const float *obs, int B, double pix, const double *ctf,
                               float *model, float *upstream, double *loss, int32_t *status, cudaStream_t st) {
@@ -942,6 +1078,34 @@ extern "C" int cgs_ctf_mse(void *plan, const float *render, const float *obs, in
     if (rc) return rc;
     if (ctf) return cgs_ctf_apply(plan, upstream, upstream, B, grid, ctf, nullptr, spectrum, layout, stream);
     return CGS_OK;
+}
+
+extern "C" int64_t cgs_obs_spectrum_elems(int32_t size, int32_t B) {
+    if (size != 64 && size != 128) return 0;
+    return (int64_t)B * size * (size / 2 + 1);  // complex (float2) elements
+}
+
+extern "C" int cgs_obs_spectrum(const float *obs, int32_t B, cgs_grid grid, float *spec, void *stream) {
+    if (!obs || !spec || B <= 0) return CGS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (grid.size == 128) return launch_obs_spectrum<4>(obs, spec, B, st);
+    if (grid.size == 64) return launch_obs_spectrum<2>(obs, spec, B, st);
+    set_error_detail("cgs_obs_spectrum", "image size must be 64 or 128");
+    return CGS_ERR_UNSUPPORTED;
+}
+
+extern "C" int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, int32_t B, cgs_grid grid,
+                                    const double *ctf, float *upstream, double *loss, int32_t *status,
+                                    void *stream) {
+    if (!render || !obs_spec || !ctf || !upstream || !loss || B <= 0 || render == upstream || !(grid.pixel_size > 0))
+        return CGS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (grid.size == 128)
+        return launch_ctf_mse_spec<4>(render, obs_spec, B, grid.pixel_size, ctf, upstream, loss, status, st);
+    if (grid.size == 64)
+        return launch_ctf_mse_spec<2>(render, obs_spec, B, grid.pixel_size, ctf, upstream, loss, status, st);
+    set_error_detail("cgs_ctf_mse_spectral", "image size must be 64 or 128");
+    return CGS_ERR_UNSUPPORTED;
 }
 
 extern "C" int cgs_fourier_filter(const float *in, float *out, int32_t B, cgs_grid grid, const double *ctf,

@@ -227,6 +227,20 @@ def loss_residual(ctx, model, obs, resid=None):
     return loss
 
 
+def obs_spectra(ctx, obs, grid_s, chunk: int = 4096):
+    """F(obs) of a device stack f32 [R][D][D] for the spectral K4: complex64 half spectra as
+    f32 [R][D*(D/2+1)*2] (cgs_obs_spectrum), or None when the size has no spectral path."""
+    R, D = obs.shape[0], grid_s.size
+    per = int(ctx.lib.cgs_obs_spectrum_elems(D, 1))
+    if per == 0 or os.environ.get("CGS_CTF_SPATIAL", "0") == "1":
+        return None
+    out = torch.empty((R, 2 * per), dtype=torch.float32, device=ctx.device)
+    for a in range(0, R, chunk):
+        b = min(R, a + chunk)
+        _lib.call("cgs_obs_spectrum", _ptr(obs[a:b]), b - a, grid_s, _ptr(out[a:b]), ctx.stream)
+    return out
+
+
 def count_pairs(ctx, splat, n, poses, grid_s) -> "torch.Tensor":
     pairs = torch.zeros(poses.shape[0], dtype=torch.int64, device=ctx.device)
     _lib.call("cgs_count_pairs", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, _ptr(pairs), ctx.stream)
@@ -268,6 +282,10 @@ class StepPipeline:
         self.acc = torch.zeros(n * 10 + 1, dtype=torch.float32, device=dev)
         self.plan = ctx.plan(D, self.B)
         self.render_ws = torch.empty(ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, dtype=torch.float32, device=dev)
+        spec_elems = int(ctx.lib.cgs_obs_spectrum_elems(D, self.B))
+        self.obs_spec = None  # per-step F(obs) scratch of the spectral K4 (None: real-space K4)
+        if spec_elems and os.environ.get("CGS_CTF_SPATIAL", "0") != "1":
+            self.obs_spec = torch.empty(2 * spec_elems, dtype=torch.float32, device=dev)
         self.T = int(ctx.lib.cgs_bin_tiles(D, tile))
         self.S = int(ctx.lib.cgs_bin_segments(n))
         if render == "tiles":
@@ -313,13 +331,23 @@ class StepPipeline:
     # prepare, wbound_partial, wbound_scale, raster_fwd_atomic, fixed_to_float, K4, raster_bwd,
     # epilogue_adam.  K4 is one ctf_mse_fused kernel for D = 32 / 64 / 128; otherwise ctf_multiply x2 +
     # loss_resid around cuFFT's own R2C/C2R kernels (library launches, not counted).
-    def own_launches_per_step(self, ctf: bool = True) -> int:
+    def own_launches_per_step(self, ctf: bool = True, obs_spectrum: bool = False) -> int:
+        """Kernels of this library per step; obs_spectrum: the spectral K4 is fed precomputed
+        observation spectra (otherwise the spectral path adds one obs_spectrum launch)."""
         if not ctf:
             return 8
+        if self.spectral:
+            return 8 if obs_spectrum else 9
         fused = self.D in (32, 64, 128) and os.environ.get("CGS_CTF_CUFFT", "0") != "1"
         return 8 if fused else 10
 
-    def forward_backward(self, params, poses, obs, ctf, events=None):
+    @property
+    def spectral(self) -> bool:
+        """K4 runs in the Fourier domain (cgs_ctf_mse_spectral) for D = 64 / 128 with a CTF;
+        CGS_CTF_SPATIAL=1 keeps the real-space kernel (A/B)."""
+        return self.obs_spec is not None
+
+    def forward_backward(self, params, poses, obs, ctf, events=None, obs_spec=None):
         """K0..K5 for a batch; leaves partial accumulators in self.partial.
 
         ``events`` (optional dict of name -> (start, end) torch.cuda.Event
@@ -346,9 +374,16 @@ class StepPipeline:
                       _lib.CGS_LAYOUT_NATURAL, s)
         mark("fwd", 1)
         mark("ctf", 0)
-        _lib.call("cgs_ctf_mse", self.plan, _ptr(self.render), _ptr(obs), self.B, self.grid, _ptr(ctf),
-                  _ptr(self.spectrum), 0, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status),
-                  _lib.CGS_LAYOUT_NATURAL, s)
+        if ctf is not None and self.spectral:
+            if obs_spec is None:  # F(obs) of this batch (a dataset passes its precomputed spectra)
+                _lib.call("cgs_obs_spectrum", _ptr(obs), self.B, self.grid, _ptr(self.obs_spec), s)
+                obs_spec = self.obs_spec
+            _lib.call("cgs_ctf_mse_spectral", _ptr(self.render), _ptr(obs_spec), self.B, self.grid, _ptr(ctf),
+                      _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
+        else:
+            _lib.call("cgs_ctf_mse", self.plan, _ptr(self.render), _ptr(obs), self.B, self.grid, _ptr(ctf),
+                      _ptr(self.spectrum), 0, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status),
+                      _lib.CGS_LAYOUT_NATURAL, s)
         mark("ctf", 1)
         mark("bwd", 0)
         _lib.call("cgs_raster_bwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid,

@@ -216,6 +216,9 @@ class Reconstructor:
         self.obs = self.obs.to(dev, torch.float32).contiguous()
         self.poses = torch.as_tensor(np.ascontiguousarray(poses, np.float64)).to(dev)
         self.ctfs = None if ctfs is None else torch.as_tensor(np.ascontiguousarray(ctfs, np.float64)).to(dev)
+        # F(obs) of every observation, once: with it K4 runs in the Fourier domain with one
+        # forward and one inverse transform per image (cgs_ctf_mse_spectral); None: real space
+        self.obs_spec = None if self.ctfs is None else engine.obs_spectra(self.ctx, self.obs, self.gs)
         self.global_batch = int(batch_size)
         self.pg = process_group
         self.world = 1
@@ -253,6 +256,14 @@ class Reconstructor:
         ctfs = None if self.ctfs is None else self.ctfs.index_select(0, idx)
         return obs, poses, ctfs
 
+    def batch_spectra(self, local: np.ndarray):
+        """The precomputed observation spectra of a batch (device), or None."""
+        if self.obs_spec is None:
+            return None
+        torch = _torch()
+        idx = torch.as_tensor(local, dtype=torch.int64).to(self.ctx.device, non_blocking=True)
+        return self.obs_spec.index_select(0, idx)
+
     def ensure_capacity(self, indices_list) -> None:
         """Size the tile-list buffers from the given batches (one host read each)."""
         for local in indices_list:
@@ -271,7 +282,7 @@ class Reconstructor:
         if self.use_graphs and self.world == 1:
             return self._graph_step_indexed(local, lr, global_batch=len(indices))
         obs, poses, ctfs = self._batch(local)
-        return self.step_batch(obs, poses, ctfs, lr, global_batch=len(indices))
+        return self.step_batch(obs, poses, ctfs, lr, global_batch=len(indices), obs_spec=self.batch_spectra(local))
 
     def _graph_step_indexed(self, local: np.ndarray, lr: float, *, global_batch: int):
         torch = _torch()
@@ -281,9 +292,11 @@ class Reconstructor:
         sl = self._idx_slots.get(key)
         if sl is None:
             D = self.grid.size
+            spec = self.obs_spec is not None
             sl = self._idx_slots[key] = {
                 "idx": torch.empty(b, dtype=torch.int64, device=dev),
-                "o": torch.empty((b, D, D), dtype=torch.float32, device=dev),
+                "o": None if spec else torch.empty((b, D, D), dtype=torch.float32, device=dev),
+                "s": torch.empty((b, self.obs_spec.shape[1]), dtype=torch.float32, device=dev) if spec else None,
                 "p": torch.empty((b, 12), dtype=torch.float64, device=dev),
                 "c": None if self.ctfs is None else torch.empty((b, 8), dtype=torch.float64, device=dev),
                 "hyper": torch.empty(3, dtype=torch.float64, device=dev), "graph": None}
@@ -295,12 +308,15 @@ class Reconstructor:
         scale = 1.0 / global_batch
 
         def body():
-            torch.index_select(self.obs, 0, sl["idx"], out=sl["o"])
+            if sl["s"] is not None:
+                torch.index_select(self.obs_spec, 0, sl["idx"], out=sl["s"])
+            else:
+                torch.index_select(self.obs, 0, sl["idx"], out=sl["o"])
             torch.index_select(self.poses, 0, sl["idx"], out=sl["p"])
             if sl["c"] is not None:
                 torch.index_select(self.ctfs, 0, sl["idx"], out=sl["c"])
             pipe.clear_status()
-            pipe.forward_backward(self.params, sl["p"], sl["o"], sl["c"])
+            pipe.forward_backward(self.params, sl["p"], sl["o"], sl["c"], obs_spec=sl["s"])
             pipe.adam_dev(self.params, self.m, self.v, sl["hyper"], scale=scale, beta1=cfg.adam_beta1,
                           beta2=cfg.adam_beta2, eps=cfg.adam_epsilon)
 
@@ -396,14 +412,16 @@ class Reconstructor:
         self.t += 1
         return pipe.loss
 
-    def step_batch(self, obs, poses, ctfs, lr: float, *, global_batch: int, events=None):
+    def step_batch(self, obs, poses, ctfs, lr: float, *, global_batch: int, events=None, obs_spec=None):
         """One step on device tensors of this rank's batch (obs f32 [b][D][D],
         poses f64 [b][12], ctfs f64 [b][8] or None); ``global_batch`` sets the
-        1/B loss scale.  Returns the device tensor of per-image losses."""
-        pipe = self.pipeline(obs.shape[0])
+        1/B loss scale.  ``obs_spec``: the batch's precomputed observation spectra
+        (batch_spectra); obs may then be None.  Returns the device tensor of
+        per-image losses."""
+        pipe = self.pipeline(poses.shape[0])
         cfg = self.config
         pipe.clear_status()
-        pipe.forward_backward(self.params, poses, obs, ctfs, events=events)
+        pipe.forward_backward(self.params, poses, obs, ctfs, events=events, obs_spec=obs_spec)
         scale = 1.0 / global_batch
         self.t += 1
         if self.world > 1:

@@ -317,6 +317,52 @@ def test_fused_ctf_mse_matches_oracle(oracle, D):
     assert status.item() == 0
 
 
+@pytest.mark.parametrize("D", [64, 128])
+def test_spectral_ctf_mse_matches_oracle(oracle, D):
+    """K4 in the Fourier domain (cgs_obs_spectrum + cgs_ctf_mse_spectral): F(r) = H_sym F(render)
+    - F(obs), the loss by Parseval over the half spectrum and the CTF^T upstream, against the
+    reference's centred complex FFTs (astigmatism, phase shift, B-factor, an odd batch) and
+    against the real-space kernel."""
+    B = 3
+    grid = oracle.Grid(D, 0.5, 1.5)
+    rng = np.random.default_rng(50 + D)
+    render = rng.standard_normal((B, D, D)).astype(np.float32)
+    obs = rng.standard_normal((B, D, D)).astype(np.float32)
+    ctfs = [oracle.Ctf(12000.0, 15000.0, 0.7), oracle.Ctf(20000.0, 18000.0, -0.3, phase_shift=0.4),
+            oracle.Ctf(9000.0, 9500.0, 1.2, b_factor=40.0)]
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(D, grid.extent, grid.pixel_size)
+    r, o = _dev(render, torch.float32), _dev(obs, torch.float32)
+    c = _dev(np.stack([x.as_array() for x in ctfs]), torch.float64)
+    spec = torch.empty(2 * int(ctx.lib.cgs_obs_spectrum_elems(D, B)), dtype=torch.float32, device=r.device)
+    up = torch.empty_like(r)
+    loss = torch.empty(B, dtype=torch.float64, device=r.device)
+    status = torch.zeros(1, dtype=torch.int32, device=r.device)
+    _lib.call("cgs_obs_spectrum", o.data_ptr(), B, gs, spec.data_ptr(), ctx.stream)
+    _lib.call("cgs_ctf_mse_spectral", r.data_ptr(), spec.data_ptr(), B, gs, c.data_ptr(), up.data_ptr(),
+              loss.data_ptr(), status.data_ptr(), ctx.stream)
+    up2 = torch.empty_like(r)
+    loss2 = torch.empty_like(loss)
+    wspec = torch.empty(2 * int(ctx.lib.cgs_fft_spectrum_elems(D, B)), dtype=torch.float32, device=r.device)
+    _lib.call("cgs_ctf_mse", ctx.plan(D, B), r.data_ptr(), o.data_ptr(), B, gs, c.data_ptr(), wspec.data_ptr(),
+              0, up2.data_ptr(), loss2.data_ptr(), status.data_ptr(), _lib.CGS_LAYOUT_NATURAL, ctx.stream)
+    torch.cuda.synchronize()
+    for b in range(B):
+        H = oracle.ctf_evaluate(ctfs[b], grid)
+        m_ref = oracle.apply_ctf(render[b].astype(np.float64), H)
+        u_ref = oracle.apply_ctf((2.0 / (D * D)) * (m_ref - obs[b]), H)
+        l_ref = oracle.loss_mse(m_ref, obs[b])
+        assert rel_l2(up[b].cpu().numpy(), u_ref) < 1e-5
+        assert abs(loss[b].item() - l_ref) <= 1e-5 * l_ref
+        assert rel_l2(up[b].cpu().numpy(), up2[b].cpu().numpy()) < 1e-5
+    np.testing.assert_allclose(loss.cpu().numpy(), loss2.cpu().numpy(), rtol=1e-5)
+    assert status.item() == 0
+    # the ABI refuses sizes without a spectral kernel and a missing CTF
+    assert ctx.lib.cgs_obs_spectrum_elems(96, 1) == 0
+    assert ctx.lib.cgs_ctf_mse_spectral(r.data_ptr(), spec.data_ptr(), B, gs, None, up.data_ptr(),
+                                        loss.data_ptr(), None, None) == 1
+
+
 def _full_step_device(params, poses, grid, obs, ctfs, render="direct"):
     """Run the engine's fused K0..K5 + epilogue grads for a batch; return (losses, grads)."""
     ctx = engine.DeviceContext.get()
