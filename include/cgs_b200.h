@@ -171,18 +171,19 @@ int cgs_ctf_mse(void *plan, const float *render, const float *obs, int32_t B, cg
                 const double *ctf, void *spectrum, float *model, float *upstream, double *loss,
                 int32_t *status, int32_t layout, void *stream);
 
-/* K4 in the Fourier domain.  cgs_obs_spectrum writes each observation's half
- * spectrum F(obs) (complex64, cgs_obs_spectrum_elems(D, B) elements, an
- * internal row order shared with the kernels; D = 64 or 128, else
- * CGS_ERR_UNSUPPORTED).  It depends only on the data, so a dataset computes it
- * once.  cgs_ctf_mse_spectral then gives the same loss and upstream as
- * cgs_ctf_mse (ctf required, no model image) from F(r) = H_sym F(render) - O:
+/* K4 in the Fourier domain.  cgs_obs_spectrum writes one record per
+ * observation: its half spectrum F(obs) (complex64) followed by H_sym / D^2 of
+ * its CTF (ctf f64 [B][8]), in an internal row order shared with the kernels;
+ * cgs_obs_spectrum_elems(D, B) floats in all (D = 64 or 128, else 0 and
+ * CGS_ERR_UNSUPPORTED).  A record depends only on the data, so a dataset
+ * computes it once.  cgs_ctf_mse_spectral then gives the loss and upstream of
+ * cgs_ctf_mse (no model image) from F(r) = H_sym F(render) - F(obs):
  * loss = sum |F(r)|^2 / D^4 by Parseval, upstream = 2/D^2 CTF^T(r), with one
  * forward and one inverse transform per image. */
 int64_t cgs_obs_spectrum_elems(int32_t size, int32_t B);
-int cgs_obs_spectrum(const float *obs, int32_t B, cgs_grid grid, float *spec, void *stream);
-int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, int32_t B, cgs_grid grid, const double *ctf,
-                         float *upstream, double *loss, int32_t *status, void *stream);
+int cgs_obs_spectrum(const float *obs, const double *ctf, int32_t B, cgs_grid grid, float *spec, void *stream);
+int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, int32_t B, cgs_grid grid, float *upstream,
+                         double *loss, int32_t *status, void *stream);
 
 /* Batched Fourier filter out = Re ifft2(F fft2(in)), per image F = H_sym (CTF,
  * ctf f64 [B][8], may be NULL) x the sub-pixel shift ramp

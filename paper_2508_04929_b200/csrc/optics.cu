@@ -799,13 +799,25 @@ __global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_r2c_kernel(
 //   upstream = 2/D^2 CTF^T(r) = c2r(H_sym / D^2 * 2/D^2 * F(r))
 // One forward and one inverse 2-D transform per image instead of two of each,
 // and the model image is never formed.
+// Per observation record (obs_spectrum_kernel): the half spectrum O = F(obs),
+// D x P complex in r2c_2d's layout, then H_sym / D^2 as D x P floats in the
+// same (permuted-row) layout, so the step reads both with coalesced loads.
 template <int R>
 __global__ void __launch_bounds__(kR2cThreads, 2) obs_spectrum_kernel(const float *__restrict__ obs,
+                                                                       const double *__restrict__ ctf, double pix,
                                                                        float2 *__restrict__ spec) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     extern __shared__ float2 X[];
+    __shared__ CtfConst cc;
     float *Xf = reinterpret_cast<float *>(X);
     const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        CtfConst c = load_ctf(ctf + 8 * (int64_t)b, D, pix);
+        c.inv_dA = 1.0 / c.dA;
+        c.pl = kPiD * c.lam;
+        c.cs3 = 0.5 * kPiD * c.cs * c.lam * c.lam * c.lam;
+        cc = c;
+    }
     WarpFft<R> F;
     F.init(threadIdx.x & 31);
     const float4 *o4 = reinterpret_cast<const float4 *>(obs + (int64_t)b * D * D);
@@ -818,39 +830,31 @@ __global__ void __launch_bounds__(kR2cThreads, 2) obs_spectrum_kernel(const floa
     __syncthreads();
     r2c_2d<R>(X, F);
     __syncthreads();
-    float2 *dst = spec + (int64_t)b * D * P;
+    float2 *dst = spec + (int64_t)b * (3 * D * P / 2);
     for (int i = threadIdx.x; i < D * P; i += kR2cThreads) dst[i] = X[i];
+    float *hd = reinterpret_cast<float *>(dst + D * P);
+    for (int i = threadIdx.x; i < D * P; i += kR2cThreads) {
+        const int py = i / P, kx = i - py * P;
+        hd[i] = ctf_sym(cc, D, perm_k<R>(py), kx) * (1.f / ((float)D * (float)D));
+    }
 }
 
 template <int R>
 __global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_spec_kernel(
-    const float *__restrict__ render, const float2 *__restrict__ obs_spec, const double *__restrict__ ctf,
-    double pix, float *__restrict__ upstream, double *__restrict__ loss, int32_t *status) {
+    const float *__restrict__ render, const float2 *__restrict__ obs_spec, float *__restrict__ upstream,
+    double *__restrict__ loss, int32_t *status) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     extern __shared__ float2 X[];
-    float *hb = reinterpret_cast<float *>(X + D * P);  // H_sym / D^2 over the half spectrum
     __shared__ double scratch[kR2cThreads / 32];
-    __shared__ CtfConst cc;
     float *Xf = reinterpret_cast<float *>(X);
     const int b = blockIdx.x;
-    if (threadIdx.x == 0) {
-        CtfConst c = load_ctf(ctf + 8 * (int64_t)b, D, pix);
-        c.inv_dA = 1.0 / c.dA;
-        c.pl = kPiD * c.lam;
-        c.cs3 = 0.5 * kPiD * c.cs * c.lam * c.lam * c.lam;
-        cc = c;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < D * P; i += kR2cThreads) {
-        const int ky = i / P, kx = i - ky * P;
-        hb[i] = ctf_sym(cc, D, ky, kx) * (1.f / ((float)D * (float)D));
-    }
     WarpFft<R> F;
     F.init(threadIdx.x & 31);
-    const float2 *O = obs_spec + (int64_t)b * D * P;
-    {  // warm L2 with the observation spectrum, read after the forward transform
+    const float2 *O = obs_spec + (int64_t)b * (3 * D * P / 2);
+    const float *Hh = reinterpret_cast<const float *>(O + D * P);  // H_sym / D^2, X's layout
+    {  // warm L2 with the observation record, read after the forward transform
         const char *ob = reinterpret_cast<const char *>(O);
-        for (int off = threadIdx.x * 128; off < D * P * (int)sizeof(float2); off += kR2cThreads * 128)
+        for (int off = threadIdx.x * 128; off < 3 * D * P * (int)sizeof(float); off += kR2cThreads * 128)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
     }
     const float4 *r4 = reinterpret_cast<const float4 *>(render + (int64_t)b * D * D);
@@ -863,13 +867,13 @@ __global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_spec_kernel(
     __syncthreads();
     r2c_2d<R>(X, F);
     __syncthreads();
-    // F(r) = H F(render) - O (H = hb D^2, exact: D^2 is a power of two); loss; then
+    // F(r) = H F(render) - O (H = Hh D^2, exact: D^2 is a power of two); loss; then
     // the CTF^T filter and the 2/D^2 residual scale in place
     const float d2 = (float)(D * D), sc = 2.f / (float)(D * D);
     double acc = 0.0;
     for (int i = threadIdx.x; i < D * P; i += kR2cThreads) {
-        const int py = i / P, kx = i - py * P;
-        const float h = hb[perm_k<R>(py) * P + kx];
+        const int kx = i % P;
+        const float h = __ldg(Hh + i);
         const float2 z = X[i], o = __ldg(O + i);
         const float hd = h * d2;
         const float rx = fmaf(hd, z.x, -o.x), ry = fmaf(hd, z.y, -o.y);
@@ -899,7 +903,8 @@ __global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_spec_kernel(
 }
 
 template <int R>
-static int launch_obs_spectrum(const float *obs, float *spec, int B, cudaStream_t st) {
+static int launch_obs_spectrum(const float *obs, const double *ctf, double pix, float *spec, int B,
+                               cudaStream_t st) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     const size_t smem = (size_t)D * P * sizeof(float2);
     static bool configured = false;
@@ -907,22 +912,22 @@ static int launch_obs_spectrum(const float *obs, float *spec, int B, cudaStream_
         cudaFuncSetAttribute(obs_spectrum_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    obs_spectrum_kernel<R><<<B, kR2cThreads, smem, st>>>(obs, reinterpret_cast<float2 *>(spec));
+    obs_spectrum_kernel<R><<<B, kR2cThreads, smem, st>>>(obs, ctf, pix, reinterpret_cast<float2 *>(spec));
     return check_launch("obs_spectrum_kernel");
 }
 
 template <int R>
-static int launch_ctf_mse_spec(const float *render, const float *spec, int B, double pix, const double *ctf,
-                               float *upstream, double *loss, int32_t *status, cudaStream_t st) {
+static int launch_ctf_mse_spec(const float *render, const float *spec, int B, float *upstream, double *loss,
+                               int32_t *status, cudaStream_t st) {
     constexpr int D = 32 * R, P = D / 2 + 1;
-    const size_t smem = (size_t)D * P * (sizeof(float2) + sizeof(float));
+    const size_t smem = (size_t)D * P * sizeof(float2);
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(ctf_mse_spec_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    ctf_mse_spec_kernel<R><<<B, kR2cThreads, smem, st>>>(render, reinterpret_cast<const float2 *>(spec), ctf, pix,
-                                                         upstream, loss, status);
+    ctf_mse_spec_kernel<R><<<B, kR2cThreads, smem, st>>>(render, reinterpret_cast<const float2 *>(spec), upstream,
+                                                         loss, status);
     return check_launch("ctf_mse_spec_kernel");
 }
 
@@ -1082,28 +1087,25 @@ extern "C" int cgs_ctf_mse(void *plan, const float *render, const float *obs, in
 
 extern "C" int64_t cgs_obs_spectrum_elems(int32_t size, int32_t B) {
     if (size != 64 && size != 128) return 0;
-    return (int64_t)B * size * (size / 2 + 1);  // complex (float2) elements
+    return (int64_t)B * 3 * size * (size / 2 + 1);  // floats: F(obs) complex + H_sym / D^2
 }
 
-extern "C" int cgs_obs_spectrum(const float *obs, int32_t B, cgs_grid grid, float *spec, void *stream) {
-    if (!obs || !spec || B <= 0) return CGS_ERR_ARG;
+extern "C" int cgs_obs_spectrum(const float *obs, const double *ctf, int32_t B, cgs_grid grid, float *spec,
+                                void *stream) {
+    if (!obs || !ctf || !spec || B <= 0 || !(grid.pixel_size > 0)) return CGS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (grid.size == 128) return launch_obs_spectrum<4>(obs, spec, B, st);
-    if (grid.size == 64) return launch_obs_spectrum<2>(obs, spec, B, st);
+    if (grid.size == 128) return launch_obs_spectrum<4>(obs, ctf, grid.pixel_size, spec, B, st);
+    if (grid.size == 64) return launch_obs_spectrum<2>(obs, ctf, grid.pixel_size, spec, B, st);
     set_error_detail("cgs_obs_spectrum", "image size must be 64 or 128");
     return CGS_ERR_UNSUPPORTED;
 }
 
 extern "C" int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, int32_t B, cgs_grid grid,
-                                    const double *ctf, float *upstream, double *loss, int32_t *status,
-                                    void *stream) {
-    if (!render || !obs_spec || !ctf || !upstream || !loss || B <= 0 || render == upstream || !(grid.pixel_size > 0))
-        return CGS_ERR_ARG;
+                                    float *upstream, double *loss, int32_t *status, void *stream) {
+    if (!render || !obs_spec || !upstream || !loss || B <= 0 || render == upstream) return CGS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (grid.size == 128)
-        return launch_ctf_mse_spec<4>(render, obs_spec, B, grid.pixel_size, ctf, upstream, loss, status, st);
-    if (grid.size == 64)
-        return launch_ctf_mse_spec<2>(render, obs_spec, B, grid.pixel_size, ctf, upstream, loss, status, st);
+    if (grid.size == 128) return launch_ctf_mse_spec<4>(render, obs_spec, B, upstream, loss, status, st);
+    if (grid.size == 64) return launch_ctf_mse_spec<2>(render, obs_spec, B, upstream, loss, status, st);
     set_error_detail("cgs_ctf_mse_spectral", "image size must be 64 or 128");
     return CGS_ERR_UNSUPPORTED;
 }

@@ -227,17 +227,18 @@ def loss_residual(ctx, model, obs, resid=None):
     return loss
 
 
-def obs_spectra(ctx, obs, grid_s, chunk: int = 4096):
-    """F(obs) of a device stack f32 [R][D][D] for the spectral K4: complex64 half spectra as
-    f32 [R][D*(D/2+1)*2] (cgs_obs_spectrum), or None when the size has no spectral path."""
+def obs_spectra(ctx, obs, ctfs, grid_s, chunk: int = 4096):
+    """Spectral-K4 records of a device stack (obs f32 [R][D][D], ctfs f64 [R][8]): F(obs) and
+    H_sym / D^2 per observation, f32 [R][3 D (D/2+1)] (cgs_obs_spectrum), or None when the size
+    has no spectral path."""
     R, D = obs.shape[0], grid_s.size
     per = int(ctx.lib.cgs_obs_spectrum_elems(D, 1))
     if per == 0 or os.environ.get("CGS_CTF_SPATIAL", "0") == "1":
         return None
-    out = torch.empty((R, 2 * per), dtype=torch.float32, device=ctx.device)
+    out = torch.empty((R, per), dtype=torch.float32, device=ctx.device)
     for a in range(0, R, chunk):
         b = min(R, a + chunk)
-        _lib.call("cgs_obs_spectrum", _ptr(obs[a:b]), b - a, grid_s, _ptr(out[a:b]), ctx.stream)
+        _lib.call("cgs_obs_spectrum", _ptr(obs[a:b]), _ptr(ctfs[a:b]), b - a, grid_s, _ptr(out[a:b]), ctx.stream)
     return out
 
 
@@ -283,9 +284,9 @@ class StepPipeline:
         self.plan = ctx.plan(D, self.B)
         self.render_ws = torch.empty(ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, dtype=torch.float32, device=dev)
         spec_elems = int(ctx.lib.cgs_obs_spectrum_elems(D, self.B))
-        self.obs_spec = None  # per-step F(obs) scratch of the spectral K4 (None: real-space K4)
+        self.obs_spec = None  # per-step observation records of the spectral K4 (None: real-space K4)
         if spec_elems and os.environ.get("CGS_CTF_SPATIAL", "0") != "1":
-            self.obs_spec = torch.empty(2 * spec_elems, dtype=torch.float32, device=dev)
+            self.obs_spec = torch.empty(spec_elems, dtype=torch.float32, device=dev)
         self.T = int(ctx.lib.cgs_bin_tiles(D, tile))
         self.S = int(ctx.lib.cgs_bin_segments(n))
         if render == "tiles":
@@ -375,10 +376,10 @@ class StepPipeline:
         mark("fwd", 1)
         mark("ctf", 0)
         if ctf is not None and self.spectral:
-            if obs_spec is None:  # F(obs) of this batch (a dataset passes its precomputed spectra)
-                _lib.call("cgs_obs_spectrum", _ptr(obs), self.B, self.grid, _ptr(self.obs_spec), s)
+            if obs_spec is None:  # this batch's records (a dataset passes its precomputed ones)
+                _lib.call("cgs_obs_spectrum", _ptr(obs), _ptr(ctf), self.B, self.grid, _ptr(self.obs_spec), s)
                 obs_spec = self.obs_spec
-            _lib.call("cgs_ctf_mse_spectral", _ptr(self.render), _ptr(obs_spec), self.B, self.grid, _ptr(ctf),
+            _lib.call("cgs_ctf_mse_spectral", _ptr(self.render), _ptr(obs_spec), self.B, self.grid,
                       _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
         else:
             _lib.call("cgs_ctf_mse", self.plan, _ptr(self.render), _ptr(obs), self.B, self.grid, _ptr(ctf),

@@ -216,9 +216,9 @@ class Reconstructor:
         self.obs = self.obs.to(dev, torch.float32).contiguous()
         self.poses = torch.as_tensor(np.ascontiguousarray(poses, np.float64)).to(dev)
         self.ctfs = None if ctfs is None else torch.as_tensor(np.ascontiguousarray(ctfs, np.float64)).to(dev)
-        # F(obs) of every observation, once: with it K4 runs in the Fourier domain with one
-        # forward and one inverse transform per image (cgs_ctf_mse_spectral); None: real space
-        self.obs_spec = None if self.ctfs is None else engine.obs_spectra(self.ctx, self.obs, self.gs)
+        # F(obs) and H_sym of every observation, once: with them K4 runs in the Fourier domain
+        # with one forward and one inverse transform per image (cgs_ctf_mse_spectral)
+        self.obs_spec = None if self.ctfs is None else engine.obs_spectra(self.ctx, self.obs, self.ctfs, self.gs)
         self.global_batch = int(batch_size)
         self.pg = process_group
         self.world = 1

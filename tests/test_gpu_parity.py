@@ -334,12 +334,12 @@ def test_spectral_ctf_mse_matches_oracle(oracle, D):
     gs = _lib.grid_struct(D, grid.extent, grid.pixel_size)
     r, o = _dev(render, torch.float32), _dev(obs, torch.float32)
     c = _dev(np.stack([x.as_array() for x in ctfs]), torch.float64)
-    spec = torch.empty(2 * int(ctx.lib.cgs_obs_spectrum_elems(D, B)), dtype=torch.float32, device=r.device)
+    spec = torch.empty(int(ctx.lib.cgs_obs_spectrum_elems(D, B)), dtype=torch.float32, device=r.device)
     up = torch.empty_like(r)
     loss = torch.empty(B, dtype=torch.float64, device=r.device)
     status = torch.zeros(1, dtype=torch.int32, device=r.device)
-    _lib.call("cgs_obs_spectrum", o.data_ptr(), B, gs, spec.data_ptr(), ctx.stream)
-    _lib.call("cgs_ctf_mse_spectral", r.data_ptr(), spec.data_ptr(), B, gs, c.data_ptr(), up.data_ptr(),
+    _lib.call("cgs_obs_spectrum", o.data_ptr(), c.data_ptr(), B, gs, spec.data_ptr(), ctx.stream)
+    _lib.call("cgs_ctf_mse_spectral", r.data_ptr(), spec.data_ptr(), B, gs, up.data_ptr(),
               loss.data_ptr(), status.data_ptr(), ctx.stream)
     up2 = torch.empty_like(r)
     loss2 = torch.empty_like(loss)
@@ -359,8 +359,7 @@ def test_spectral_ctf_mse_matches_oracle(oracle, D):
     assert status.item() == 0
     # the ABI refuses sizes without a spectral kernel and a missing CTF
     assert ctx.lib.cgs_obs_spectrum_elems(96, 1) == 0
-    assert ctx.lib.cgs_ctf_mse_spectral(r.data_ptr(), spec.data_ptr(), B, gs, None, up.data_ptr(),
-                                        loss.data_ptr(), None, None) == 1
+    assert ctx.lib.cgs_obs_spectrum(o.data_ptr(), None, B, gs, spec.data_ptr(), None) == 1
 
 
 def _full_step_device(params, poses, grid, obs, ctfs, render="direct"):
