@@ -609,6 +609,9 @@ static int launch_fourier_filter(const float *in, float *out, int B, double pix,
 #define CGS_R2C_THREADS 384
 #endif
 constexpr int kR2cThreads = CGS_R2C_THREADS;
+#ifndef CGS_SPEC_MINB
+#define CGS_SPEC_MINB 2
+#endif
 
 // forward real 2-D FFT of the real image held row-wise (floats, row stride 2P)
 // in X: afterwards X[py][kx] = spectrum at (perm_k(py), kx), kx <= D/2
@@ -840,7 +843,7 @@ __global__ void __launch_bounds__(kR2cThreads, 2) obs_spectrum_kernel(const floa
 }
 
 template <int R>
-__global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_spec_kernel(
+__global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kernel(
     const float *__restrict__ render, const float2 *__restrict__ obs_spec, float *__restrict__ upstream,
     double *__restrict__ loss, int32_t *status) {
     constexpr int D = 32 * R, P = D / 2 + 1;
