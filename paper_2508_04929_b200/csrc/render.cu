@@ -197,6 +197,10 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     const float *__restrict__ scale_ptr, int HB, int64_t mulA, int chunk, int *__restrict__ out) {
     extern __shared__ int band[];
     const int D = G.D;
+    // the row stride as an opaque register value, so it is not re-read from the
+    // constant bank per row (that reload's destination register would wait on
+    // the row's last shared atomic reading it)
+    const int ld = D + (int)(clock64() >> 62);  // = D (the counter never reaches 2^62), opaque to the compiler
     const int b = blockIdx.y;
     const int r0 = blockIdx.z * HB, r1 = min(D, r0 + HB);
     const int npx = (r1 - r0) * D;
@@ -227,9 +231,9 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
         if (ylo > yhi) continue;
         // widest row = 2 sqrt(cut / p00) = 2 * 6.5 sqrt(cut / 6.5^2) / sqrt(p00)
         if (13.f * sqrt_approx(cut * (1.f / kCutoffSq)) * s.inv_sqrt_p00 < 31.f)
-            fwd_rows_band<true>(band, r0, D, D - 1, ylo, yhi, s, scale, cut);
+            fwd_rows_band<true>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
         else
-            fwd_rows_band<false>(band, r0, D, D - 1, ylo, yhi, s, scale, cut);
+            fwd_rows_band<false>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
     }
     __syncthreads();
     int *dst = out + (int64_t)b * D * D + (int64_t)r0 * D;
