@@ -137,6 +137,13 @@ int cgs_raster_fwd(const float *splat, int64_t n, const double *poses, int32_t B
 size_t cgs_render_workspace_bytes(int64_t n);
 int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
                void *ws, void *stream);
+/* cgs_render without the final conversion: out holds the int32 fixed-point
+ * image; its scale (pixel value = int / scale) is the float at
+ * ws + cgs_render_scale_offset(n) floats, for a consumer that converts on load
+ * (cgs_ctf_mse_spectral). */
+int cgs_render_fixed(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, int32_t *out,
+                     void *ws, void *stream);
+int64_t cgs_render_scale_offset(int64_t n);
 
 /* ---- K4: CTF, centred FFTs and MSE (optics.py:78-141, train.py:114-121,153)
  * ctf_evaluate (optics.py:93-121): H f64 [B][D][D], centred layout. */
@@ -184,6 +191,11 @@ int64_t cgs_obs_spectrum_elems(int32_t size, int32_t B);
 int cgs_obs_spectrum(const float *obs, const double *ctf, int32_t B, cgs_grid grid, float *spec, void *stream);
 int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, int32_t B, cgs_grid grid, float *upstream,
                          double *loss, int32_t *status, void *stream);
+/* The same from a cgs_render_fixed image: render_fixed int32 [B][D][D] and its
+ * scale pointer (ws + cgs_render_scale_offset(n)). */
+int cgs_ctf_mse_spectral_fixed(const int32_t *render_fixed, const float *render_scale, const float *obs_spec,
+                               int32_t B, cgs_grid grid, float *upstream, double *loss, int32_t *status,
+                               void *stream);
 
 /* Batched Fourier filter out = Re ifft2(F fft2(in)), per image F = H_sym (CTF,
  * ctf f64 [B][8], may be NULL) x the sub-pixel shift ramp

@@ -64,6 +64,8 @@ PROTOTYPES = {
     "cgs_raster_fwd": (ctypes.c_int, [P, I64, P, I32, G, I32, P, P, I64, P, I32, P]),
     "cgs_render_workspace_bytes": (ctypes.c_size_t, [I64]),
     "cgs_render": (ctypes.c_int, [P, I64, P, I32, G, P, P, P]),
+    "cgs_render_fixed": (ctypes.c_int, [P, I64, P, I32, G, P, P, P]),
+    "cgs_render_scale_offset": (I64, [I64]),
     "cgs_ctf_evaluate": (ctypes.c_int, [P, I32, G, P, P]),
     "cgs_fft_plan_create": (ctypes.c_int, [I32, I32, ctypes.POINTER(ctypes.c_void_p)]),
     "cgs_fft_plan_destroy": (ctypes.c_int, [P]),
@@ -75,6 +77,7 @@ PROTOTYPES = {
     "cgs_obs_spectrum_elems": (I64, [I32, I32]),
     "cgs_obs_spectrum": (ctypes.c_int, [P, P, I32, G, P, P]),
     "cgs_ctf_mse_spectral": (ctypes.c_int, [P, P, I32, G, P, P, P, P]),
+    "cgs_ctf_mse_spectral_fixed": (ctypes.c_int, [P, P, P, I32, G, P, P, P, P]),
     "cgs_voxelize_workspace_bytes": (ctypes.c_size_t, [I64]),
     "cgs_voxelize": (ctypes.c_int, [P, I64, G, P, P, P, P]),
     "cgs_bwd_groups": (I64, [I32, I32]),

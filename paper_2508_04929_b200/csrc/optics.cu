@@ -842,10 +842,10 @@ __global__ void __launch_bounds__(kR2cThreads, 2) obs_spectrum_kernel(const floa
     }
 }
 
-template <int R>
+template <int R, bool kFixed>  // kFixed: render is cgs_render_fixed's int32 image, converted on load
 __global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kernel(
-    const float *__restrict__ render, const float2 *__restrict__ obs_spec, float *__restrict__ upstream,
-    double *__restrict__ loss, int32_t *status) {
+    const float *__restrict__ render, const float *__restrict__ render_scale, const float2 *__restrict__ obs_spec,
+    float *__restrict__ upstream, double *__restrict__ loss, int32_t *status) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     extern __shared__ float2 X[];
     __shared__ double scratch[kR2cThreads / 32];
@@ -861,9 +861,14 @@ __global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kerne
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
     }
     const float4 *r4 = reinterpret_cast<const float4 *>(render + (int64_t)b * D * D);
+    const float inv_scale = kFixed ? 1.f / __ldg(render_scale) : 1.f;
     for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
         const int y = (4 * i) / D, x = 4 * i - y * D;
-        const float4 v = __ldg(r4 + i);
+        float4 v = __ldg(r4 + i);
+        if (kFixed) {
+            v = make_float4((float)__float_as_int(v.x) * inv_scale, (float)__float_as_int(v.y) * inv_scale,
+                            (float)__float_as_int(v.z) * inv_scale, (float)__float_as_int(v.w) * inv_scale);
+        }
         float *row = Xf + y * 2 * P + x;
         row[0] = v.x; row[1] = v.y; row[2] = v.z; row[3] = v.w;
     }
@@ -919,18 +924,19 @@ static int launch_obs_spectrum(const float *obs, const double *ctf, double pix, 
     return check_launch("obs_spectrum_kernel");
 }
 
-template <int R>
-static int launch_ctf_mse_spec(const float *render, const float *spec, int B, float *upstream, double *loss,
-                               int32_t *status, cudaStream_t st) {
+template <int R, bool kFixed>
+static int launch_ctf_mse_spec(const float *render, const float *render_scale, const float *spec, int B,
+                               float *upstream, double *loss, int32_t *status, cudaStream_t st) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     const size_t smem = (size_t)D * P * sizeof(float2);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(ctf_mse_spec_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ctf_mse_spec_kernel<R, kFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         configured = true;
     }
-    ctf_mse_spec_kernel<R><<<B, kR2cThreads, smem, st>>>(render, reinterpret_cast<const float2 *>(spec), upstream,
-                                                         loss, status);
+    ctf_mse_spec_kernel<R, kFixed><<<B, kR2cThreads, smem, st>>>(
+        render, render_scale, reinterpret_cast<const float2 *>(spec), upstream, loss, status);
     return check_launch("ctf_mse_spec_kernel");
 }
 
@@ -1107,9 +1113,25 @@ extern "C" int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, 
                                     float *upstream, double *loss, int32_t *status, void *stream) {
     if (!render || !obs_spec || !upstream || !loss || B <= 0 || render == upstream) return CGS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (grid.size == 128) return launch_ctf_mse_spec<4>(render, obs_spec, B, upstream, loss, status, st);
-    if (grid.size == 64) return launch_ctf_mse_spec<2>(render, obs_spec, B, upstream, loss, status, st);
+    if (grid.size == 128)
+        return launch_ctf_mse_spec<4, false>(render, nullptr, obs_spec, B, upstream, loss, status, st);
+    if (grid.size == 64)
+        return launch_ctf_mse_spec<2, false>(render, nullptr, obs_spec, B, upstream, loss, status, st);
     set_error_detail("cgs_ctf_mse_spectral", "image size must be 64 or 128");
+    return CGS_ERR_UNSUPPORTED;
+}
+
+extern "C" int cgs_ctf_mse_spectral_fixed(const int32_t *render_fixed, const float *render_scale,
+                                          const float *obs_spec, int32_t B, cgs_grid grid, float *upstream,
+                                          double *loss, int32_t *status, void *stream) {
+    const float *r = reinterpret_cast<const float *>(render_fixed);
+    if (!r || !render_scale || !obs_spec || !upstream || !loss || B <= 0 || r == upstream) return CGS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (grid.size == 128)
+        return launch_ctf_mse_spec<4, true>(r, render_scale, obs_spec, B, upstream, loss, status, st);
+    if (grid.size == 64)
+        return launch_ctf_mse_spec<2, true>(r, render_scale, obs_spec, B, upstream, loss, status, st);
+    set_error_detail("cgs_ctf_mse_spectral_fixed", "image size must be 64 or 128");
     return CGS_ERR_UNSUPPORTED;
 }
 

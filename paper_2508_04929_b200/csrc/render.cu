@@ -293,8 +293,8 @@ extern "C" size_t cgs_render_workspace_bytes(int64_t n) {
     return (size_t)(2 * parts + 1) * sizeof(float);
 }
 
-extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
-                          void *ws, void *stream) {
+static int render_impl(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
+                          void *ws, void *stream, bool convert) {
     if (n <= 0 || B <= 0 || grid.size < 1 || !splat || !poses || !out || !ws) return CGS_ERR_ARG;
     const int D = grid.size;
     cudaStream_t st = (cudaStream_t)stream;
@@ -332,9 +332,21 @@ extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, in
     raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), part + 2 * parts, HB,
                                                          scramble_multiplier(n), chunk, reinterpret_cast<int *>(out));
     int rc = check_launch("raster_fwd_atomic_kernel");
-    if (rc) return rc;
+    if (rc || !convert) return rc;
     const int64_t threads = (count + 3) / 4;
     fixed_to_float_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(reinterpret_cast<int *>(out), count,
                                                                            part + 2 * parts);
     return check_launch("fixed_to_float_kernel");
 }
+
+extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
+                          void *ws, void *stream) {
+    return render_impl(splat, n, poses, B, grid, out, ws, stream, true);
+}
+
+extern "C" int cgs_render_fixed(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
+                                int32_t *out, void *ws, void *stream) {
+    return render_impl(splat, n, poses, B, grid, reinterpret_cast<float *>(out), ws, stream, false);
+}
+
+extern "C" int64_t cgs_render_scale_offset(int64_t n) { return 2 * ((n + kWbBlock - 1) / kWbBlock); }

@@ -337,8 +337,9 @@ class StepPipeline:
         observation spectra (otherwise the spectral path adds one obs_spectrum launch)."""
         if not ctf:
             return 8
-        if self.spectral:
-            return 8 if obs_spectrum else 9
+        if self.spectral:  # the direct render hands K4 its fixed-point image: no conversion kernel
+            n = 7 if self.render_mode == "direct" else 8
+            return n if obs_spectrum else n + 1
         fused = self.D in (32, 64, 128) and os.environ.get("CGS_CTF_CUFFT", "0") != "1"
         return 8 if fused else 10
 
@@ -347,6 +348,18 @@ class StepPipeline:
         """K4 runs in the Fourier domain (cgs_ctf_mse_spectral) for D = 64 / 128 with a CTF;
         CGS_CTF_SPATIAL=1 keeps the real-space kernel (A/B)."""
         return self.obs_spec is not None
+
+    def _render_scale(self):
+        """Device view of the fixed-point render's scale (pixel = int / scale) in render_ws."""
+        off = int(self.ctx.lib.cgs_render_scale_offset(self.n))
+        return self.render_ws[off:off + 1]
+
+    def render_image(self):
+        """The last forward's rendered images as f32 [B][D][D] (converted from the fixed-point
+        image when the step fed it to K4 unconverted)."""
+        if not getattr(self, "_render_fixed", False):
+            return self.render
+        return self.render.view(torch.int32).to(torch.float32) / self._render_scale()
 
     def forward_backward(self, params, poses, obs, ctf, events=None, obs_spec=None):
         """K0..K5 for a batch; leaves partial accumulators in self.partial.
@@ -363,7 +376,13 @@ class StepPipeline:
 
         mark("fwd", 0)
         self._prepare(params)
-        if self.render_mode == "direct":
+        # direct render feeding the spectral K4: the int32 fixed-point image is converted as K4 loads it
+        fixed = self.render_mode == "direct" and ctf is not None and self.spectral
+        self._render_fixed = fixed
+        if fixed:
+            _lib.call("cgs_render_fixed", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid,
+                      _ptr(self.render), _ptr(self.render_ws), s)
+        elif self.render_mode == "direct":
             _lib.call("cgs_render", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid, _ptr(self.render),
                       _ptr(self.render_ws), s)
         else:
@@ -379,8 +398,12 @@ class StepPipeline:
             if obs_spec is None:  # this batch's records (a dataset passes its precomputed ones)
                 _lib.call("cgs_obs_spectrum", _ptr(obs), _ptr(ctf), self.B, self.grid, _ptr(self.obs_spec), s)
                 obs_spec = self.obs_spec
-            _lib.call("cgs_ctf_mse_spectral", _ptr(self.render), _ptr(obs_spec), self.B, self.grid,
-                      _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
+            if fixed:
+                _lib.call("cgs_ctf_mse_spectral_fixed", _ptr(self.render), _ptr(self._render_scale()), _ptr(obs_spec),
+                          self.B, self.grid, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
+            else:
+                _lib.call("cgs_ctf_mse_spectral", _ptr(self.render), _ptr(obs_spec), self.B, self.grid,
+                          _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
         else:
             _lib.call("cgs_ctf_mse", self.plan, _ptr(self.render), _ptr(obs), self.B, self.grid, _ptr(ctf),
                       _ptr(self.spectrum), 0, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status),

@@ -387,7 +387,7 @@ def test_fused_step_matches_reference(oracle, case, render):
     if not np.isnan(g["defocus"][0]):
         ctfs = np.stack([oracle.Ctf(d, d).as_array() for d in g["defocus"]])
     losses, grads, pipe = _full_step_device(params, poses, grid, g["observed"], ctfs, render=render)
-    rend = pipe.render.cpu().numpy()
+    rend = pipe.render_image().cpu().numpy()
     for i in range(len(poses)):
         assert rel_l2(rend[i], g["rendered"][i]) < RENDER_TOL
     np.testing.assert_allclose(losses, g["losses"], rtol=1e-4)
@@ -421,11 +421,11 @@ def test_determinism_bitwise(oracle):
     obs = np.random.default_rng(5).standard_normal((16, 128, 128)).astype(np.float32) * 1e-3
     ctfs = np.stack([oracle.Ctf(15000.0, 15000.0).as_array()] * 16)
     l1, g1, p1 = _full_step_device(params, poses, grid, obs, ctfs)
-    r1 = p1.render.clone()
+    r1 = p1.render_image().clone()
     l2, g2, p2 = _full_step_device(params, poses, grid, obs, ctfs)
     assert np.array_equal(l1, l2)
     assert np.array_equal(g1, g2)
-    assert torch.equal(r1, p2.render)
+    assert torch.equal(r1, p2.render_image())
 
 
 @pytest.mark.parametrize("D", [32, 64, 128])
