@@ -333,15 +333,20 @@ class StepPipeline:
     # epilogue_adam.  K4 is one ctf_mse_fused kernel for D = 32 / 64 / 128; otherwise ctf_multiply x2 +
     # loss_resid around cuFFT's own R2C/C2R kernels (library launches, not counted).
     def own_launches_per_step(self, ctf: bool = True, obs_spectrum: bool = False) -> int:
-        """Kernels of this library per step; obs_spectrum: the spectral K4 is fed precomputed
-        observation spectra (otherwise the spectral path adds one obs_spectrum launch)."""
+        """Kernels of this library per direct-mode step (bench accounting): prepare; weight bound
+        (2) + raster_fwd_atomic (+ fixed_to_float unless the spectral K4 converts on load); K4;
+        raster_bwd; epilogue + Adam.  K4 is one kernel (spectral, plus obs_spectrum when the
+        batch's records are not precomputed; or the real-space kernel for D = 32/64/128), or
+        multiply x2 + loss around cuFFT's own transforms; without a CTF it is the loss/residual
+        kernel."""
+        spectral = ctf and self.spectral
+        n = 1 + 3 + (0 if spectral else 1) + 1 + 1
         if not ctf:
-            return 8
-        if self.spectral:  # the direct render hands K4 its fixed-point image: no conversion kernel
-            n = 7 if self.render_mode == "direct" else 8
-            return n if obs_spectrum else n + 1
+            return n + 1
+        if spectral:
+            return n + (1 if obs_spectrum else 2)
         fused = self.D in (32, 64, 128) and os.environ.get("CGS_CTF_CUFFT", "0") != "1"
-        return 8 if fused else 10
+        return n + (1 if fused else 3)
 
     @property
     def spectral(self) -> bool:
