@@ -7,7 +7,7 @@ The dataset (128^2, helix-50 truth, DefocusRange(1e4, 2.5e4), SNR 0.1) is genera
 by ``cs.simulate`` with device noise and kept in HBM (6.5 GB at 100k).  The epoch is the
 reference's schedule at a fixed global batch of 256: the seeded permutation cut into 391
 batches (train.py:228-232), one Reconstructor step each (50k random-init Gaussians, CTF, Adam).
-Timed with CUDA events around the whole epoch, after 3 warm-up steps; the loss is read back
+Timed with CUDA events around the whole epoch, after 50 warm-up steps; the loss is read back
 once at the end.  Experiment tooling: bench.py holds the headline line.
 """
 
@@ -60,7 +60,7 @@ def main():
     rec = Reconstructor(grid, params, res.images, poses, ctfs, batch_size=args.batch, process_group=pg)
     del res
     batches = parallel.epoch_batches(args.particles, args.batch, np.random.default_rng(0))
-    for b in batches[:3]:  # warm-up (pipelines, plans, clocks)
+    for b in batches[:50]:  # warm-up (pipelines, graphs, clocks)
         rec.step(b, args.lr)
     torch.cuda.synchronize()
     a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
