@@ -446,6 +446,7 @@ class StepPipeline:
     def render_only(self, params, poses):
         """K0 + K3 (direct mode): rendered images in self.render."""
         self._prepare(params)
+        self._render_fixed = False
         _lib.call("cgs_render", _ptr(self.splat), self.n, _ptr(poses), poses.shape[0], self.grid, _ptr(self.render),
                   _ptr(self.render_ws), self.ctx.stream)
         return self.render
