@@ -778,3 +778,14 @@ def test_data_parallel_step_two_ranks(tmp_path, poison):
     rec.step_batch(rec.obs, rec.poses, rec.ctfs, 1e-3, global_batch=8)
     ref = rec.params_host()
     assert rel_l2(got - params, ref - params) < 1e-5
+
+
+def test_graft_entry_smoke():
+    """The driver's smoke(): one small fused step on cuda:0 checked against the oracle."""
+    import importlib
+    import sys
+
+    from conftest import ROOT
+
+    sys.path.insert(0, ROOT)
+    importlib.import_module("__graft_entry__").smoke()
