@@ -43,6 +43,9 @@ extern "C" {
 
 #define CGS_LAYOUT_NATURAL 0
 #define CGS_LAYOUT_FFT 1
+/* rows 2j and 2j+1 interleaved: pixel (2j + t, x) at float index (j D + x) 2 + t
+ * (even D; the spectral K4's upstream for the backward's region staging) */
+#define CGS_LAYOUT_ROWPAIR 2
 
 #define CGS_MODE_ANISOTROPIC 0
 #define CGS_MODE_ISOTROPIC 1
@@ -190,12 +193,13 @@ int cgs_ctf_mse(void *plan, const float *render, const float *obs, int32_t B, cg
 int64_t cgs_obs_spectrum_elems(int32_t size, int32_t B);
 int cgs_obs_spectrum(const float *obs, const double *ctf, int32_t B, cgs_grid grid, float *spec, void *stream);
 int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, int32_t B, cgs_grid grid, float *upstream,
-                         double *loss, int32_t *status, void *stream);
+                         double *loss, int32_t *status, int32_t upstream_layout, void *stream);
 /* The same from a cgs_render_fixed image: render_fixed int32 [B][D][D] and its
- * scale pointer (ws + cgs_render_scale_offset(n)). */
+ * scale pointer (ws + cgs_render_scale_offset(n)).  upstream_layout:
+ * CGS_LAYOUT_NATURAL or CGS_LAYOUT_ROWPAIR. */
 int cgs_ctf_mse_spectral_fixed(const int32_t *render_fixed, const float *render_scale, const float *obs_spec,
                                int32_t B, cgs_grid grid, float *upstream, double *loss, int32_t *status,
-                               void *stream);
+                               int32_t upstream_layout, void *stream);
 
 /* Batched Fourier filter out = Re ifft2(F fft2(in)), per image F = H_sym (CTF,
  * ctf f64 [B][8], may be NULL) x the sub-pixel shift ramp

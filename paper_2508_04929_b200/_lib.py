@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("CGS_B200_LIB") or os.path.join(_HERE, "libcgs_b200.so
 CGS_OK = 0
 CGS_LAYOUT_NATURAL = 0
 CGS_LAYOUT_FFT = 1
+CGS_LAYOUT_ROWPAIR = 2
 CGS_MODE = {"anisotropic": 0, "isotropic": 1}
 CGS_SPLAT_STRIDE = 16
 CGS_ACC_STRIDE = 10
@@ -76,8 +77,8 @@ PROTOTYPES = {
     "cgs_fourier_filter": (ctypes.c_int, [P, P, I32, G, P, P, P]),
     "cgs_obs_spectrum_elems": (I64, [I32, I32]),
     "cgs_obs_spectrum": (ctypes.c_int, [P, P, I32, G, P, P]),
-    "cgs_ctf_mse_spectral": (ctypes.c_int, [P, P, I32, G, P, P, P, P]),
-    "cgs_ctf_mse_spectral_fixed": (ctypes.c_int, [P, P, P, I32, G, P, P, P, P]),
+    "cgs_ctf_mse_spectral": (ctypes.c_int, [P, P, I32, G, P, P, P, I32, P]),
+    "cgs_ctf_mse_spectral_fixed": (ctypes.c_int, [P, P, P, I32, G, P, P, P, I32, P]),
     "cgs_voxelize_workspace_bytes": (ctypes.c_size_t, [I64]),
     "cgs_voxelize": (ctypes.c_int, [P, I64, G, P, P, P, P]),
     "cgs_bwd_groups": (I64, [I32, I32]),

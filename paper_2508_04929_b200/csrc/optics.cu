@@ -842,7 +842,8 @@ __global__ void __launch_bounds__(kR2cThreads, 2) obs_spectrum_kernel(const floa
     }
 }
 
-template <int R, bool kFixed>  // kFixed: render is cgs_render_fixed's int32 image, converted on load
+template <int R, bool kFixed, bool kRowPair>  // kFixed: render is cgs_render_fixed's int32 image, converted
+                                              // on load; kRowPair: upstream in CGS_LAYOUT_ROWPAIR
 __global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kernel(
     const float *__restrict__ render, const float *__restrict__ render_scale, const float2 *__restrict__ obs_spec,
     float *__restrict__ upstream, double *__restrict__ loss, int32_t *status) {
@@ -903,10 +904,18 @@ __global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kerne
     }
     c2r_2d<R>(X, F);
     float4 *u4 = reinterpret_cast<float4 *>(upstream + (int64_t)b * D * D);
-    for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
-        const int y = (4 * i) / D, x = 4 * i - y * D;
-        const float *row = Xf + y * 2 * P + x;
-        u4[i] = make_float4(row[0], row[1], row[2], row[3]);
+    if (kRowPair) {  // float4 i = pixels (2j, x), (2j+1, x), (2j, x+1), (2j+1, x+1)
+        for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
+            const int j = (2 * i) / D, x = 2 * i - j * D;
+            const float *r0 = Xf + (2 * j) * 2 * P + x, *r1 = r0 + 2 * P;
+            u4[i] = make_float4(r0[0], r1[0], r0[1], r1[1]);
+        }
+    } else {
+        for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
+            const int y = (4 * i) / D, x = 4 * i - y * D;
+            const float *row = Xf + y * 2 * P + x;
+            u4[i] = make_float4(row[0], row[1], row[2], row[3]);
+        }
     }
 }
 
@@ -924,20 +933,30 @@ static int launch_obs_spectrum(const float *obs, const double *ctf, double pix, 
     return check_launch("obs_spectrum_kernel");
 }
 
-template <int R, bool kFixed>
-static int launch_ctf_mse_spec(const float *render, const float *render_scale, const float *spec, int B,
-                               float *upstream, double *loss, int32_t *status, cudaStream_t st) {
+template <int R, bool kFixed, bool kRowPair>
+static int launch_ctf_mse_spec_t(const float *render, const float *render_scale, const float *spec, int B,
+                                 float *upstream, double *loss, int32_t *status, cudaStream_t st) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     const size_t smem = (size_t)D * P * sizeof(float2);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(ctf_mse_spec_kernel<R, kFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(ctf_mse_spec_kernel<R, kFixed, kRowPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         configured = true;
     }
-    ctf_mse_spec_kernel<R, kFixed><<<B, kR2cThreads, smem, st>>>(
+    ctf_mse_spec_kernel<R, kFixed, kRowPair><<<B, kR2cThreads, smem, st>>>(
         render, render_scale, reinterpret_cast<const float2 *>(spec), upstream, loss, status);
     return check_launch("ctf_mse_spec_kernel");
+}
+
+template <int R, bool kFixed>
+static int launch_ctf_mse_spec(const float *render, const float *render_scale, const float *spec, int B,
+                               float *upstream, double *loss, int32_t *status, int layout, cudaStream_t st) {
+    if (layout == CGS_LAYOUT_ROWPAIR)
+        return launch_ctf_mse_spec_t<R, kFixed, true>(render, render_scale, spec, B, upstream, loss, status, st);
+    if (layout == CGS_LAYOUT_NATURAL)
+        return launch_ctf_mse_spec_t<R, kFixed, false>(render, render_scale, spec, B, upstream, loss, status, st);
+    return CGS_ERR_ARG;
 }
 
 template <int R>
@@ -1110,27 +1129,28 @@ extern "C" int cgs_obs_spectrum(const float *obs, const double *ctf, int32_t B, 
 }
 
 extern "C" int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, int32_t B, cgs_grid grid,
-                                    float *upstream, double *loss, int32_t *status, void *stream) {
+                                    float *upstream, double *loss, int32_t *status, int32_t upstream_layout,
+                                    void *stream) {
     if (!render || !obs_spec || !upstream || !loss || B <= 0 || render == upstream) return CGS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     if (grid.size == 128)
-        return launch_ctf_mse_spec<4, false>(render, nullptr, obs_spec, B, upstream, loss, status, st);
+        return launch_ctf_mse_spec<4, false>(render, nullptr, obs_spec, B, upstream, loss, status, upstream_layout, st);
     if (grid.size == 64)
-        return launch_ctf_mse_spec<2, false>(render, nullptr, obs_spec, B, upstream, loss, status, st);
+        return launch_ctf_mse_spec<2, false>(render, nullptr, obs_spec, B, upstream, loss, status, upstream_layout, st);
     set_error_detail("cgs_ctf_mse_spectral", "image size must be 64 or 128");
     return CGS_ERR_UNSUPPORTED;
 }
 
 extern "C" int cgs_ctf_mse_spectral_fixed(const int32_t *render_fixed, const float *render_scale,
                                           const float *obs_spec, int32_t B, cgs_grid grid, float *upstream,
-                                          double *loss, int32_t *status, void *stream) {
+                                          double *loss, int32_t *status, int32_t upstream_layout, void *stream) {
     const float *r = reinterpret_cast<const float *>(render_fixed);
     if (!r || !render_scale || !obs_spec || !upstream || !loss || B <= 0 || r == upstream) return CGS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     if (grid.size == 128)
-        return launch_ctf_mse_spec<4, true>(r, render_scale, obs_spec, B, upstream, loss, status, st);
+        return launch_ctf_mse_spec<4, true>(r, render_scale, obs_spec, B, upstream, loss, status, upstream_layout, st);
     if (grid.size == 64)
-        return launch_ctf_mse_spec<2, true>(r, render_scale, obs_spec, B, upstream, loss, status, st);
+        return launch_ctf_mse_spec<2, true>(r, render_scale, obs_spec, B, upstream, loss, status, upstream_layout, st);
     set_error_detail("cgs_ctf_mse_spectral_fixed", "image size must be 64 or 128");
     return CGS_ERR_UNSUPPORTED;
 }

@@ -447,7 +447,7 @@ constexpr int kMaxPoseImages = 64;  // image groups up to this size keep fp32 po
 #endif
 constexpr int kRegFloats = CGS_BWD_REG_FLOATS;  // 24 KB per band (measured 8..32 KB)
 
-template <bool kPoseSmem>
+template <bool kPoseSmem, bool kRowPair>  // kRowPair: upstream in CGS_LAYOUT_ROWPAIR (a straight float2 copy)
 __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
@@ -513,13 +513,21 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
             // from an integer, far above the rcp error; i is tracked as an exact float
             {
                 const float invW = rcp_approx((float)W);
-                const float *sb = src + by0 * D + R.x0;
                 const int nel = np * W;
                 float fi = (float)threadIdx.x + 0.5f;
-                for (int i = threadIdx.x; i < nel; i += kRegThreads, fi += (float)kRegThreads) {
-                    const int j = __float_as_int(__fmaf_rd(fi, invW, 12582912.0f)) - 0x4B400000;
-                    const float *p = sb + j * (2 * D) + (i - j * W);
-                    reg2[i] = f2pack(__ldg(p), by0 + 2 * j + 1 < D ? __ldg(p + D) : 0.f);
+                if (kRowPair) {  // the pair rows are already interleaved in HBM (even D)
+                    const float2 *sb2 = reinterpret_cast<const float2 *>(src) + (by0 >> 1) * D + R.x0;
+                    for (int i = threadIdx.x; i < nel; i += kRegThreads, fi += (float)kRegThreads) {
+                        const int j = __float_as_int(__fmaf_rd(fi, invW, 12582912.0f)) - 0x4B400000;
+                        reg2[i] = __ldg(sb2 + j * D + (i - j * W));
+                    }
+                } else {
+                    const float *sb = src + by0 * D + R.x0;
+                    for (int i = threadIdx.x; i < nel; i += kRegThreads, fi += (float)kRegThreads) {
+                        const int j = __float_as_int(__fmaf_rd(fi, invW, 12582912.0f)) - 0x4B400000;
+                        const float *p = sb + j * (2 * D) + (i - j * W);
+                        reg2[i] = f2pack(__ldg(p), by0 + 2 * j + 1 < D ? __ldg(p + D) : 0.f);
+                    }
                 }
             }
             __syncthreads();
@@ -591,14 +599,25 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
         const char *v = getenv("CGS_BWD_KERNEL");
         variant = (v && v[0] == 'd') ? 1 : (v && v[0] == 'b') ? 2 : 0;
     }
-    if (layout == CGS_LAYOUT_NATURAL && variant == 0 && D <= kRegFloats / 2) {
+    if (layout == CGS_LAYOUT_ROWPAIR && ((D & 1) || D > kRegFloats / 2)) return CGS_ERR_UNSUPPORTED;
+    if ((layout == CGS_LAYOUT_NATURAL && variant == 0 && D <= kRegFloats / 2) || layout == CGS_LAYOUT_ROWPAIR) {
         dim3 g((unsigned)((n + kRegThreads - 1) / kRegThreads), (unsigned)G);
-        if (images_per_group <= kMaxPoseImages)
-            raster_bwd_region_kernel<true><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), upstream,
-                                                                      partial, images_per_group);
-        else
-            raster_bwd_region_kernel<false><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, make_grid_f(grid), upstream,
-                                                                       partial, images_per_group);
+        const GridF gf = make_grid_f(grid);
+        const bool ps = images_per_group <= kMaxPoseImages;
+        if (layout == CGS_LAYOUT_ROWPAIR) {
+            if (ps)
+                raster_bwd_region_kernel<true, true><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, gf, upstream,
+                                                                               partial, images_per_group);
+            else
+                raster_bwd_region_kernel<false, true><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, gf, upstream,
+                                                                                partial, images_per_group);
+        } else if (ps) {
+            raster_bwd_region_kernel<true, false><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, gf, upstream,
+                                                                            partial, images_per_group);
+        } else {
+            raster_bwd_region_kernel<false, false><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, gf, upstream,
+                                                                             partial, images_per_group);
+        }
         return check_launch("raster_bwd_region_kernel");
     }
     const size_t db_bytes = (2 * (size_t)D * D + kRowPad) * sizeof(float);

@@ -403,20 +403,24 @@ class StepPipeline:
             if obs_spec is None:  # this batch's records (a dataset passes its precomputed ones)
                 _lib.call("cgs_obs_spectrum", _ptr(obs), _ptr(ctf), self.B, self.grid, _ptr(self.obs_spec), s)
                 obs_spec = self.obs_spec
+            # the upstream goes out with row pairs interleaved: the backward's region staging is a copy
+            up_layout = _lib.CGS_LAYOUT_ROWPAIR
             if fixed:
                 _lib.call("cgs_ctf_mse_spectral_fixed", _ptr(self.render), _ptr(self._render_scale()), _ptr(obs_spec),
-                          self.B, self.grid, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
+                          self.B, self.grid, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), up_layout, s)
             else:
                 _lib.call("cgs_ctf_mse_spectral", _ptr(self.render), _ptr(obs_spec), self.B, self.grid,
-                          _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
+                          _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), up_layout, s)
         else:
+            up_layout = _lib.CGS_LAYOUT_NATURAL
             _lib.call("cgs_ctf_mse", self.plan, _ptr(self.render), _ptr(obs), self.B, self.grid, _ptr(ctf),
                       _ptr(self.spectrum), 0, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status),
                       _lib.CGS_LAYOUT_NATURAL, s)
+        self.upstream_layout = up_layout
         mark("ctf", 1)
         mark("bwd", 0)
         _lib.call("cgs_raster_bwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid,
-                  _ptr(self.upstream), _lib.CGS_LAYOUT_NATURAL, _ptr(self.partial), self.ipg, s)
+                  _ptr(self.upstream), up_layout, _ptr(self.partial), self.ipg, s)
         mark("bwd", 1)
 
     def reduce(self):

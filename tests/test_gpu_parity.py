@@ -340,7 +340,10 @@ def test_spectral_ctf_mse_matches_oracle(oracle, D):
     status = torch.zeros(1, dtype=torch.int32, device=r.device)
     _lib.call("cgs_obs_spectrum", o.data_ptr(), c.data_ptr(), B, gs, spec.data_ptr(), ctx.stream)
     _lib.call("cgs_ctf_mse_spectral", r.data_ptr(), spec.data_ptr(), B, gs, up.data_ptr(),
-              loss.data_ptr(), status.data_ptr(), ctx.stream)
+              loss.data_ptr(), status.data_ptr(), _lib.CGS_LAYOUT_NATURAL, ctx.stream)
+    up_rp = torch.empty_like(r)  # the same upstream with row pairs interleaved (the step's layout)
+    _lib.call("cgs_ctf_mse_spectral", r.data_ptr(), spec.data_ptr(), B, gs, up_rp.data_ptr(),
+              loss.data_ptr(), status.data_ptr(), _lib.CGS_LAYOUT_ROWPAIR, ctx.stream)
     up2 = torch.empty_like(r)
     loss2 = torch.empty_like(loss)
     wspec = torch.empty(2 * int(ctx.lib.cgs_fft_spectrum_elems(D, B)), dtype=torch.float32, device=r.device)
@@ -356,6 +359,8 @@ def test_spectral_ctf_mse_matches_oracle(oracle, D):
         assert abs(loss[b].item() - l_ref) <= 1e-5 * l_ref
         assert rel_l2(up[b].cpu().numpy(), up2[b].cpu().numpy()) < 1e-5
     np.testing.assert_allclose(loss.cpu().numpy(), loss2.cpu().numpy(), rtol=1e-5)
+    interleaved = up.view(B, D // 2, 2, D).transpose(2, 3).reshape(B, D, D)
+    assert torch.equal(up_rp, interleaved)
     assert status.item() == 0
     # the ABI refuses sizes without a spectral kernel and a missing CTF
     assert ctx.lib.cgs_obs_spectrum_elems(96, 1) == 0
