@@ -794,3 +794,32 @@ def test_graft_entry_smoke():
 
     sys.path.insert(0, ROOT)
     importlib.import_module("__graft_entry__").smoke()
+
+
+def test_backward_rowpair_layout_is_bitwise_natural(oracle):
+    """K5 reading the upstream as interleaved row pairs (CGS_LAYOUT_ROWPAIR, the spectral K4's
+    output) stages exactly what the natural layout stages: partial accumulators bitwise equal.
+    Odd D has no row-pair layout."""
+    D, n, B = 128, 3000, 12
+    grid = oracle.Grid(D, 0.5, 1.5)
+    params = oracle.init_random(n, 1, grid)
+    poses = [oracle.sample_pose(np.random.default_rng(60 + i)) for i in range(B)]
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(D, 0.5, 1.5)
+    p = _dev(params, torch.float64)
+    P = _dev(engine.pose_array([W for W, _ in poses], [t for _, t in poses]), torch.float64)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    splat = engine.prepare(ctx, p, status)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    up = torch.randn((B, D, D), generator=gen, device="cuda", dtype=torch.float32) * 1e-3
+    up_rp = up.view(B, D // 2, 2, D).transpose(2, 3).contiguous()
+    G = int(ctx.lib.cgs_bwd_groups(B, engine.DEFAULT_IMAGES_PER_GROUP))
+    a = torch.empty(G * n * 10, dtype=torch.float32, device="cuda")
+    b = torch.empty_like(a)
+    engine.raster_bwd(ctx, splat, n, P, gs, up, out=a)
+    engine.raster_bwd(ctx, splat, n, P, gs, up_rp, out=b, layout=_lib.CGS_LAYOUT_ROWPAIR)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    g33 = _lib.grid_struct(33, 0.5, 1.5)
+    assert ctx.lib.cgs_raster_bwd(splat.data_ptr(), n, P.data_ptr(), B, g33, up.data_ptr(),
+                                  _lib.CGS_LAYOUT_ROWPAIR, a.data_ptr(), 10, None) == 4  # CGS_ERR_UNSUPPORTED
