@@ -427,14 +427,15 @@ class StepPipeline:
         _lib.call("cgs_reduce_partials", _ptr(self.partial), self.G, self.n, _ptr(self.acc), self.ctx.stream)
         return self.acc
 
-    def adam(self, params, m, v, *, scale, lr, beta1, beta2, eps, t, acc=None, groups=None, skip=None):
+    def adam(self, params, m, v, *, scale, lr, beta1, beta2, eps, t, acc=None, groups=None, skip=None, n=None):
         """K6 fused epilogue + Adam; acc defaults to this step's partials.  ``skip`` (int32 device
         status) decides whether the update is skipped; default: this pipeline's own status."""
         src = self.partial if acc is None else acc
         G = self.G if acc is None else (groups or 1)
         bc1 = 1.0 - beta1 ** t
         bc2 = 1.0 - beta2 ** t
-        _lib.call("cgs_epilogue_adam", _ptr(src), G, self.n, _ptr(params), _ptr(m), _ptr(v), self.mode,
+        _lib.call("cgs_epilogue_adam", _ptr(src), G, self.n if n is None else n, _ptr(params), _ptr(m), _ptr(v),
+                  self.mode,
                   float(scale), float(lr), float(beta1), float(beta2), float(eps), float(bc1), float(bc2),
                   _ptr(self.status if skip is None else skip), self.ctx.stream)
 

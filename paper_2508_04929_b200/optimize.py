@@ -236,6 +236,9 @@ class Reconstructor:
         self._idx_slots: dict = {}  # step's graph inputs (batch indices, gathered batch, Adam scalars)
         # step_host replays each slot's step as a CUDA graph (single GPU; CGS_GRAPHS=0 disables)
         self.use_graphs = os.environ.get("CGS_GRAPHS", "1") == "1"
+        # multi-GPU: CGS_DP_SHARDED=1 reduce-scatters the accumulator, runs the epilogue + Adam
+        # on this rank's Gaussian slice only and all-gathers the parameters (ZeRO-1 style)
+        self.sharded = self.world > 1 and os.environ.get("CGS_DP_SHARDED", "0") == "1"
 
     # -- helpers -------------------------------------------------------------
     def local_slice(self, indices: np.ndarray) -> np.ndarray:
@@ -424,7 +427,16 @@ class Reconstructor:
         pipe.forward_backward(self.params, poses, obs, ctfs, events=events, obs_spec=obs_spec)
         scale = 1.0 / global_batch
         self.t += 1
-        if self.world > 1:
+        if self.sharded:
+            acc = pipe.reduce()
+            part, skip = parallel.reduce_scatter_accumulator(acc, self.n, self.pg, status=pipe.status)
+            a, b, per = parallel.gaussian_slice(self.n, self.rank, self.world)
+            if b > a:
+                pipe.adam(self.params[a:b], self.m[a:b], self.v[a:b], scale=scale, lr=lr, beta1=cfg.adam_beta1,
+                          beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t, acc=part, groups=1, skip=skip,
+                          n=b - a)
+            parallel.all_gather_rows(self.params, per, self.pg)
+        elif self.world > 1:
             acc = pipe.reduce()
             skip = parallel.allreduce_accumulator(acc, self.pg, status=pipe.status)
             pipe.adam(self.params, self.m, self.v, scale=scale, lr=lr, beta1=cfg.adam_beta1,
@@ -451,6 +463,10 @@ class Reconstructor:
         torch = _torch()
         local = morton_order(self.params[:, :3].cpu().numpy(), self.grid.extent)
         idx = torch.as_tensor(local, device=self.params.device)
+        if self.sharded:  # the moments are current only on their owner: replicate before permuting
+            per = parallel.gaussian_slice(self.n, self.rank, self.world)[2]
+            parallel.all_gather_rows(self.m, per, self.pg)
+            parallel.all_gather_rows(self.v, per, self.pg)
         # in place: captured step graphs keep pointing at these buffers
         self.params.copy_(self.params.index_select(0, idx))
         self.m.copy_(self.m.index_select(0, idx))

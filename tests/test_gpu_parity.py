@@ -715,7 +715,7 @@ def test_full_size_c2_properties(oracle):
     assert int(status.item()) == 0
 
 
-def _dp_gpu_worker(rank, world, port, out_path, poison):
+def _dp_gpu_worker(rank, world, port, out_path, poison, sharded=False):
     import os
     import sys
 
@@ -723,6 +723,7 @@ def _dp_gpu_worker(rank, world, port, out_path, poison):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["CGS_DP_SHARDED"] = "1" if sharded else "0"
     from conftest import ROOT
 
     sys.path.insert(0, ROOT)
@@ -736,6 +737,7 @@ def _dp_gpu_worker(rank, world, port, out_path, poison):
         obs = obs.copy()
         obs[5, 0, 0] = np.nan  # image 5 is in rank 1's half of the batch
     rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=8, process_group=dist.group.WORLD)
+    assert rec.sharded == sharded
     idx = rec.local_slice(np.arange(8))
     dev = rec.ctx.device
     sel = torch.as_tensor(idx, device=dev)
@@ -758,11 +760,13 @@ def _dp_inputs(cs2, eng):
     return params, obs, eng.pose_array(rot), ctfs, grid
 
 
+@pytest.mark.parametrize("sharded", [False, True])
 @pytest.mark.parametrize("poison", [False, True])
-def test_data_parallel_step_two_ranks(tmp_path, poison):
+def test_data_parallel_step_two_ranks(tmp_path, poison, sharded):
     """Reconstructor.step_batch with a 2-rank process group (gloo; both ranks on this GPU, host-level
     collectives only, no kernel waits on another rank) equals the single-process full-batch step;
-    a NaN observation on one rank makes both ranks skip the update."""
+    a NaN observation on one rank makes both ranks skip the update.  sharded: the ZeRO-1 style
+    epilogue (reduce-scatter, Adam on each rank's Gaussian slice, all-gather of the parameters)."""
     import socket
 
     import torch.multiprocessing as mp
@@ -773,7 +777,7 @@ def test_data_parallel_step_two_ranks(tmp_path, poison):
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     out = str(tmp_path / "dp.npy")
-    mp.spawn(_dp_gpu_worker, args=(2, port, out, poison), nprocs=2, join=True)
+    mp.spawn(_dp_gpu_worker, args=(2, port, out, poison, sharded), nprocs=2, join=True)
     got = np.load(out)
     params, obs, poses, ctfs, grid = _dp_inputs(cs, engine)
     if poison:

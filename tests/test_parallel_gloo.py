@@ -139,3 +139,46 @@ def test_skip_decision_is_shared_by_all_ranks(tmp_path):
     assert res[:, 0].tolist() == [6.0, 6.0]  # SKIP_BITS on both ranks
     assert res[:, 1].tolist() == [3.0, 3.0]  # the accumulator itself is summed
     assert res[:, 2].tolist() == [0.0, 0.0]
+
+
+def _shard_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_2508_04929_b200 import parallel
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 7
+    acc = torch.arange(n * 10 + 1, dtype=torch.float32) * (rank + 1)
+    status = torch.tensor([4 if rank == 2 else 0], dtype=torch.int32)
+    part, skip = parallel.reduce_scatter_accumulator(acc, n, status=status)
+    a, b, per = parallel.gaussian_slice(n, rank, world)
+    full = torch.full((n, 11), float(rank))
+    parallel.all_gather_rows(full, per)
+    res = [part[: (b - a) * 10].clone(), skip.clone(), full.clone()]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, [t.numpy() for t in res])
+    if rank == 0:
+        np.save(out_path, np.array(gathered, dtype=object), allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_epilogue_collectives(tmp_path):
+    """The ZeRO-1 style exchange on 3 ranks: each rank receives the rank-sum of its own Gaussian
+    slice (ceil(7/3) = 3, 3, 1 rows), the skip flag is shared, and every rank ends with every
+    slice's rows."""
+    out = str(tmp_path / "shard.npy")
+    mp.spawn(_shard_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    res = np.load(out, allow_pickle=True)
+    from paper_2508_04929_b200 import parallel
+
+    total = np.arange(7 * 10 + 1, dtype=np.float32) * (1 + 2 + 3)
+    for r in range(3):
+        a, b, _ = parallel.gaussian_slice(7, r, 3)
+        np.testing.assert_array_equal(res[r][0], total[a * 10:b * 10])
+        assert int(res[r][1][0]) == parallel.SKIP_BITS
+        rows = np.concatenate([np.full((min(7, (k + 1) * 3) - min(7, k * 3), 11), float(k)) for k in range(3)])
+        np.testing.assert_array_equal(res[r][2], rows)
