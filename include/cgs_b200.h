@@ -66,18 +66,27 @@ typedef struct cgs_grid {
 #define CGS_STATUS_DEGENERATE_ROTATION 1 /* DegenerateRotationError, splat.py:191-193 */
 #define CGS_STATUS_BIN_OVERFLOW 2        /* tile list exceeded the item capacity */
 #define CGS_STATUS_NONFINITE_LOSS 4      /* a loss was NaN/inf: Adam skips the update (train.py:144-145) */
+#define CGS_STATUS_NONFINITE_PARAMS 8    /* a mean / scale / amplitude was NaN or inf (set by cgs_prepare):
+                                          * the loss kernels then report NaN losses, as the reference's
+                                          * render of such a mixture does (train.py:146-149) */
 
 const char *cgs_version(void);
 const char *cgs_error_string(int code);
 /* last CUDA / cuFFT error text seen by the library (host string, thread-local) */
 const char *cgs_last_error_detail(void);
+/* number of (kernel) launch-state entries (dynamic shared-memory opt-in,
+ * resident-slot memo) the library holds for a device ordinal: the state is
+ * per device, so a process may drive several GPUs (evaluate.py:182-200). */
+int32_t cgs_launch_state_entries(int32_t device);
 
 /* ---- K0: per-Gaussian preparation ---------------------------------------
  * Replaces the image-independent part of _Projection.__init__
  * (splat.py:184-196): softplus activate (gmm.py:76-80), quaternion
  * normalisation and rotation (gmm.py:101-124), M = R diag(s).
- * Writes splat[N][16] = {mean xyz, amp, M (9, row-major), 0,0,0}.  A zero or
- * non-finite quaternion norm sets CGS_STATUS_DEGENERATE_ROTATION in *status. */
+ * Writes splat[N][16] = {mean xyz, amp, M (9, row-major), s_max, s_min, s_mid}.  A zero or
+ * non-finite quaternion norm sets CGS_STATUS_DEGENERATE_ROTATION in *status;
+ * a non-finite mean, activated scale or amplitude (after the fp32 cast) sets
+ * CGS_STATUS_NONFINITE_PARAMS. */
 int cgs_prepare(const double *params, int64_t n, float *splat, int32_t *status, void *stream);
 
 /* ---- K2: tile binning (build_tile_work, _kernels.py:17-63) ----------------
@@ -131,21 +140,30 @@ int cgs_raster_fwd(const float *splat, int64_t n, const double *poses, int32_t B
 
 /* ---- K3 (training path): binning-free render -------------------------------
  * Same image as cgs_raster_fwd without tile lists: one lane per (image,
- * Gaussian) walks its footprint and adds w (e - sub) into a shared-memory
- * image as int32 fixed point (scale 2^30 / sum of view-independent weight
- * bounds, so sums cannot overflow and the result is bitwise deterministic).
+ * Gaussian) walks its footprint and adds w e into a shared-memory image as
+ * int32 fixed point.  The Gaussians split into chunks (one CTA per chunk and
+ * image); a chunk's band uses its own scale 2^30 / (sum of its Gaussians'
+ * view-independent weight bounds), so band sums cannot overflow, and the band
+ * is added to the image in one image-wide unit (2^30 / sum over all
+ * Gaussians).  Each Gaussian walks q < 6.5^2 (splat.py:49) down to 2e-5 of its
+ * peak (the dropped tail bounds the render error near 1.2e-5 rel L2 at any N;
+ * the reference's -sub per pixel, 6.7e-10 of the peak, is below that).
+ * Integer sums make the result bitwise deterministic.
  * out f32 [B][D][D] natural layout (used as int32 scratch first); ws holds
- * cgs_render_workspace_bytes(n) bytes.  Replaces rasterize (splat.py:263-298)
- * inside the training step. */
+ * cgs_render_workspace_bytes(n) bytes.  clamp_count (nullable, device int64)
+ * is incremented by the number of (image, Gaussian) projections that hit the
+ * eigenvalue floor: CLAMP_EVENTS.count += proj.n_clamped per image
+ * (splat.py:276-277).  Replaces rasterize (splat.py:263-298) inside the
+ * training step. */
 size_t cgs_render_workspace_bytes(int64_t n);
 int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
-               void *ws, void *stream);
+               int64_t *clamp_count, void *ws, void *stream);
 /* cgs_render without the final conversion: out holds the int32 fixed-point
  * image; its scale (pixel value = int / scale) is the float at
  * ws + cgs_render_scale_offset(n) floats, for a consumer that converts on load
  * (cgs_ctf_mse_spectral). */
 int cgs_render_fixed(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, int32_t *out,
-                     void *ws, void *stream);
+                     int64_t *clamp_count, void *ws, void *stream);
 int64_t cgs_render_scale_offset(int64_t n);
 
 /* ---- K4: CTF, centred FFTs and MSE (optics.py:78-141, train.py:114-121,153)

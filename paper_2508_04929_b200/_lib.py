@@ -24,6 +24,7 @@ CGS_BIN_CHUNK = 2048
 CGS_STATUS_DEGENERATE_ROTATION = 1
 CGS_STATUS_BIN_OVERFLOW = 2
 CGS_STATUS_NONFINITE_LOSS = 4
+CGS_STATUS_NONFINITE_PARAMS = 8
 
 
 class CudaUnavailableError(RuntimeError):
@@ -54,6 +55,7 @@ PROTOTYPES = {
     "cgs_version": (ctypes.c_char_p, []),
     "cgs_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "cgs_last_error_detail": (ctypes.c_char_p, []),
+    "cgs_launch_state_entries": (I32, [I32]),
     "cgs_prepare": (ctypes.c_int, [P, I64, P, P, P]),
     "cgs_bin_segments": (I64, [I64]),
     "cgs_bin_tiles": (I64, [I32, I32]),
@@ -64,8 +66,8 @@ PROTOTYPES = {
     "cgs_bin_scatter": (ctypes.c_int, [P, I64, I32, I32, I32, P, P, I64, P, P]),
     "cgs_raster_fwd": (ctypes.c_int, [P, I64, P, I32, G, I32, P, P, I64, P, I32, P]),
     "cgs_render_workspace_bytes": (ctypes.c_size_t, [I64]),
-    "cgs_render": (ctypes.c_int, [P, I64, P, I32, G, P, P, P]),
-    "cgs_render_fixed": (ctypes.c_int, [P, I64, P, I32, G, P, P, P]),
+    "cgs_render": (ctypes.c_int, [P, I64, P, I32, G, P, P, P, P]),
+    "cgs_render_fixed": (ctypes.c_int, [P, I64, P, I32, G, P, P, P, P]),
     "cgs_render_scale_offset": (I64, [I64]),
     "cgs_ctf_evaluate": (ctypes.c_int, [P, I32, G, P, P]),
     "cgs_fft_plan_create": (ctypes.c_int, [I32, I32, ctypes.POINTER(ctypes.c_void_p)]),

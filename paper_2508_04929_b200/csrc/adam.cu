@@ -157,7 +157,7 @@ __global__ void epilogue_adam_kernel(const float *__restrict__ part, int G, int6
                                      double *__restrict__ v, int mode, double scale, double lr,
                                      double b1, double b2, double eps, double bc1, double bc2,
                                      const int32_t *__restrict__ skip, const double *__restrict__ hyper) {
-    if (skip && (*skip & (CGS_STATUS_BIN_OVERFLOW | CGS_STATUS_NONFINITE_LOSS))) return;
+    if (skip && (*skip & (CGS_STATUS_BIN_OVERFLOW | CGS_STATUS_NONFINITE_LOSS | CGS_STATUS_NONFINITE_PARAMS))) return;
     if (hyper) {  // device-resident (lr, bc1, bc2): one launch serves every step of a captured graph
         lr = hyper[0];
         bc1 = hyper[1];

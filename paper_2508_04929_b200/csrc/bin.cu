@@ -404,8 +404,8 @@ extern "C" int cgs_bin_scatter(const uint32_t *rects, int64_t n, int32_t B, int3
     int S = (int)cgs_bin_segments(n);
     size_t smem = (size_t)T * 9 * sizeof(int);
     cudaStream_t st = (cudaStream_t)stream;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rc = ensure_smem_limit((const void *)bin_scatter_kernel, smem, "bin_scatter_kernel");
+    if (rc) return rc;
     dim3 g(S, B);
     bin_scatter_kernel<<<g, 256, smem, st>>>(rects, n, ntx, T, S, offs, items, capacity, status);
     return check_launch("bin_scatter_kernel");

@@ -22,6 +22,10 @@ constexpr float kL2Cut = -21.125f * 1.4426950408889634f;
 
 void set_error_detail(const char *what, const char *detail);
 int check_launch(const char *what);
+// per-device dynamic shared-memory opt-in (cudaFuncSetAttribute) for func, checked
+int ensure_smem_limit(const void *func, size_t bytes, const char *what);
+// SMs x resident CTAs of func on the current device, memoised per (device, func)
+int resident_slots(const void *func, int threads, size_t smem, int *slots, const char *what);
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -125,6 +129,7 @@ struct Splat2 {
     float cnorm;           // 1 / (2 pi sqrt(det)) in normalised units
     float w;               // amp * cnorm
     float hx, hy;          // half-extents of the q < cutoff ellipse [px]
+    int clamped;           // 1 when the small eigenvalue hit the floor (CLAMP_EVENTS, splat.py:277)
 };
 
 // fast approximate rcp/sqrt (MUFU, ~1 ulp): the raster tolerances are 1e-4/1e-3
@@ -153,7 +158,8 @@ __device__ __forceinline__ Splat2 project2(const SplatRec &r, const PoseF &P, co
     float rad = sqrt_approx(hd * hd + c01 * c01);
     float l1 = mid + rad;
     float l2 = l1 > 0.f ? det * rcp_approx(l1) : 0.f;
-    if (l2 < kEigenFloorPx2) {
+    s.clamped = l2 < kEigenFloorPx2;
+    if (s.clamped) {
         // floor the small eigenvalue, keep the eigenvector (splat.py:245-259)
         float a1 = fmaxf(l1, kEigenFloorPx2), a2 = kEigenFloorPx2;
         float vx = c01, vy = l1 - c00;
@@ -314,6 +320,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // order this thread's prior generic-proxy shared accesses before async-proxy writes
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// A step whose parameters were non-finite (cgs_prepare sets CGS_STATUS_NONFINITE_PARAMS)
+// reports a NaN loss, as the reference's fp64 render of such a mixture would
+// (train.py:146-149 -> DivergenceError); the loss kernels pass each image's
+// loss through this before they store it.
+__device__ __forceinline__ double poison_loss(double l, const int32_t *status) {
+    if (status && (*(volatile const int32_t *)status & CGS_STATUS_NONFINITE_PARAMS)) return __longlong_as_double(0x7ff8000000000000ll);
+    return l;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -1,6 +1,8 @@
 // Error reporting and version strings of the C ABI.
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -19,7 +21,85 @@ int check_launch(const char *what) {
     return CGS_ERR_CUDA;
 }
 
+// Per-device launch state.  A process may drive several GPUs (e.g. the two
+// gold-standard halves of evaluate.py:182-200 on two device groups), so the
+// dynamic shared-memory opt-in and the occupancy memo are keyed by
+// (device ordinal, kernel) instead of one process-wide static.
+namespace {
+struct FuncState {
+    int dev;
+    const void *func;
+    size_t smem_limit;   // largest opt-in set so far
+    size_t slots_smem;   // smem of the memoised slot count
+    int threads;
+    int slots;
+};
+std::mutex g_state_mu;
+std::vector<FuncState> g_state;
+
+FuncState &state_for(int dev, const void *func) {
+    for (auto &s : g_state)
+        if (s.dev == dev && s.func == func) return s;
+    g_state.push_back(FuncState{dev, func, 0, 0, 0, 0});
+    return g_state.back();
+}
+}  // namespace
+
+int ensure_smem_limit(const void *func, size_t bytes, const char *what) {
+    if (bytes <= 48 * 1024) return CGS_OK;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        set_error_detail(what, cudaGetErrorString(e));
+        return CGS_ERR_CUDA;
+    }
+    std::lock_guard<std::mutex> lock(g_state_mu);
+    FuncState &s = state_for(dev, func);
+    if (bytes <= s.smem_limit) return CGS_OK;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) {
+        set_error_detail(what, cudaGetErrorString(e));
+        return CGS_ERR_CUDA;
+    }
+    s.smem_limit = bytes;
+    return CGS_OK;
+}
+
+int resident_slots(const void *func, int threads, size_t smem, int *slots, const char *what) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        set_error_detail(what, cudaGetErrorString(e));
+        return CGS_ERR_CUDA;
+    }
+    std::lock_guard<std::mutex> lock(g_state_mu);
+    FuncState &s = state_for(dev, func);
+    if (s.slots > 0 && s.slots_smem == smem && s.threads == threads) {
+        *slots = s.slots;
+        return CGS_OK;
+    }
+    int sms = 0, per_sm = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem);
+    if (e != cudaSuccess) {
+        set_error_detail(what, cudaGetErrorString(e));
+        return CGS_ERR_CUDA;
+    }
+    s.slots = sms * (per_sm > 0 ? per_sm : 1);
+    s.slots_smem = smem;
+    s.threads = threads;
+    *slots = s.slots;
+    return CGS_OK;
+}
+
 }  // namespace cgs
+
+extern "C" int32_t cgs_launch_state_entries(int32_t device) {
+    std::lock_guard<std::mutex> lock(cgs::g_state_mu);
+    int32_t k = 0;
+    for (const auto &s : cgs::g_state) k += s.dev == device;
+    return k;
+}
 
 extern "C" const char *cgs_version(void) { return "cgs_b200 0.1.0 sm_100a"; }
 

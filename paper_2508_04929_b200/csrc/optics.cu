@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(1024) loss_resid_kernel(const float *__restric
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
-        double l = t / (double)npix;
+        double l = poison_loss(t / (double)npix, status);
         loss[b] = l;
         if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
     }
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ctf_mse_fused_kernel(
     a1 = block_sum_f64(a1, scratch);
     a2 = block_sum_f64(a2, scratch);
     if (threadIdx.x == 0) {
-        const double l1 = a1 / (double)(D * D), l2 = a2 / (double)(D * D);
+        const double l1 = poison_loss(a1 / (double)(D * D), status), l2 = poison_loss(a2 / (double)(D * D), status);
         loss[b0] = l1;
         if (two) loss[b0 + 1] = l2;
         if (status && (!isfinite(l1) || (two && !isfinite(l2)))) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
@@ -577,11 +577,8 @@ static int launch_fourier_filter(const float *in, float *out, int B, double pix,
                                  const double *shifts, cudaStream_t st) {
     constexpr int D = 32 * R;
     const size_t smem = (size_t)D * (D + 1) * sizeof(float2);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(fourier_filter_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    const int rc = ensure_smem_limit((const void *)fourier_filter_kernel<R>, smem, "fourier_filter_kernel");
+    if (rc) return rc;
     fourier_filter_kernel<R><<<(B + 1) / 2, kFusedThreads, smem, st>>>(in, out, B, pix, ctf, shifts);
     return check_launch("fourier_filter_kernel");
 }
@@ -776,7 +773,7 @@ __global__ void __launch_bounds__(kR2cThreads, 2) ctf_mse_r2c_kernel(
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < kR2cThreads / 32; ++w) t += scratch[w];
-        const double l = t / (double)(D * D);
+        const double l = poison_loss(t / (double)(D * D), status);
         loss[b] = l;
         if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
     }
@@ -898,7 +895,7 @@ __global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kerne
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < kR2cThreads / 32; ++w) t += scratch[w];
-        const double l = t / ((double)D * D * (double)D * D);
+        const double l = poison_loss(t / ((double)D * D * (double)D * D), status);
         loss[b] = l;
         if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
     }
@@ -924,11 +921,8 @@ static int launch_obs_spectrum(const float *obs, const double *ctf, double pix, 
                                cudaStream_t st) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     const size_t smem = (size_t)D * P * sizeof(float2);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(obs_spectrum_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    const int rc = ensure_smem_limit((const void *)obs_spectrum_kernel<R>, smem, "obs_spectrum_kernel");
+    if (rc) return rc;
     obs_spectrum_kernel<R><<<B, kR2cThreads, smem, st>>>(obs, ctf, pix, reinterpret_cast<float2 *>(spec));
     return check_launch("obs_spectrum_kernel");
 }
@@ -938,12 +932,8 @@ static int launch_ctf_mse_spec_t(const float *render, const float *render_scale,
                                  float *upstream, double *loss, int32_t *status, cudaStream_t st) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     const size_t smem = (size_t)D * P * sizeof(float2);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(ctf_mse_spec_kernel<R, kFixed, kRowPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        configured = true;
-    }
+    const int rc = ensure_smem_limit((const void *)ctf_mse_spec_kernel<R, kFixed, kRowPair>, smem, "ctf_mse_spec_kernel");
+    if (rc) return rc;
     ctf_mse_spec_kernel<R, kFixed, kRowPair><<<B, kR2cThreads, smem, st>>>(
         render, render_scale, reinterpret_cast<const float2 *>(spec), upstream, loss, status);
     return check_launch("ctf_mse_spec_kernel");
@@ -964,11 +954,8 @@ static int launch_ctf_mse_r2c(const float *render, const float *obs, int B, doub
                               float *model, float *upstream, double *loss, int32_t *status, cudaStream_t st) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     const size_t smem = (size_t)D * P * (sizeof(float2) + sizeof(float));
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(ctf_mse_r2c_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    const int rc = ensure_smem_limit((const void *)ctf_mse_r2c_kernel<R>, smem, "ctf_mse_r2c_kernel");
+    if (rc) return rc;
     ctf_mse_r2c_kernel<R><<<B, kR2cThreads, smem, st>>>(render, obs, ctf, pix, model, upstream, loss, status);
     return check_launch("ctf_mse_r2c_kernel");
 }
@@ -978,11 +965,8 @@ static int launch_ctf_mse_fused(const float *render, const float *obs, int B, do
                                 float *model, float *upstream, double *loss, int32_t *status, cudaStream_t st) {
     constexpr int D = 32 * R;
     const size_t smem = (size_t)D * (D + 1) * sizeof(float2);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(ctf_mse_fused_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    const int rc = ensure_smem_limit((const void *)ctf_mse_fused_kernel<R>, smem, "ctf_mse_fused_kernel");
+    if (rc) return rc;
     ctf_mse_fused_kernel<R><<<(B + 1) / 2, kFusedThreads, smem, st>>>(render, obs, B, pix, ctf, model, upstream,
                                                                       loss, status);
     return check_launch("ctf_mse_fused_kernel");

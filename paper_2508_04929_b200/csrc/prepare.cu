@@ -36,8 +36,11 @@ __global__ void __launch_bounds__(256) prepare_kernel(const double *__restrict__
     o[0] = make_float4((float)p[0], (float)p[1], (float)p[2], (float)amp);
     o[1] = make_float4((float)(R[0] * s0), (float)(R[1] * s1), (float)(R[2] * s2), (float)(R[3] * s0));
     o[2] = make_float4((float)(R[4] * s1), (float)(R[5] * s2), (float)(R[6] * s0), (float)(R[7] * s1));
-    // slots 13-15 carry the activated scales for cgs_render's weight bound
-    o[3] = make_float4((float)(R[8] * s2), (float)s0, (float)s1, (float)s2);
+    // slots 14 / 15 carry the smallest and middle activated scale for cgs_render's weight bound
+    const double lo = fmin(s0, fmin(s1, s2)), hi = fmax(s0, fmax(s1, s2));
+    o[3] = make_float4((float)(R[8] * s2), (float)hi, (float)lo, (float)(s0 + s1 + s2 - lo - hi));
+    const float chk = (float)p[0] + (float)p[1] + (float)p[2] + (float)amp + (float)s0 + (float)s1 + (float)s2;
+    if (!isfinite(chk)) atomicOr(status, CGS_STATUS_NONFINITE_PARAMS);
 }
 
 }  // namespace cgs

@@ -623,11 +623,8 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
     const size_t db_bytes = (2 * (size_t)D * D + kRowPad) * sizeof(float);
     const bool aligned = ((reinterpret_cast<uintptr_t>(upstream) & 15) == 0) && ((D * D) % 4 == 0);
     if (layout == CGS_LAYOUT_NATURAL && variant == 1 && db_bytes <= (size_t)kDBMaxBytes && aligned) {
-        static size_t configured = 0;
-        if (db_bytes > 48 * 1024 && db_bytes > configured) {
-            cudaFuncSetAttribute(raster_bwd_db_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)db_bytes);
-            configured = db_bytes;
-        }
+        const int rc = ensure_smem_limit((const void *)raster_bwd_db_kernel, db_bytes, "raster_bwd_db_kernel");
+        if (rc) return rc;
         dim3 g((unsigned)((n + kBwdThreadsDB - 1) / kBwdThreadsDB), (unsigned)G);
         raster_bwd_db_kernel<<<g, kBwdThreadsDB, db_bytes, st>>>(splat, n, poses, B, make_grid_f(grid), upstream,
                                                                  partial, images_per_group);
@@ -637,11 +634,8 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
     if (HB < 1) return CGS_ERR_UNSUPPORTED;
     HB = HB > D ? D : HB;
     const size_t smem = ((size_t)HB * D + kRowPad) * sizeof(float);
-    static size_t configured_band = 0;
-    if (smem > 48 * 1024 && smem > configured_band) {
-        cudaFuncSetAttribute(raster_bwd_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured_band = smem;
-    }
+    const int rc = ensure_smem_limit((const void *)raster_bwd_band_kernel, smem, "raster_bwd_band_kernel");
+    if (rc) return rc;
     dim3 g((unsigned)((n + kBwdThreadsBand - 1) / kBwdThreadsBand), (unsigned)G);
     raster_bwd_band_kernel<<<g, kBwdThreadsBand, smem, st>>>(splat, n, poses, B, make_grid_f(grid), upstream, layout,
                                                              partial, images_per_group, HB);

@@ -224,11 +224,8 @@ extern "C" int cgs_raster_fwd(const float *splat, int64_t n, const double *poses
             break;
         default: {
             const size_t smem = (size_t)kSHalves * kST * kST * sizeof(float) + kSThreads * sizeof(ScatItem);
-            static bool configured = false;
-            if (!configured) {
-                cudaFuncSetAttribute(raster_fwd_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                configured = true;
-            }
+            const int rc = ensure_smem_limit((const void *)raster_fwd_scatter_kernel, smem, "raster_fwd_scatter_kernel");
+            if (rc) return rc;
             raster_fwd_scatter_kernel<<<g, kSThreads, smem, st>>>(splat, poses, G, ntx, T, S, items, offs, capacity,
                                                                   out, layout);
             break;

@@ -5,16 +5,32 @@
 // (build_tile_work + forward_tiles, _kernels.py:17-125).  On B200 the faster
 // schedule for ~1 px footprints is Gaussian-major, like the backward: one
 // lane per (image, Gaussian) walks its own footprint along the exact
-// q < 6.5^2 row spans and adds w (e - sub) into a shared-memory image.  Lanes
-// of a warp hit unrelated pixels, so the adds must be atomic; shared-memory
-// float atomics are CAS loops on sm_100a (3 updates/clk/SM measured), native
-// int32 ATOMS.ADD sustain ~10/clk/SM at random addresses
+// q < 6.5^2 row spans and adds w e into a shared-memory image.  Lanes of a
+// warp hit unrelated pixels, so the adds must be atomic; shared-memory float
+// atomics are CAS loops on sm_100a (3 updates/clk/SM measured), native int32
+// ATOMS.ADD sustain ~10/clk/SM at random addresses
 // (profiles/microbench_smem_atomics_r01.txt).  Values are therefore added as
-// round-to-nearest int32 fixed point with one scale per step:
-//   scale = 2^30 / sum_g wb_g,   wb_g >= w_g(b) for every view b,
-// so no pixel sum can overflow, and integer addition makes the render
-// bitwise reproducible regardless of scheduling.  One ulp is sum wb / 2^30,
-// ~1e-6 of the image's total peak weight (render tolerance is 1e-4 rel L2).
+// round-to-nearest int32 fixed point.
+//
+// Scales.  The Gaussians split into chunks; a CTA accumulates one chunk of
+// one image into a shared-memory band in the chunk's own unit
+//   scale_c = min(2^30 / sum_{g in c} wb_g, 2^22 / max_{g in c} wb_g),
+// wb_g >= w_g(b) for every view b, so no band sum can overflow and no single
+// contribution reaches 2^22.  At the end the band is added to the global
+// image in the image-wide unit S = min(2^30 / sum_g wb_g, ...) <= scale_c
+// (round(v S / scale_c), one rounding per pixel and chunk), where no pixel
+// can overflow either.  Integer addition makes the render bitwise
+// reproducible whatever the scheduling.
+//
+// Precision (round 2).  Round 1 rounded every contribution in the global unit
+// S, so a Gaussian's peak was only ~2^30 / N units and its tail below
+// 0.5 / peak rounded away: the render error grew linearly with N (1.35e-5 rel
+// L2 at 50k, 3.1e-4 at 1M).  With per-chunk units a chunk of <= 8192
+// Gaussians keeps >= 2^30 / 8192 units per peak at any N, and the walk is cut
+// at a fixed fraction of each Gaussian's own peak, kTailFrac = 2e-5: the
+// dropped tail carries kTailFrac of the Gaussian's mass (a 2-D Gaussian
+// holds a fraction t of its mass where e < t), which bounds the image error
+// near 0.6 kTailFrac = 1.2e-5 rel L2 for every N (profiles/parity_margins_r02.tsv).
 //
 // wb_g: by eigenvalue interlacing the projected 2x2 covariance has
 // lambda1 >= s_mid^2 and lambda2 >= s_min^2; with the eigenvalue floor
@@ -23,8 +39,7 @@
 //
 // Along a row, e = exp(-q/2) follows e_{k+1} = e_k g_k, g_{k+1} = g_k c with
 // c = 2^(2A): two FMULs per pixel instead of an MUFU.EX2, restarted every 32
-// pixels so the recurrence error stays below 2e-5.  Rounding to int uses the
-// FMA-pipe magic-number trick (common.cuh fast_rint) instead of F2I on the XU.
+// pixels so the recurrence error stays below 2e-5.
 #include <algorithm>
 #include <cmath>
 
@@ -48,55 +63,94 @@ constexpr int kRChunkMin = 512;
 #define CGS_FWD_BAND_KB 64
 #endif
 constexpr int kRBandBytes = CGS_FWD_BAND_KB * 1024;  // int32 accumulator rows per CTA
-constexpr int kWbBlock = 1024;
-constexpr float kFixedRange = 1073741824.f;  // 2^30
-constexpr float kContribRange = 4194304.f;   // 2^22
+constexpr int kWbThreads = 1024;
+constexpr double kFixedRange = 1073741824.0;  // 2^30
+constexpr double kContribRange = 4194304.0;   // 2^22
+#ifndef CGS_FWD_TAIL
+#define CGS_FWD_TAIL 2e-5f
+#endif
+constexpr float kTailFrac = CGS_FWD_TAIL;      // walk each footprint down to this fraction of its peak
 
-__global__ void __launch_bounds__(kWbBlock) wbound_partial_kernel(const float *__restrict__ splat, int64_t n,
-                                                                  double h, float *__restrict__ part) {
-    const int64_t g = blockIdx.x * (int64_t)kWbBlock + threadIdx.x;
-    float wb = 0.f;
-    if (g < n) {
-        const float *r = splat + g * CGS_SPLAT_STRIDE;
-        const double s0 = r[13], s1 = r[14], s2 = r[15], amp = r[3];
-        const double lo = fmin(s0, fmin(s1, s2)), hi = fmax(s0, fmax(s1, s2));
-        const double mid = s0 + s1 + s2 - lo - hi;
-        const double fl = (0.1 * h) * (0.1 * h);
-        const double det = fmax(mid * mid, fl) * fmax(lo * lo, fl);
-        // 1.001: headroom for the fp32 evaluation of w inside the kernels
-        wb = (float)(1.001 * amp / (2.0 * kPiD * sqrt(det)));
+// View-independent peak-weight bound of one Gaussian (see the header); slots
+// 14 / 15 of the splat record hold the smallest and middle activated scale
+// (cgs_prepare).
+__device__ __forceinline__ double weight_bound(const float *__restrict__ splat, int64_t g, double fl) {
+    const float *r = splat + g * CGS_SPLAT_STRIDE;
+    const float2 lm = __ldg(reinterpret_cast<const float2 *>(r + 14));
+    const double lo = lm.x, mid = lm.y, amp = __ldg(r + 3);
+    const double det = fmax(mid * mid, fl) * fmax(lo * lo, fl);
+    // 1.001: headroom for the fp32 evaluation of w inside the kernels
+    return 1.001 * amp / (2.0 * kPiD * sqrt(det));
+}
+
+// One CTA per chunk: sum and max of wb over the chunk's Gaussians, in the
+// chunk's scrambled order g = (i * A) mod n, i in [c chunk, (c+1) chunk),
+// stepped incrementally like the raster kernel.  Fixed-order reduction: the
+// scales are deterministic.
+__global__ void __launch_bounds__(kWbThreads) wbound_chunk_kernel(const float *__restrict__ splat, int64_t n,
+                                                                  double h, int64_t mulA, int chunk,
+                                                                  double *__restrict__ csum,
+                                                                  float *__restrict__ cmax) {
+    const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+    const double fl = (0.1 * h) * (0.1 * h);
+    const int64_t stepA = (kWbThreads * mulA) % n;
+    int64_t g = ((i0 + threadIdx.x) % n) * mulA % n;
+    double t = 0.0;
+    float m = 0.f;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += kWbThreads) {
+        const double wb = weight_bound(splat, g, fl);
+        g += stepA;
+        if (g >= n) g -= n;
+        t += wb;
+        m = fmaxf(m, (float)wb);
     }
-    __shared__ float ws[kWbBlock / 32], wm[kWbBlock / 32];
-    float v = warp_sum(wb), m = wb;
+    __shared__ double ws[kWbThreads / 32];
+    __shared__ float wm[kWbThreads / 32];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
     if ((threadIdx.x & 31) == 0) {
-        ws[threadIdx.x >> 5] = v;
+        ws[threadIdx.x >> 5] = t;
         wm[threadIdx.x >> 5] = m;
     }
     __syncthreads();
     if (threadIdx.x < 32) {
-        float t = warp_sum(ws[threadIdx.x]), mm = wm[threadIdx.x];
+        double s = threadIdx.x < kWbThreads / 32 ? ws[threadIdx.x] : 0.0;
+        float mx = threadIdx.x < kWbThreads / 32 ? wm[threadIdx.x] : 0.f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+        for (int o = 16; o > 0; o >>= 1) {
+            s += __shfl_xor_sync(0xffffffffu, s, o);
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
         if (threadIdx.x == 0) {
-            part[blockIdx.x] = t;
-            part[gridDim.x + blockIdx.x] = mm;
+            csum[blockIdx.x] = s;
+            cmax[blockIdx.x] = mx;
         }
     }
 }
 
-// scale = min(2^30 / sum wb, 2^22 / max wb) -> part[2 nparts]; fixed-order
-// reduction.  The first bound keeps every pixel sum below 2^30; the second
-// keeps every single contribution below 2^22, where fast_rint is exact.
-__global__ void __launch_bounds__(256) wbound_scale_kernel(float *part, int nparts) {
+__device__ __forceinline__ double unit_scale(double sum, double mx) {
+    double sc = sum > 0.0 ? kFixedRange / sum : 1.0;
+    if (mx > 0.0) sc = fmin(sc, kContribRange / mx);
+    return sc;
+}
+
+// Image-wide unit S from all chunks (fixed order), then per chunk its own unit
+// scale_c >= S and the band -> image factor S / scale_c <= 1.
+__global__ void __launch_bounds__(256) wbound_scale_kernel(const double *__restrict__ csum,
+                                                           const float *__restrict__ cmax, int nch,
+                                                           float *__restrict__ gscale, float *__restrict__ cscale,
+                                                           float *__restrict__ cratio) {
     __shared__ double ws[8];
     __shared__ float wm[8];
+    __shared__ float S;
     double t = 0.0;
     float m = 0.f;
-    for (int i = threadIdx.x; i < nparts; i += 256) {
-        t += part[i];
-        m = fmaxf(m, part[nparts + i]);
+    for (int i = threadIdx.x; i < nch; i += 256) {
+        t += csum[i];
+        m = fmaxf(m, cmax[i]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -115,9 +169,15 @@ __global__ void __launch_bounds__(256) wbound_scale_kernel(float *part, int npar
             s += ws[w];
             mx = fmaxf(mx, wm[w]);
         }
-        double sc = s > 0.0 ? (double)kFixedRange / s : 1.0;
-        if (mx > 0.f) sc = fmin(sc, (double)kContribRange / mx);
-        part[2 * nparts] = (float)sc;
+        S = (float)unit_scale(s, mx);
+        *gscale = S;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nch; c += 256) {
+        // scale_c >= S by construction (a chunk's sum and max are <= the image's); fmaxf guards rounding
+        const float sc = fmaxf((float)unit_scale(csum[c], cmax[c]), S);
+        cscale[c] = sc;
+        cratio[c] = S / sc;
     }
 }
 
@@ -185,16 +245,18 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
     }
 }
 
-// CTA = (chunk of kRChunk Gaussians, image, band of rows); the band's int32
-// accumulator (whole 128^2 image in 64 KB) lives in shared memory and is
-// added to the global image once at the end.  Lanes of a warp must hit
-// unrelated pixels to keep ATOMS conflicts rare, but the device order of the
-// Gaussians is spatial (Morton, chosen for the backward's region staging), so
-// the chunk visits Gaussians in a scrambled order: logical index i maps to
-// g = (i * A) mod n with gcd(A, n) = 1, stepped incrementally.
+// CTA = (chunk of Gaussians, image, band of rows); the band's int32
+// accumulator (whole 128^2 image in 64 KB) lives in shared memory, in the
+// chunk's unit, and is added to the global image (image-wide unit) once at
+// the end.  Lanes of a warp must hit unrelated pixels to keep ATOMS conflicts
+// rare, but the device order of the Gaussians is spatial (Morton, chosen for
+// the backward's region staging), so the chunk visits Gaussians in a
+// scrambled order: logical index i maps to g = (i * A) mod n with
+// gcd(A, n) = 1, stepped incrementally.
 __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, GridF G,
-    const float *__restrict__ scale_ptr, int HB, int64_t mulA, int chunk, int *__restrict__ out) {
+    const float *__restrict__ cscale, const float *__restrict__ cratio, int HB, int64_t mulA, int chunk,
+    unsigned long long *__restrict__ clamp_count, int *__restrict__ out) {
     extern __shared__ int band[];
     const int D = G.D;
     // the row stride as an opaque register value, so it is not re-read from the
@@ -205,24 +267,25 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     const int r0 = blockIdx.z * HB, r1 = min(D, r0 + HB);
     const int npx = (r1 - r0) * D;
     for (int i = threadIdx.x; i < npx; i += kRThreads) band[i] = 0;
-    const float scale = *scale_ptr;
+    const float scale = cscale[blockIdx.x];
     const PoseF P = load_pose_f(poses, b);
     const int64_t i_begin = (int64_t)blockIdx.x * chunk;
     const int64_t i_end = min(n, i_begin + chunk);
     const int64_t stepA = (kRThreads * mulA) % n;
     int64_t g = ((i_begin + threadIdx.x) % n) * mulA % n;
+    int nclamp = 0;
     __syncthreads();
     for (int64_t i = i_begin + threadIdx.x; i < i_end; i += kRThreads) {
         const Splat2 s = project2(load_splat(splat, g), P, G);
         g += stepA;
         if (g >= n) g -= n;
+        nclamp += s.clamped;
         if (!(s.w > 0.f)) continue;
-        // Contribution-exact footprint: a pixel adds round(wS e) units, which is
-        // 0 wherever e < 0.5 / wS.  Walk only q < cut with e(cut) = 0.4995 / wS
-        // (the 1e-3 margin keeps every pixel that can round to >= 1 unit) and
-        // q < 6.5^2: the same integer image as the whole culled ellipse, far
-        // fewer updates.
-        const float thr = fmaxf(0.4995f * rcp_approx(s.w * scale), kSub);  // >= sub: no denormals
+        // Walk q < cut: e(cut) is the larger of kTailFrac (the precision cut,
+        // see the header) and 0.4995 / (w scale), below which a pixel rounds
+        // to 0 units anyway (the 1e-3 margin keeps every pixel that can round
+        // to >= 1 unit), and q < 6.5^2 (splat.py:49).
+        const float thr = fmaxf(0.4995f * rcp_approx(s.w * scale), kTailFrac);
         if (!(thr < 1.f)) continue;
         const float cut = fminf(kCutoffSq, -2.f * kLn2 * lg2_approx(thr));
         const float hy = s.hy * sqrt_approx(cut * (1.f / kCutoffSq));
@@ -235,11 +298,16 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
         else
             fwd_rows_band<false>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
     }
+    if (clamp_count && blockIdx.z == 0) {  // every (image, Gaussian) projection counted once
+        nclamp = __reduce_add_sync(0xffffffffu, nclamp);
+        if ((threadIdx.x & 31) == 0 && nclamp) atomicAdd(clamp_count, (unsigned long long)nclamp);
+    }
     __syncthreads();
+    const float ratio = cratio[blockIdx.x];
     int *dst = out + (int64_t)b * D * D + (int64_t)r0 * D;
     for (int i = threadIdx.x; i < npx; i += kRThreads) {
         const int v = band[i];
-        if (v) atomicAdd(dst + i, v);
+        if (v) atomicAdd(dst + i, __float2int_rn((float)v * ratio));
     }
 }
 
@@ -288,65 +356,68 @@ static int64_t fwd_chunks(int64_t n, int64_t ctas_per_chunk, int slots) {
     return best;
 }
 
+// Workspace: [0] image-wide scale (float), [1] pad, then csum f64 [mc], then
+// cmax, cscale, cratio f32 [mc] each; mc = the most chunks any split uses.
+static int64_t max_chunks(int64_t n) { return (n + kRChunkMin - 1) / kRChunkMin; }
+
 extern "C" size_t cgs_render_workspace_bytes(int64_t n) {
-    int64_t parts = (n + kWbBlock - 1) / kWbBlock;
-    return (size_t)(2 * parts + 1) * sizeof(float);
+    const int64_t mc = max_chunks(n);
+    return (size_t)(8 + 8 * mc + 3 * 4 * mc);
 }
 
 static int render_impl(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
-                          void *ws, void *stream, bool convert) {
+                       int64_t *clamp_count, void *ws, void *stream, bool convert) {
     if (n <= 0 || B <= 0 || grid.size < 1 || !splat || !poses || !out || !ws) return CGS_ERR_ARG;
     const int D = grid.size;
     cudaStream_t st = (cudaStream_t)stream;
-    const int parts = (int)((n + kWbBlock - 1) / kWbBlock);
-    float *part = (float *)ws;
     const double h = 2.0 * grid.extent / grid.size;
-    wbound_partial_kernel<<<parts, kWbBlock, 0, st>>>(splat, n, h, part);
-    wbound_scale_kernel<<<1, 256, 0, st>>>(part, parts);
     int HB = kRBandBytes / (D * (int)sizeof(int));
     if (HB < 1) return CGS_ERR_UNSUPPORTED;
     HB = HB > D ? D : HB;
     const int bands = (D + HB - 1) / HB;
     const size_t smem = (size_t)HB * D * sizeof(int);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(raster_fwd_atomic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
-    const int64_t count = (int64_t)B * D * D;
-    cudaMemsetAsync(out, 0, sizeof(int) * count, st);
-    thread_local int slots = 0;
-    thread_local size_t slots_smem = 0;
-    if (slots == 0 || slots_smem != smem) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_atomic_kernel, kRThreads, smem);
-        slots = std::max(1, sms * per_sm);
-        slots_smem = smem;
-    }
+    int rc = ensure_smem_limit((const void *)raster_fwd_atomic_kernel, smem, "raster_fwd_atomic_kernel");
+    if (rc) return rc;
+    int slots = 0;
+    rc = resident_slots((const void *)raster_fwd_atomic_kernel, kRThreads, smem, &slots, "raster_fwd_atomic_kernel");
+    if (rc) return rc;
     int64_t nchunks = fwd_chunks(n, (int64_t)B * bands, slots);
     const int chunk = (int)((n + nchunks - 1) / nchunks);
     nchunks = (n + chunk - 1) / chunk;
+    const int64_t mulA = scramble_multiplier(n);
+    const int64_t mc = max_chunks(n);
+    float *gscale = (float *)ws;
+    double *csum = (double *)((char *)ws + 8);
+    float *cmax = (float *)(csum + mc), *cscale = cmax + mc, *cratio = cscale + mc;
+    wbound_chunk_kernel<<<(unsigned)nchunks, kWbThreads, 0, st>>>(splat, n, h, mulA, chunk, csum, cmax);
+    wbound_scale_kernel<<<1, 256, 0, st>>>(csum, cmax, (int)nchunks, gscale, cscale, cratio);
+    const int64_t count = (int64_t)B * D * D;
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int) * count, st);
+    if (e != cudaSuccess) {
+        set_error_detail("cgs_render memset", cudaGetErrorString(e));
+        return CGS_ERR_CUDA;
+    }
     dim3 g((unsigned)nchunks, (unsigned)B, (unsigned)bands);
-    raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), part + 2 * parts, HB,
-                                                         scramble_multiplier(n), chunk, reinterpret_cast<int *>(out));
-    int rc = check_launch("raster_fwd_atomic_kernel");
+    raster_fwd_atomic_kernel<<<g, kRThreads, smem, st>>>(splat, n, poses, make_grid_f(grid), cscale, cratio, HB,
+                                                         mulA, chunk,
+                                                         reinterpret_cast<unsigned long long *>(clamp_count),
+                                                         reinterpret_cast<int *>(out));
+    rc = check_launch("raster_fwd_atomic_kernel");
     if (rc || !convert) return rc;
     const int64_t threads = (count + 3) / 4;
     fixed_to_float_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(reinterpret_cast<int *>(out), count,
-                                                                           part + 2 * parts);
+                                                                           gscale);
     return check_launch("fixed_to_float_kernel");
 }
 
 extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
-                          void *ws, void *stream) {
-    return render_impl(splat, n, poses, B, grid, out, ws, stream, true);
+                          int64_t *clamp_count, void *ws, void *stream) {
+    return render_impl(splat, n, poses, B, grid, out, clamp_count, ws, stream, true);
 }
 
 extern "C" int cgs_render_fixed(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
-                                int32_t *out, void *ws, void *stream) {
-    return render_impl(splat, n, poses, B, grid, reinterpret_cast<float *>(out), ws, stream, false);
+                                int32_t *out, int64_t *clamp_count, void *ws, void *stream) {
+    return render_impl(splat, n, poses, B, grid, reinterpret_cast<float *>(out), clamp_count, ws, stream, false);
 }
 
-extern "C" int64_t cgs_render_scale_offset(int64_t n) { return 2 * ((n + kWbBlock - 1) / kWbBlock); }
+extern "C" int64_t cgs_render_scale_offset(int64_t) { return 0; }

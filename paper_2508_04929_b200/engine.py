@@ -171,10 +171,12 @@ def raster_fwd(ctx, splat, n, poses, grid_s, binning: Binning, out, layout=_lib.
     return out
 
 
-def render_direct(ctx, splat, n, poses, grid_s, out):
-    """K3 binning-free render (cgs_render): images f32 [B][D][D], natural layout."""
+def render_direct(ctx, splat, n, poses, grid_s, out, clamp=None):
+    """K3 binning-free render (cgs_render): images f32 [B][D][D], natural layout; ``clamp`` (device
+    int64 [1], optional) accumulates the eigenvalue-floor clamp count."""
     ws = ctx.buf("render_ws", ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, torch.float32)
-    _lib.call("cgs_render", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, _ptr(out), _ptr(ws), ctx.stream)
+    _lib.call("cgs_render", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, _ptr(out), _ptr(clamp), _ptr(ws),
+              ctx.stream)
     return out
 
 
@@ -273,6 +275,11 @@ class StepPipeline:
         D = self.D
         self.splat = torch.empty(n * 16, dtype=torch.float32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        # eigenvalue-floor clamps of every render, folded into CLAMP_EVENTS when it is read
+        self.clamp = torch.zeros(1, dtype=torch.int64, device=dev)
+        from .render import CLAMP_EVENTS
+
+        CLAMP_EVENTS.track(self.clamp)
         self.render = torch.empty((self.B, D, D), dtype=torch.float32, device=dev)
         self.upstream = torch.empty((self.B, D, D), dtype=torch.float32, device=dev)
         self.spectrum = torch.empty(2 * int(ctx.lib.cgs_fft_spectrum_elems(D, self.B)), dtype=torch.float32, device=dev)
@@ -386,10 +393,10 @@ class StepPipeline:
         self._render_fixed = fixed
         if fixed:
             _lib.call("cgs_render_fixed", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid,
-                      _ptr(self.render), _ptr(self.render_ws), s)
+                      _ptr(self.render), _ptr(self.clamp), _ptr(self.render_ws), s)
         elif self.render_mode == "direct":
             _lib.call("cgs_render", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid, _ptr(self.render),
-                      _ptr(self.render_ws), s)
+                      _ptr(self.clamp), _ptr(self.render_ws), s)
         else:
             self._count(params, poses)
             _lib.call("cgs_bin_scatter", _ptr(self.rects), self.n, self.B, self.D, self.tile, _ptr(self.offs),
@@ -453,7 +460,7 @@ class StepPipeline:
         self._prepare(params)
         self._render_fixed = False
         _lib.call("cgs_render", _ptr(self.splat), self.n, _ptr(poses), poses.shape[0], self.grid, _ptr(self.render),
-                  _ptr(self.render_ws), self.ctx.stream)
+                  _ptr(self.clamp), _ptr(self.render_ws), self.ctx.stream)
         return self.render
 
     def degenerate(self) -> bool:

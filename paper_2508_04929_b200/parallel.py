@@ -22,7 +22,7 @@ def shard(indices, rank: int, world: int) -> np.ndarray:
 
 
 # status bits that make the Adam epilogue skip a step (cgs_b200.h)
-SKIP_BITS = 2 | 4  # CGS_STATUS_BIN_OVERFLOW | CGS_STATUS_NONFINITE_LOSS
+SKIP_BITS = 2 | 4 | 8  # CGS_STATUS_BIN_OVERFLOW | CGS_STATUS_NONFINITE_LOSS | CGS_STATUS_NONFINITE_PARAMS
 
 
 def allreduce_accumulator(acc, group=None, status=None):

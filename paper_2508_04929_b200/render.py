@@ -33,10 +33,44 @@ DEFAULT_TILE_SIZE = 16
 
 
 class ClampCounter:
-    """Running count of Gaussians that hit the 2D eigenvalue floor (splat.py:60-70)."""
+    """Running count of Gaussians that hit the 2D eigenvalue floor (splat.py:60-70).
+
+    The reference adds each rasterize's clamp count on the host (splat.py:276-277).
+    Here the training step's render (K3, cgs_render) adds it into a device int64
+    counter with no host sync; ``track`` registers such a counter and reading
+    ``count`` folds every tracked counter into the host total (one device read per
+    counter), so ``CLAMP_EVENTS.count`` means what it means in the reference."""
 
     def __init__(self):
-        self.count = 0
+        self._host = 0
+        self._pending = []  # device int64 [1] counters (strong references: a count outlives its pipeline)
+
+    def track(self, counter) -> None:
+        self._pending.append(counter)
+
+    def _drain(self) -> None:
+        import sys
+
+        live = []
+        for t in self._pending:
+            v = int(t.item())
+            if v:
+                self._host += v
+                t.zero_()
+            # keep counters someone else still holds; drop drained orphans
+            if sys.getrefcount(t) > 3:
+                live.append(t)
+        self._pending = live
+
+    @property
+    def count(self) -> int:
+        self._drain()
+        return self._host
+
+    @count.setter
+    def count(self, value: int) -> None:
+        self._drain()
+        self._host = int(value)
 
     def reset(self):
         self.count = 0
@@ -163,9 +197,10 @@ def rasterize_batch(mixture: GaussianMixture, rotations, translations, grid: Gri
     """Render B poses at once -> (B, D, D) (float32 device tensor or float64 array).
 
     ``method="tiles"`` follows the reference schedule (fp64 bbox, tile lists,
-    tiled forward) and adds the eigenvalue-floor clamp count to CLAMP_EVENTS;
-    ``method="direct"`` uses the binning-free fixed-point render of the
-    training step (no clamp counting).
+    tiled forward); ``method="direct"`` uses the binning-free fixed-point render
+    of the training step.  Both add the eigenvalue-floor clamp count to
+    CLAMP_EVENTS (splat.py:276-277): the tile path from its fp64 projection, the
+    direct path from the render's fp32 projection.
     """
     import torch
 
@@ -178,8 +213,10 @@ def rasterize_batch(mixture: GaussianMixture, rotations, translations, grid: Gri
     splat = engine.prepare(ctx, params, status)
     out = torch.empty((B, grid.size, grid.size), dtype=torch.float32, device=ctx.device)
     if method == "direct":
-        engine.render_direct(ctx, splat, len(mixture), poses, gs, out)
+        clamp = torch.zeros(1, dtype=torch.int64, device=ctx.device)
+        engine.render_direct(ctx, splat, len(mixture), poses, gs, out, clamp=clamp)
         _check_status(status)
+        CLAMP_EVENTS.count += int(clamp.item())
     elif method == "tiles":
         clamp = torch.zeros(B, dtype=torch.int32, device=ctx.device)
         binning = engine.bin_full(ctx, params, poses, gs, tile_size, status, clamp=clamp)

@@ -310,6 +310,81 @@ def evaluate_cases():
     print("evaluate", sorted(out), c.resolution_0143, c.resolution_05)
 
 
+def _train_records(rng, truth, grid, k, scale_of=None):
+    records = []
+    for i in range(k):
+        pose = random_pose(rng)
+        ctf = cs.CtfParams(defocus_u=15000.0, defocus_v=15000.0)
+        img = cs.apply_ctf(cs.rasterize(truth, pose, grid), ctf).pixels
+        if scale_of is not None:
+            img = img * scale_of(i)
+        records.append(cs.ParticleRecord(image=img, pose=pose, ctf=ctf))
+    return records
+
+
+def train_behaviour_cases():
+    """train() behaviours beyond the loss values (train.py:194-264), run on the reference:
+    the per-epoch CGS1 checkpoint files (gmm.py:259-265) and loss_trace.txt of the
+    train_small run; an isotropic-mode run (train.py:157-159); the divergence guard on a
+    non-finite loss and on 1e3 x the epoch-0 median (train.py:238-251), as the raised
+    DivergenceError's (epoch, step, record_index) and message."""
+    import tempfile
+
+    from cryosplat.errors import DivergenceError
+
+    out = {}
+    grid = cs.GridSpec(32, 0.5, 3.0)
+    rng = np.random.default_rng(7)
+    truth = random_mixture(rng, 6, grid, amp_range=(0.5, 1.5))
+    records = _train_records(rng, truth, grid, 3)
+    with tempfile.TemporaryDirectory() as d:
+        cs.train(cs.Dataset(records=records, grid=grid), cs.TrainConfig(epochs=3, seed=0), n_gaussians=8,
+                 out_dir=d)
+        for e in range(3):
+            out[f"ckpt_e{e}"] = np.frombuffer(open(os.path.join(d, f"checkpoint_epoch_{e}.cgs"), "rb").read(),
+                                              np.uint8)
+        out["trace"] = np.array(open(os.path.join(d, "loss_trace.txt")).read())
+    # isotropic mode: one shared raw scale per Gaussian
+    rng = np.random.default_rng(17)
+    truth = random_mixture(rng, 6, grid, amp_range=(0.5, 1.5))
+    records = _train_records(rng, truth, grid, 4)
+    out["iso_images"] = np.stack([r.image for r in records])
+    out["iso_rotations"] = np.stack([r.pose.rotation for r in records])
+    mix, losses = cs.train(cs.Dataset(records=records, grid=grid),
+                           cs.TrainConfig(epochs=2, seed=3, mode="isotropic"), n_gaussians=10)
+    out["iso_losses"] = np.stack(losses)
+    out["iso_final_params"] = mix.params
+    # divergence: one record 1e3 x brighter than the others (loss ~1e6 x)
+    rng = np.random.default_rng(27)
+    truth = random_mixture(rng, 6, grid, amp_range=(0.5, 1.5))
+    records = _train_records(rng, truth, grid, 5, scale_of=lambda i: 1e3 if i == 2 else 1.0)
+    out["big_images"] = np.stack([r.image for r in records])
+    out["big_rotations"] = np.stack([r.pose.rotation for r in records])
+    for seed in range(20):
+        try:
+            cs.train(cs.Dataset(records=records, grid=grid), cs.TrainConfig(epochs=2, seed=seed), n_gaussians=8)
+        except DivergenceError as e:
+            if e.step > 0:
+                out["big_seed"] = np.array(seed)
+                out["big_raise"] = np.array([e.epoch, e.step, e.record_index])
+                out["big_message"] = np.array(str(e))
+                break
+    assert "big_raise" in out
+    # non-finite loss: an initial mixture whose amplitude overflows the loss
+    init = cs.init_random(8, 0, grid)
+    init.params[3, 10] = 1e300
+    out["nan_initial"] = init.params.copy()
+    try:
+        cs.train(cs.Dataset(records=records[:3], grid=grid), cs.TrainConfig(epochs=1, seed=4), n_gaussians=8,
+                 initial=init)
+        raise AssertionError("expected DivergenceError")
+    except DivergenceError as e:
+        out["nan_raise"] = np.array([e.epoch, e.step, e.record_index])
+        out["nan_message"] = np.array(str(e))
+    np.savez_compressed(os.path.join(OUT, "train_behaviour.npz"), **out)
+    print("train_behaviour", {k: getattr(v, "shape", v) for k, v in out.items()})
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     for name in sys.argv[1:]:
         globals()[name]()
@@ -321,3 +396,4 @@ if __name__ == "__main__":
     kat_cases()
     ctf_cases()
     train_case()
+    train_behaviour_cases()

@@ -681,8 +681,9 @@ def test_indexed_step_graph_matches_eager_across_reorder():
 
 def test_full_size_c2_properties(oracle):
     """BASELINE configs[1] at full size (50k Gaussians, 128^2, B = 256) through properties that hold
-    at any size.  (1) A batch render equals the renders of its images alone, bitwise: the
-    fixed-point sums are order-free and the scale belongs to the mixture, whatever the chunk split.
+    at any size.  (1) A batch render equals the renders of its images alone to fixed-point
+    rounding: the sums are order-free, but each chunk of Gaussians rounds in its own unit and the
+    chunk split depends on the batch size (render.cu), so images agree to ~1e-7, not bitwise.
     (2) The backward is linear in the upstream: 2g gives exactly twice the partial accumulators
     (every operation scales exactly by a power of two).  (3) Images of the batch match the oracle."""
     grid = oracle.Grid(128, 0.5, 1.5)
@@ -700,7 +701,7 @@ def test_full_size_c2_properties(oracle):
     for k in (0, 101, 255):
         one = torch.empty((1, D, D), dtype=torch.float32, device="cuda")
         engine.render_direct(ctx, splat, n, P[k:k + 1].contiguous(), gs, one)
-        assert torch.equal(one[0], full[k])
+        assert rel_l2(one[0].cpu().numpy(), full[k].cpu().numpy()) < 1e-6
     for k in (0, 255):
         ref, _ = oracle.rasterize(params, poses[k][0], poses[k][1], grid)
         assert rel_l2(full[k].cpu().numpy(), ref) < RENDER_TOL
@@ -827,3 +828,263 @@ def test_backward_rowpair_layout_is_bitwise_natural(oracle):
     g33 = _lib.grid_struct(33, 0.5, 1.5)
     assert ctx.lib.cgs_raster_bwd(splat.data_ptr(), n, P.data_ptr(), B, g33, up.data_ptr(),
                                   _lib.CGS_LAYOUT_ROWPAIR, a.data_ptr(), 10, None) == 4  # CGS_ERR_UNSUPPORTED
+
+
+# ---------------------------------------------------------------------------
+# Round 2: the training-step render at BASELINE's large configs (C4, C5) and on a
+# heterogeneous mixture.  Round 1's fixed-point render rounded every contribution in one
+# image-wide unit (2^30 / sum of weight bounds), so its error grew linearly with N (1.35e-5
+# at 50k, emulated 3.1e-4 at 1M); render.cu now keeps each chunk in its own unit and cuts
+# every footprint at a fixed fraction of its own peak.  R02_RENDER_TARGET is the round-2
+# goal for that error; RENDER_TOL stays the gate.
+# ---------------------------------------------------------------------------
+R02_RENDER_TARGET = 5e-5
+LARGE_CASES = {
+    # name: (Gaussians, D, images)
+    "c4_200k_256": (200000, 256, 2),
+    "c5_500k_128": (500000, 128, 1),
+    "c5_1m_128": (1000000, 128, 1),
+}
+
+
+def _hetero_mixture(oracle, n, grid, seed):
+    """Amplitudes spread 100x (log-uniform), anisotropic scales 0.3..3 px, random rotations,
+    means spread over the field."""
+    rng = np.random.default_rng(seed)
+    p = oracle.init_random(n, seed, grid)
+    p[:, 0:3] = rng.normal(0.0, 0.12, (n, 3))
+    p[:, 3:6] = oracle.inverse_activate(rng.uniform(0.3, 3.0, (n, 3)) * grid.pixel_width)
+    p[:, 6:10] = rng.standard_normal((n, 4))
+    p[:, 10] = oracle.inverse_activate(10.0 ** rng.uniform(-2.0, 0.0, n) / n)
+    return p
+
+
+@pytest.mark.parametrize("case", list(LARGE_CASES))
+def test_training_render_and_step_large_configs(oracle, case):
+    """C4 (200k, 256^2, CTF) and C5 (500k / 1M at 128^2, CTF): the training step's render (the
+    fixed-point image K4 reads) within RENDER_TOL of the oracle and within the round-2 target;
+    the step's losses and gradients against the oracle (observed = 0, the reference bench frame,
+    bench.py:43-103)."""
+    n, D, B = LARGE_CASES[case]
+    grid = oracle.Grid(D, 0.5, 1.5)
+    params = oracle.init_random(n, 0, grid)
+    poses = [oracle.sample_pose(np.random.default_rng(1000 + i)) for i in range(B)]
+    cp = [oracle.Ctf(*np.random.default_rng(3000 + i).uniform(1e4, 2.5e4, 1).repeat(2)) for i in range(B)]
+    ctfs = np.stack([c.as_array() for c in cp])
+    obs = np.zeros((B, D, D), np.float32)
+    losses, grads, pipe = _full_step_device(params, poses, grid, obs, ctfs)
+    rend = pipe.render_image().cpu().numpy()
+    for i, (W, t) in enumerate(poses):
+        ref, _ = oracle.rasterize(params, W, t, grid)
+        err = rel_l2(rend[i], ref)
+        assert err < RENDER_TOL and err < R02_RENDER_TARGET, err
+    ref_losses, ref_grads = oracle.batch_step(params, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs)
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
+
+
+def test_training_render_heterogeneous_mixture(oracle):
+    """50k Gaussians with amplitudes spread 100x and mixed anisotropic scales (0.3..3 px), 128^2,
+    4 images with CTF: render, losses and gradients against the oracle, for the direct render
+    alone and inside the fused step."""
+    n, D, B = 50000, 128, 4
+    grid = oracle.Grid(D, 0.5, 1.5)
+    params = _hetero_mixture(oracle, n, grid, 5)
+    poses = [oracle.sample_pose(np.random.default_rng(4000 + i)) for i in range(B)]
+    cp = [oracle.Ctf(11000.0 + 3000 * i, 13000.0 + 2000 * i, 0.4 * i) for i in range(B)]
+    ctfs = np.stack([c.as_array() for c in cp])
+    refs = [oracle.rasterize(params, W, t, grid)[0] for W, t in poses]
+    obs = np.stack([0.7 * r for r in refs]).astype(np.float32)
+    direct = cs.rasterize_batch(cs.GaussianMixture(params), np.stack([W for W, _ in poses]),
+                                np.stack([t for _, t in poses]), cs.GridSpec(D, 0.5, 1.5), method="direct")
+    for i in range(B):
+        assert rel_l2(direct[i], refs[i]) < R02_RENDER_TARGET
+    losses, grads, pipe = _full_step_device(params, poses, grid, obs, ctfs)
+    rend = pipe.render_image().cpu().numpy()
+    for i in range(B):
+        assert rel_l2(rend[i], refs[i]) < R02_RENDER_TARGET
+    ref_losses, ref_grads = oracle.batch_step(params, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs)
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
+
+
+def test_render_error_does_not_grow_with_gaussian_count(oracle):
+    """The fixed-point render's error at 10k, 100k and 1M Gaussians (128^2, one pose): every
+    point within the round-2 target, and 1M no worse than 3x the 10k error (round 1 grew
+    linearly: 100x from 10k to 1M)."""
+    grid = oracle.Grid(128, 0.5, 1.5)
+    W, t = oracle.sample_pose(np.random.default_rng(1000))
+    errs = {}
+    for n in (10000, 100000, 1000000):
+        params = oracle.init_random(n, 0, grid)
+        img = cs.rasterize_batch(cs.GaussianMixture(params), W[None], t[None], cs.GridSpec(128, 0.5, 1.5),
+                                 method="direct")[0]
+        ref, _ = oracle.rasterize(params, W, t, grid)
+        errs[n] = rel_l2(img, ref)
+    assert max(errs.values()) < R02_RENDER_TARGET, errs
+    assert errs[1000000] < 3.0 * errs[10000] + 1e-6, errs
+
+
+def test_direct_render_counts_eigenvalue_clamps(oracle):
+    """CLAMP_EVENTS in the training path (splat.py:276-277): the direct render and the fused
+    step add one per clamped (image, Gaussian) projection, like the reference's per-rasterize
+    count; the needle KAT's clamp count, once per image of a 3-image batch."""
+    k = load_golden("kat")
+    prm = k["needle_params"]
+    grid = cs.GridSpec(64, 0.5, 3.0)
+    expect = int(k["needle_clamp_count"])
+    assert expect > 0
+    cs_splat.CLAMP_EVENTS.reset()
+    cs.rasterize_batch(cs.GaussianMixture(prm), np.stack([np.eye(3)] * 3), None, grid, method="direct")
+    assert cs_splat.CLAMP_EVENTS.count == 3 * expect
+    cs_splat.CLAMP_EVENTS.reset()
+    ogrid = oracle.Grid(64, 0.5, 3.0)
+    poses = [(np.eye(3), np.zeros(2))] * 3
+    _full_step_device(prm, poses, ogrid, np.zeros((3, 64, 64), np.float32), None)
+    assert cs_splat.CLAMP_EVENTS.count == 3 * expect
+    # init mixtures never clamp (SURVEY 8(a) row 7): the count stays put
+    cs_splat.CLAMP_EVENTS.reset()
+    params = oracle.init_random(2000, 0, oracle.Grid(64, 0.5, 1.5))
+    cs.rasterize_batch(cs.GaussianMixture(params), np.eye(3)[None], None, cs.GridSpec(64, 0.5, 1.5), method="direct")
+    assert cs_splat.CLAMP_EVENTS.count == 0
+
+
+def test_launch_state_is_per_device():
+    """The dynamic shared-memory opt-in and the resident-slot memo are keyed by device ordinal
+    (a process may drive several GPUs): after a render on cuda:0 the library holds state for
+    device 0 and none for other ordinals; on a second device, if present, a render works and
+    gets its own entries."""
+    grid = cs.GridSpec(128, 0.5, 1.5)
+    mix = cs.init_random(3000, 0, grid)
+    cs.rasterize_batch(mix, np.eye(3)[None], None, grid, method="direct")
+    lib = _lib.load()
+    assert lib.cgs_launch_state_entries(0) > 0
+    assert lib.cgs_launch_state_entries(torch.cuda.device_count() + 3) == 0
+    if torch.cuda.device_count() > 1:  # pragma: no cover - one GPU per gpurun box
+        with torch.cuda.device(1):
+            img = cs.rasterize_batch(mix, np.eye(3)[None], None, grid, method="direct")
+        assert lib.cgs_launch_state_entries(1) > 0
+        assert np.isfinite(img).all()
+
+
+# ---------------------------------------------------------------------------
+# train() behaviours against the reference's own outputs (tests/golden/train_behaviour.npz,
+# written by make_golden.py:train_behaviour_cases running /root/reference): trace text and
+# per-epoch checkpoints, isotropic mode, the divergence guard, degenerate rotations.
+# ---------------------------------------------------------------------------
+def _small_records(images, rotations):
+    return [cs.ParticleRecord(image=images[i], pose=cs.Pose(rotations[i]),
+                              ctf=cs.CtfParams(defocus_u=15000.0, defocus_v=15000.0)) for i in range(len(images))]
+
+
+def test_train_trace_and_checkpoints_match_reference(tmp_path):
+    """loss_trace.txt (train.py:252,259-263): identical header, one '%d %d %.17g %.17g' line per
+    step with identical epoch / step / lr fields and losses within 2e-3; one CGS1 checkpoint per
+    epoch (train.py:256-257, gmm.py:259-265): identical header bytes and length, parameters
+    within 1e-3 of the reference's."""
+    t = load_golden("train_small")
+    b = load_golden("train_behaviour")
+    grid = cs.GridSpec(32, 0.5, 3.0)
+    cs.train(cs.Dataset(_small_records(t["images"], t["rotations"]), grid), cs.TrainConfig(epochs=3, seed=0),
+             n_gaussians=8, out_dir=str(tmp_path))
+    text = (tmp_path / "loss_trace.txt").read_text()
+    ref = str(b["trace"])
+    assert text.endswith("\n") and ref.endswith("\n")
+    lines, ref_lines = text.splitlines(), ref.splitlines()
+    assert len(lines) == len(ref_lines) == 2 + 3 * 3
+    assert lines[:2] == ref_lines[:2]
+    for a, r in zip(lines[2:], ref_lines[2:]):
+        ea, sa, la, lra = a.split(" ")
+        er, sr, lrf, lrr = r.split(" ")
+        assert (ea, sa, lra) == (er, sr, lrr)
+        assert la == f"{float(la):.17g}"
+        assert float(la) == pytest.approx(float(lrf), rel=2e-3)
+    for e in range(3):
+        path = tmp_path / f"checkpoint_epoch_{e}.cgs"
+        got, want = path.read_bytes(), b[f"ckpt_e{e}"].tobytes()
+        assert len(got) == len(want) and got[:13] == want[:13]
+        pg = np.frombuffer(got, "<f8", offset=13)
+        assert rel_l2(pg, np.frombuffer(want, "<f8", offset=13)) < 1e-3
+        assert np.array_equal(cs.load_checkpoint(str(path)).params.ravel(), pg)
+
+
+def test_train_isotropic_matches_reference():
+    """Isotropic mode (train.py:157-159): the raw-scale gradient columns are summed so the three
+    scales stay tied; a 2-epoch reference run's losses and final parameters."""
+    b = load_golden("train_behaviour")
+    grid = cs.GridSpec(32, 0.5, 3.0)
+    mix, losses = cs.train(cs.Dataset(_small_records(b["iso_images"], b["iso_rotations"]), grid),
+                           cs.TrainConfig(epochs=2, seed=3, mode="isotropic"), n_gaussians=10)
+    np.testing.assert_allclose(np.stack(losses), b["iso_losses"], rtol=2e-3)
+    assert rel_l2(mix.params, b["iso_final_params"]) < 1e-3
+    assert np.all(mix.params[:, 3] == mix.params[:, 4]) and np.all(mix.params[:, 4] == mix.params[:, 5])
+
+
+def test_isotropic_fused_step_matches_oracle(oracle):
+    """The fused step's gradients in isotropic mode (K6 ties the scale columns) against
+    oracle.batch_step(isotropic=True), 2000 Gaussians, 5 images with CTF."""
+    grid = oracle.Grid(64, 0.5, 1.5)
+    params = oracle.init_random(2000, 4, grid)
+    params[:, 3:6] = params[:, 3:4] + np.random.default_rng(4).normal(0.0, 0.3, (2000, 1))
+    poses = [oracle.sample_pose(np.random.default_rng(80 + i)) for i in range(5)]
+    cp = [oracle.Ctf(12000.0 + 1500 * i, 12000.0 + 1500 * i) for i in range(5)]
+    obs = np.random.default_rng(9).standard_normal((5, 64, 64)).astype(np.float32) * 1e-2
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(64, 0.5, 1.5)
+    pipe = engine.StepPipeline(ctx, 2000, 5, gs, mode="isotropic")
+    p = _dev(params, torch.float64)
+    P = _dev(engine.pose_array([W for W, _ in poses], [t for _, t in poses]), torch.float64)
+    pipe.forward_backward(p, P, _dev(obs, torch.float32), _dev(np.stack([c.as_array() for c in cp]), torch.float64))
+    grads = engine.epilogue_grads(ctx, pipe.partial, pipe.G, p, _lib.CGS_MODE["isotropic"], 1.0 / 5).cpu().numpy()
+    ref_losses, ref_grads = oracle.batch_step(params, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs,
+                                              isotropic=True)
+    np.testing.assert_allclose(pipe.loss.cpu().numpy(), ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
+    assert np.array_equal(grads[:, 3], grads[:, 4]) and np.array_equal(grads[:, 4], grads[:, 5])
+
+
+def test_train_divergence_guard_matches_reference():
+    """DivergenceError (train.py:238-251, errors.py:28-35) as the reference raises it: a record
+    1e3 x brighter than the rest trips the 1e3 x epoch-0-median guard at the same (epoch, step,
+    record); an initial amplitude that overflows the loss raises 'non-finite loss' at step 0."""
+    b = load_golden("train_behaviour")
+    grid = cs.GridSpec(32, 0.5, 3.0)
+    records = _small_records(b["big_images"], b["big_rotations"])
+    with pytest.raises(cs.DivergenceError) as ei:
+        cs.train(cs.Dataset(records, grid), cs.TrainConfig(epochs=2, seed=int(b["big_seed"])), n_gaussians=8)
+    e = ei.value
+    assert [e.epoch, e.step, e.record_index] == list(b["big_raise"])
+    assert "exceeded 1000 x epoch-0 median" in str(e)
+    assert str(e).endswith(str(b["big_message"]).split(")")[-2].split("(")[-1] + ")")
+    init = cs.GaussianMixture(b["nan_initial"])
+    with pytest.raises(cs.DivergenceError) as ei:
+        cs.train(cs.Dataset(records[:3], grid), cs.TrainConfig(epochs=1, seed=4), n_gaussians=8, initial=init)
+    e = ei.value
+    assert [e.epoch, e.step, e.record_index] == list(b["nan_raise"])
+    assert str(e) == str(b["nan_message"])
+    # train_step raises the same for one record, leaving the parameters unchanged
+    before = init.params.copy()
+    with pytest.raises(cs.DivergenceError):
+        cs.train_step(init, records[0], cs.TrainConfig(), cs.AdamState(8), grid=grid, record_index=0)
+    assert np.array_equal(init.params, before)
+
+
+def test_degenerate_rotation_raises_on_device():
+    """A zero quaternion (splat.py:191-193 -> DegenerateRotationError) detected by K0 on the device:
+    rasterize (tile path), the direct render, rasterize_backward, train_step and train all raise."""
+    grid = cs.GridSpec(32, 0.5, 3.0)
+    mix = cs.init_random(8, 0, grid)
+    mix.params[5, 6:10] = 0.0
+    pose = cs.Pose.identity()
+    with pytest.raises(cs.DegenerateRotationError):
+        cs.rasterize(mix, pose, grid)
+    with pytest.raises(cs.DegenerateRotationError):
+        cs.rasterize_batch(mix, np.eye(3)[None], None, grid, method="direct")
+    with pytest.raises(cs.DegenerateRotationError):
+        cs.rasterize_backward(mix, pose, grid, np.ones((32, 32)))
+    t = load_golden("train_small")
+    records = _small_records(t["images"], t["rotations"])
+    with pytest.raises(cs.DegenerateRotationError):
+        cs.train_step(mix, records[0], cs.TrainConfig(), cs.AdamState(8), grid=grid)
+    with pytest.raises(cs.DegenerateRotationError):
+        cs.train(cs.Dataset(records, grid), cs.TrainConfig(epochs=1), n_gaussians=8, initial=mix)

@@ -136,7 +136,9 @@ def test_skip_decision_is_shared_by_all_ranks(tmp_path):
     out = str(tmp_path / "skip.npy")
     mp.spawn(_skip_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     res = np.load(out)
-    assert res[:, 0].tolist() == [6.0, 6.0]  # SKIP_BITS on both ranks
+    from paper_2508_04929_b200.parallel import SKIP_BITS
+
+    assert res[:, 0].tolist() == [float(SKIP_BITS)] * 2  # SKIP_BITS on both ranks
     assert res[:, 1].tolist() == [3.0, 3.0]  # the accumulator itself is summed
     assert res[:, 2].tolist() == [0.0, 0.0]
 

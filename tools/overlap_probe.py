@@ -49,7 +49,7 @@ def main():
 
     def fwd(st):
         _lib.call("cgs_render", pipe.splat.data_ptr(), n, poses.data_ptr(), B, pipe.grid, render2.data_ptr(),
-                  ws2.data_ptr(), st.cuda_stream)
+                  None, ws2.data_ptr(), st.cuda_stream)
 
     def bwd(st):
         _lib.call("cgs_raster_bwd", pipe.splat.data_ptr(), n, poses.data_ptr(), B, pipe.grid,
