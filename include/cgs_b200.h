@@ -252,9 +252,32 @@ int cgs_raster_bwd(const float *splat, int64_t n, const double *poses, int32_t B
                    const float *upstream, int32_t layout, float *partial,
                    int32_t images_per_group, void *stream);
 
-/* Sum partial [G][n][10] over groups in fixed order -> acc f32 [n][10]
- * (the buffer a multi-GPU run all-reduces). */
+/* Data-parallel exchange buffer: the sum of partial
+ * [G][n][10] over groups, in group order in fp64 (the order of the
+ * single-GPU epilogue), rounded once to f32, laid out in slices of `per`
+ * Gaussians: slice k = acc[k * S .. (k+1) * S), S = cgs_acc_slice_floats(n,
+ * per) = per * 10 + 2 floats (8-byte aligned), Gaussian g at slice g / per,
+ * offset (g % per) * 10; slot per * 10 of every slice is this rank's skip
+ * flag (1.0 when *status has CGS_STATUS_BIN_OVERFLOW / _NONFINITE_LOSS /
+ * _NONFINITE_PARAMS, status nullable), then one pad float; rows past n are 0.
+ * per = n is the all-reduce layout (one slice); per = ceil(n / world) is the
+ * reduce-scatter layout (rank k owns slice k).  G = 0 (an empty local batch)
+ * writes zeros, so an idle rank still joins the collective.  acc holds
+ * ceil(n / per) * S floats.  Replaces the per-image sum of rasterize_backward
+ * results across a batch (train.py:136-161 for B > 1, over ranks). */
+int64_t cgs_acc_slice_floats(int64_t n, int64_t per);
+int cgs_reduce_partials_sliced(const float *partial, int32_t G, int64_t n, int64_t per, const int32_t *status,
+                               float *acc, void *stream);
+/* cgs_reduce_partials_sliced with per = n and no status: acc f32 [n][10] + 2. */
 int cgs_reduce_partials(const float *partial, int32_t G, int64_t n, float *acc, void *stream);
+
+/* ---- particle residency -----------------------------------
+ * dst[i] = src[idx[i]] for i < rows, rows of row_bytes (multiple of 16; src,
+ * dst 16-byte aligned); idx int64 on the device.  src may be device memory or
+ * pinned host memory (UVA, zero-copy over PCIe/C2C): it loads a rank's epoch
+ * slice of a host-resident particle stack into HBM on a side stream.
+ * Replaces the per-record host reads of train.py:222-223 for the slice. */
+int cgs_gather_rows(const void *src, const int64_t *idx, int64_t rows, int64_t row_bytes, void *dst, void *stream);
 
 /* ---- K6: epilogue + Adam (splat.py:344-381, train.py:157-159, train.py:101-111)
  * grads f64 [n][11] = scale * chain(acc) for the raw parameters; mode

@@ -86,11 +86,14 @@ PROTOTYPES = {
     "cgs_bwd_groups": (I64, [I32, I32]),
     "cgs_raster_bwd": (ctypes.c_int, [P, I64, P, I32, G, P, I32, P, I32, P]),
     "cgs_reduce_partials": (ctypes.c_int, [P, I32, I64, P, P]),
+    "cgs_acc_slice_floats": (I64, [I64, I64]),
+    "cgs_reduce_partials_sliced": (ctypes.c_int, [P, I32, I64, I64, P, P, P]),
     "cgs_epilogue_grads": (ctypes.c_int, [P, I32, I64, P, I32, F64, P, P]),
     "cgs_adam": (ctypes.c_int, [P, P, P, P, I64, F64, F64, F64, F64, F64, F64, P]),
     "cgs_epilogue_adam": (ctypes.c_int, [P, I32, I64, P, P, P, I32, F64, F64, F64, F64, F64, F64, F64, P, P]),
     "cgs_epilogue_adam_dev": (ctypes.c_int, [P, I32, I64, P, P, P, I32, F64, F64, F64, F64, P, P, P]),
     "cgs_count_pairs": (ctypes.c_int, [P, I64, P, I32, G, P, P]),
+    "cgs_gather_rows": (ctypes.c_int, [P, P, I64, I64, P, P]),
 }
 
 _lib = None

@@ -10,6 +10,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cgs {
@@ -119,13 +121,38 @@ __device__ __forceinline__ void adam_elem(double &p, double g, double &m, double
     p = __dsub_rn(p, __dmul_rn(lr, mh) / __dadd_rn(sqrt(vh), eps));
 }
 
-__global__ void reduce_partials_kernel(const float *__restrict__ part, int G, int64_t n,
-                                       float *__restrict__ acc) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// Sum of the G partial groups in fp64, in group order (the order of the
+// single-GPU epilogue's sum_groups), rounded once to fp32.  Gaussian g's 10
+// floats land in slice g / per at offset (g % per) * 10; a slice is
+// per * 10 + 2 floats (8-byte aligned), slot per * 10 carries the rank's skip
+// flag (1 when status has a skip bit) and the last slot is padding.  per = n
+// is the dense all-reduce layout; per = ceil(n / world) feeds a reduce-scatter
+// whose rank k receives slice k in place.
+__global__ void reduce_partials_kernel(const float *__restrict__ part, int G, int64_t n, int64_t per,
+                                       const int32_t *__restrict__ status, float *__restrict__ acc) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t chunk = per * CGS_ACC_STRIDE + 2;
+    const int64_t slices = (n + per - 1) / per;
+    if (i < slices) {
+        const bool skip = status && (*status & (CGS_STATUS_BIN_OVERFLOW | CGS_STATUS_NONFINITE_LOSS |
+                                                CGS_STATUS_NONFINITE_PARAMS));
+        acc[i * chunk + per * CGS_ACC_STRIDE] = skip ? 1.f : 0.f;
+        acc[i * chunk + per * CGS_ACC_STRIDE + 1] = 0.f;
+    }
     if (i >= n * CGS_ACC_STRIDE) return;
-    float s = 0.f;
-    for (int k = 0; k < G; ++k) s += part[(int64_t)k * n * CGS_ACC_STRIDE + i];
-    acc[i] = s;
+    double s = 0.0;
+    for (int k = 0; k < G; ++k) s += (double)part[(int64_t)k * n * CGS_ACC_STRIDE + i];
+    const int64_t g = i / CGS_ACC_STRIDE;
+    acc[(g / per) * chunk + (g % per) * CGS_ACC_STRIDE + i % CGS_ACC_STRIDE] = (float)s;
+}
+
+// slices of the padded tail (rows n .. slices * per) stay zero
+__global__ void zero_tail_kernel(float *__restrict__ acc, int64_t n, int64_t per) {
+    const int64_t chunk = per * CGS_ACC_STRIDE + 2;
+    const int64_t slices = (n + per - 1) / per;
+    const int64_t tail0 = n - (slices - 1) * per;  // rows used in the last slice
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < (per - tail0) * CGS_ACC_STRIDE) acc[(slices - 1) * chunk + tail0 * CGS_ACC_STRIDE + i] = 0.f;
 }
 
 __global__ void epilogue_grads_kernel(const float *__restrict__ part, int G, int64_t n,
@@ -184,11 +211,40 @@ __global__ void epilogue_adam_kernel(const float *__restrict__ part, int G, int6
 
 using namespace cgs;
 
+extern "C" int64_t cgs_acc_slice_floats(int64_t n, int64_t per) {
+    if (n <= 0 || per <= 0) return 0;
+    return per * CGS_ACC_STRIDE + 2;
+}
+
+extern "C" int cgs_reduce_partials_sliced(const float *partial, int32_t G, int64_t n, int64_t per,
+                                          const int32_t *status, float *acc, void *stream) {
+    if (G < 0 || n <= 0 || per <= 0 || !acc || (G > 0 && !partial)) return CGS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t slices = (n + per - 1) / per;
+    if (G == 0) {  // an empty local batch: a zero accumulator (and a clear flag) joins the exchange
+        cudaError_t e = cudaMemsetAsync(acc, 0, sizeof(float) * slices * (per * CGS_ACC_STRIDE + 2), st);
+        if (e != cudaSuccess) {
+            set_error_detail("cgs_reduce_partials_sliced memset", cudaGetErrorString(e));
+            return CGS_ERR_CUDA;
+        }
+        return CGS_OK;
+    }
+    const int64_t tot = std::max(n * CGS_ACC_STRIDE, slices);
+    reduce_partials_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, G, n, per, status, acc);
+    int rc = check_launch("reduce_partials_kernel");
+    if (rc) return rc;
+    const int64_t pad = (slices * per - n) * CGS_ACC_STRIDE;
+    if (pad > 0) {
+        zero_tail_kernel<<<(unsigned)((pad + 255) / 256), 256, 0, st>>>(acc, n, per);
+        rc = check_launch("zero_tail_kernel");
+    }
+    return rc;
+}
+
 extern "C" int cgs_reduce_partials(const float *partial, int32_t G, int64_t n, float *acc, void *stream) {
     if (G <= 0 || n <= 0 || !partial || !acc) return CGS_ERR_ARG;
-    int64_t tot = n * CGS_ACC_STRIDE;
-    reduce_partials_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(partial, G, n, acc);
-    return check_launch("reduce_partials_kernel");
+    // dense layout: one slice of n rows, then the flag slot (left 0: no status)
+    return cgs_reduce_partials_sliced(partial, G, n, n, nullptr, acc, stream);
 }
 
 extern "C" int cgs_epilogue_grads(const float *acc, int32_t G, int64_t n, const double *params,

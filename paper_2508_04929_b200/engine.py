@@ -229,18 +229,28 @@ def loss_residual(ctx, model, obs, resid=None):
     return loss
 
 
-def obs_spectra(ctx, obs, ctfs, grid_s, chunk: int = 4096):
+def obs_spectra(ctx, obs, ctfs, grid_s, chunk: int = 4096, out=None):
     """Spectral-K4 records of a device stack (obs f32 [R][D][D], ctfs f64 [R][8]): F(obs) and
     H_sym / D^2 per observation, f32 [R][3 D (D/2+1)] (cgs_obs_spectrum), or None when the size
-    has no spectral path."""
+    has no spectral path.  ``out``: an existing [R][per] buffer to fill."""
     R, D = obs.shape[0], grid_s.size
     per = int(ctx.lib.cgs_obs_spectrum_elems(D, 1))
     if per == 0 or os.environ.get("CGS_CTF_SPATIAL", "0") == "1":
         return None
-    out = torch.empty((R, per), dtype=torch.float32, device=ctx.device)
+    if out is None:
+        out = torch.empty((R, per), dtype=torch.float32, device=ctx.device)
     for a in range(0, R, chunk):
         b = min(R, a + chunk)
         _lib.call("cgs_obs_spectrum", _ptr(obs[a:b]), _ptr(ctfs[a:b]), b - a, grid_s, _ptr(out[a:b]), ctx.stream)
+    return out
+
+
+def gather_rows(ctx, src, idx, out):
+    """out[i] = src[idx[i]] (rows of src's trailing shape); src on the device or in pinned host
+    memory (zero-copy, cgs_gather_rows); idx int64 on the device."""
+    rows = idx.numel()
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 0
+    _lib.call("cgs_gather_rows", _ptr(src), _ptr(idx), rows, row_bytes, _ptr(out), ctx.stream)
     return out
 
 
@@ -286,8 +296,6 @@ class StepPipeline:
         self.loss = torch.empty(self.B, dtype=torch.float64, device=dev)
         self.G = int(ctx.lib.cgs_bwd_groups(self.B, self.ipg))
         self.partial = torch.empty(self.G * n * 10, dtype=torch.float32, device=dev)
-        # summed accumulator + one slot for the rank's skip flag (parallel.allreduce_accumulator)
-        self.acc = torch.zeros(n * 10 + 1, dtype=torch.float32, device=dev)
         self.plan = ctx.plan(D, self.B)
         self.render_ws = torch.empty(ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, dtype=torch.float32, device=dev)
         spec_elems = int(ctx.lib.cgs_obs_spectrum_elems(D, self.B))
@@ -429,10 +437,6 @@ class StepPipeline:
         _lib.call("cgs_raster_bwd", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid,
                   _ptr(self.upstream), up_layout, _ptr(self.partial), self.ipg, s)
         mark("bwd", 1)
-
-    def reduce(self):
-        _lib.call("cgs_reduce_partials", _ptr(self.partial), self.G, self.n, _ptr(self.acc), self.ctx.stream)
-        return self.acc
 
     def adam(self, params, m, v, *, scale, lr, beta1, beta2, eps, t, acc=None, groups=None, skip=None, n=None):
         """K6 fused epilogue + Adam; acc defaults to this step's partials.  ``skip`` (int32 device

@@ -181,18 +181,81 @@ def _centered_observation(record: ParticleRecord) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # device-resident reconstruction
 # ---------------------------------------------------------------------------
+class _StepRunner:
+    """One step shape as a list of segments: ("dev", fn) device work on the current stream,
+    ("coll", fn) a collective.  With graphs the first run is eager (one-time kernel attribute
+    setup, NCCL communicator warm-up) and the step is then captured: as one CUDA graph when
+    every segment can be captured (single GPU, or NCCL collectives), else one graph per device
+    segment with the collectives run eagerly between the replays (gloo)."""
+
+    def __init__(self, segments, graphs: bool, whole: bool):
+        self.segments, self.graphs, self.whole = segments, graphs, whole
+        self._plan = None
+        self._graphs = []
+
+    @property
+    def captured(self) -> bool:
+        return self._plan is not None
+
+    def run(self) -> None:
+        if not self.graphs:
+            for _, fn in self.segments:
+                fn()
+            return
+        if self._plan is not None:
+            for _, fn in self._plan:
+                fn()
+            return
+        torch = _torch()
+        for _, fn in self.segments:
+            fn()
+        plan = []
+        if self.whole:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _, fn in self.segments:
+                    fn()
+            self._graphs.append(g)
+            plan.append(("dev", g.replay))
+        else:
+            for kind, fn in self.segments:
+                if kind == "dev":
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        fn()
+                    self._graphs.append(g)
+                    plan.append(("dev", g.replay))
+                else:
+                    plan.append((kind, fn))
+        self._plan = plan
+
+
 class Reconstructor:
     """Holds a dataset and a mixture in HBM and runs batched Adam steps.
 
     ``obs`` f32 [R][D][D] (centred observations), ``poses`` f64 [R][12],
     ``ctfs`` f64 [R][8] or None (no CTF).  ``step(indices, lr)`` launches one
-    full step for the given record indices and returns the device tensor of
-    per-image losses (no host sync).
+    full step for the given global batch of record indices (this rank runs its
+    shard of it) and returns the device tensor of this rank's per-image losses
+    (no host sync).
+
+    Data parallel (``process_group`` or an initialised default group with more
+    than one rank): the step is K0..K5 on the local shard, the accumulator
+    exchange (``parallel.Exchange``: all-reduce, or reduce-scatter + parameter
+    all-gather with ``CGS_DP_SHARDED=1``) and the fused epilogue + Adam, all
+    graph-captured (see ``_StepRunner``).  A rank whose shard of a short batch
+    is empty still joins the exchange with a zero accumulator.
+
+    Residency: ``"full"`` keeps every record (and its spectral-K4 record) in
+    HBM; ``"epoch"`` (default with more than one rank) keeps only the records
+    this rank touches in the current epoch, 1/world of the dataset, loaded by
+    ``begin_epoch`` (and prefetched for the next epoch on a copy stream).
     """
 
     def __init__(self, grid: GridSpec, params: np.ndarray, obs, poses, ctfs, *, batch_size: int,
                  mode: str = "anisotropic", config: TrainConfig | None = None, process_group=None,
-                 images_per_group: int = engine.DEFAULT_IMAGES_PER_GROUP, tile: int = engine.DEFAULT_TILE):
+                 images_per_group: int = engine.DEFAULT_IMAGES_PER_GROUP, tile: int = engine.DEFAULT_TILE,
+                 residency: str | None = None):
         torch = _torch()
         self.ctx = engine.DeviceContext.get()
         dev = self.ctx.device
@@ -201,44 +264,73 @@ class Reconstructor:
         self.config = config or TrainConfig(batch_size=batch_size, mode=mode)
         self.mode = mode
         self.n = int(params.shape[0])
-        # Gaussians live on the device in spatial (Morton) order: a CTA's
-        # Gaussians then project into a small region of each image, which is
-        # what the region-staged kernels exploit.  Per-Gaussian math does not
-        # depend on the order (renders are integer sums), so results are
-        # unchanged; params_host() returns the caller's order.
-        self.perm = morton_order(np.asarray(params)[:, :3], grid.extent)
-        params = np.asarray(params, dtype=np.float64)[self.perm]
-        self.params = torch.as_tensor(np.ascontiguousarray(params, dtype=np.float64)).to(dev)
-        self.m = torch.zeros_like(self.params)
-        self.v = torch.zeros_like(self.params)
-        self.t = 0
-        self.obs = obs if isinstance(obs, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(obs, np.float32))
-        self.obs = self.obs.to(dev, torch.float32).contiguous()
-        self.poses = torch.as_tensor(np.ascontiguousarray(poses, np.float64)).to(dev)
-        self.ctfs = None if ctfs is None else torch.as_tensor(np.ascontiguousarray(ctfs, np.float64)).to(dev)
-        # F(obs) and H_sym of every observation, once: with them K4 runs in the Fourier domain
-        # with one forward and one inverse transform per image (cgs_ctf_mse_spectral)
-        self.obs_spec = None if self.ctfs is None else engine.obs_spectra(self.ctx, self.obs, self.ctfs, self.gs)
         self.global_batch = int(batch_size)
         self.pg = process_group
-        self.world = 1
-        self.rank = 0
+        self.world, self.rank = 1, 0
         if process_group is not None or _dist_active():
             import torch.distributed as dist
 
             self.world = dist.get_world_size(process_group)
             self.rank = dist.get_rank(process_group)
-        self.ipg = images_per_group
-        self.tile = tile
-        self._pipes: dict = {}
-        self._copy_stream = None  # H2D stream of step_host
-        self._h2d_slots: dict = {}  # step_host's double-buffered device inputs
-        self._idx_slots: dict = {}  # step's graph inputs (batch indices, gathered batch, Adam scalars)
-        # step_host replays each slot's step as a CUDA graph (single GPU; CGS_GRAPHS=0 disables)
-        self.use_graphs = os.environ.get("CGS_GRAPHS", "1") == "1"
         # multi-GPU: CGS_DP_SHARDED=1 reduce-scatters the accumulator, runs the epilogue + Adam
         # on this rank's Gaussian slice only and all-gathers the parameters (ZeRO-1 style)
         self.sharded = self.world > 1 and os.environ.get("CGS_DP_SHARDED", "0") == "1"
+        self.xch = None
+        if self.world > 1:
+            per = parallel.gaussian_slice(self.n, self.rank, self.world)[2] if self.sharded else self.n
+            self.xch = parallel.Exchange(self.n, process_group, sharded=self.sharded, device=dev,
+                                         slice_floats=int(self.ctx.lib.cgs_acc_slice_floats(self.n, per)))
+        # Gaussians live on the device in spatial (Morton) order: a CTA's
+        # Gaussians then project into a small region of each image, which is
+        # what the region-staged kernels exploit.  Per-Gaussian math does not
+        # depend on the order (renders are integer sums), so results are
+        # unchanged; params_host() returns the caller's order.  The fp64
+        # parameters and moments sit in buffers padded to world x ceil(N / world)
+        # rows in sharded mode, so the parameter all-gather runs in place.
+        self.perm = morton_order(np.asarray(params)[:, :3], grid.extent)
+        params = np.asarray(params, dtype=np.float64)[self.perm]
+        rows = self.xch.per * self.world if self.sharded else self.n
+        self._store = torch.zeros((rows, 11), dtype=torch.float64, device=dev)
+        self._m_store = torch.zeros_like(self._store)
+        self._v_store = torch.zeros_like(self._store)
+        self._store[: self.n].copy_(torch.as_tensor(np.ascontiguousarray(params)))
+        self.params, self.m, self.v = self._store[: self.n], self._m_store[: self.n], self._v_store[: self.n]
+        self.t = 0
+        # dataset
+        self.residency = residency or ("epoch" if self.world > 1 else "full")
+        if self.residency not in ("full", "epoch"):
+            raise ValueError(f"unknown residency {self.residency!r}")
+        R = len(poses)
+        self.n_records = R
+        self._poses_all = torch.as_tensor(np.ascontiguousarray(poses, np.float64)).to(dev)
+        self._ctfs_all = None if ctfs is None else torch.as_tensor(np.ascontiguousarray(ctfs, np.float64)).to(dev)
+        if self.residency == "full":
+            o = obs if isinstance(obs, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(obs, np.float32))
+            self.obs = o.to(dev, torch.float32).contiguous()
+            self.poses, self.ctfs = self._poses_all, self._ctfs_all
+            # F(obs) and H_sym of every observation, once: with them K4 runs in the Fourier domain
+            # with one forward and one inverse transform per image (cgs_ctf_mse_spectral)
+            self.obs_spec = None if self.ctfs is None else engine.obs_spectra(self.ctx, self.obs, self.ctfs, self.gs)
+            self._slot = np.arange(R)
+        else:
+            o = obs.cpu() if isinstance(obs, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(obs, np.float32))
+            self._obs_host = o.to(torch.float32).contiguous().pin_memory()
+            self.obs = self.poses = self.ctfs = self.obs_spec = None
+            self._slot = np.full(R, -1, dtype=np.int64)
+            self._epoch_key = None
+            self._staged = None
+        self.ipg = images_per_group
+        self.tile = tile
+        self._pipes: dict = {}
+        self._copy_stream = None  # H2D stream of step_host and of the epoch prefetch
+        self._h2d_slots: dict = {}  # step_host's double-buffered device inputs
+        self._idx_slots: dict = {}  # step's graph inputs (batch indices, gathered batch, Adam scalars)
+        # each step shape is captured as a CUDA graph (CGS_GRAPHS=0: eager); with NCCL the
+        # collectives are inside the graph (CGS_DP_GRAPH_COLLECTIVES=0 keeps them outside)
+        self.use_graphs = os.environ.get("CGS_GRAPHS", "1") == "1"
+        self._whole_graph = self.xch is None or (self.xch.capturable and
+                                                 os.environ.get("CGS_DP_GRAPH_COLLECTIVES", "1") == "1")
+        self._empty_loss = torch.zeros(0, dtype=torch.float64, device=dev)
 
     # -- helpers -------------------------------------------------------------
     def local_slice(self, indices: np.ndarray) -> np.ndarray:
@@ -246,14 +338,23 @@ class Reconstructor:
         return parallel.shard(indices, self.rank, self.world)
 
     def pipeline(self, b: int) -> engine.StepPipeline:
+        if b < 1:
+            raise ValueError("a step pipeline needs at least one image")
         if b not in self._pipes:
             self._pipes[b] = engine.StepPipeline(self.ctx, self.n, b, self.gs, tile=self.tile,
                                                  images_per_group=self.ipg, mode=self.mode)
         return self._pipes[b]
 
+    def slots(self, records) -> np.ndarray:
+        """Device rows of the given records in the resident set (raises if one is not resident)."""
+        s = self._slot[np.asarray(records, dtype=np.int64)]
+        if len(s) and s.min() < 0:
+            raise RuntimeError("record not resident on this rank: call begin_epoch(order) first")
+        return s
+
     def _batch(self, local: np.ndarray):
         torch = _torch()
-        idx = torch.as_tensor(local, dtype=torch.int64).to(self.ctx.device, non_blocking=True)
+        idx = torch.as_tensor(self.slots(local), dtype=torch.int64).to(self.ctx.device, non_blocking=True)
         obs = self.obs.index_select(0, idx)
         poses = self.poses.index_select(0, idx)
         ctfs = None if self.ctfs is None else self.ctfs.index_select(0, idx)
@@ -264,75 +365,178 @@ class Reconstructor:
         if self.obs_spec is None:
             return None
         torch = _torch()
-        idx = torch.as_tensor(local, dtype=torch.int64).to(self.ctx.device, non_blocking=True)
+        idx = torch.as_tensor(self.slots(local), dtype=torch.int64).to(self.ctx.device, non_blocking=True)
         return self.obs_spec.index_select(0, idx)
 
     def ensure_capacity(self, indices_list) -> None:
         """Size the tile-list buffers from the given batches (one host read each)."""
         for local in indices_list:
+            if len(local) == 0:
+                continue
             pipe = self.pipeline(len(local))
             _, poses, _ = self._batch(local)
             pipe.grow(pipe.measure_items(self.params, poses))
 
-    def step(self, indices, lr: float):
-        """One step over the global batch ``indices``; returns per-image losses (device).
-
-        On one GPU the step (batch gather from the HBM-resident stack, status clear,
-        K0..K6) is a CUDA graph per batch size, replayed with this step's indices and
-        Adam scalars written into its static inputs (CGS_GRAPHS=0: eager)."""
-        indices = np.asarray(indices)
-        local = self.local_slice(indices)
-        if self.use_graphs and self.world == 1:
-            return self._graph_step_indexed(local, lr, global_batch=len(indices))
-        obs, poses, ctfs = self._batch(local)
-        return self.step_batch(obs, poses, ctfs, lr, global_batch=len(indices), obs_spec=self.batch_spectra(local))
-
-    def _graph_step_indexed(self, local: np.ndarray, lr: float, *, global_batch: int):
+    # -- particle residency --------------------------------------------------
+    def _load_records(self, records, out, stream):
+        """Device copies of ``records`` into the dict ``out`` (obs, poses, ctfs, spectra), on
+        ``stream``, without blocking the host: the observations are gathered straight from the
+        pinned host stack by a zero-copy kernel (cgs_gather_rows), then the spectral-K4 records
+        are made from them."""
         torch = _torch()
         dev = self.ctx.device
-        b = len(local)
-        key = (b, global_batch)
+        r = len(records)
+        D = self.grid.size
+        if out.get("obs") is None:
+            out["obs"] = torch.empty((r, D, D), dtype=torch.float32, device=dev)
+            out["poses"] = torch.empty((r, 12), dtype=torch.float64, device=dev)
+            out["ctfs"] = None if self._ctfs_all is None else torch.empty((r, 8), dtype=torch.float64, device=dev)
+            out["idx"] = torch.empty(r, dtype=torch.int64, device=dev)
+            out["idx_host"] = torch.empty(r, dtype=torch.int64).pin_memory()
+            out["spec"] = None
+            per = int(self.ctx.lib.cgs_obs_spectrum_elems(D, 1))
+            if out["ctfs"] is not None and per and os.environ.get("CGS_CTF_SPATIAL", "0") != "1":
+                out["spec"] = torch.empty((r, per), dtype=torch.float32, device=dev)
+        with torch.cuda.stream(stream):
+            if out.get("event") is not None:  # the pinned index buffer is reused: its last copy must be done
+                out["event"].synchronize()
+            out["idx_host"].copy_(torch.as_tensor(np.asarray(records, dtype=np.int64)))
+            out["idx"].copy_(out["idx_host"], non_blocking=True)
+            engine.gather_rows(self.ctx, self._obs_host, out["idx"], out["obs"])
+            torch.index_select(self._poses_all, 0, out["idx"], out=out["poses"])
+            if out["ctfs"] is not None:
+                torch.index_select(self._ctfs_all, 0, out["idx"], out=out["ctfs"])
+            if out["spec"] is not None:
+                engine.obs_spectra(self.ctx, out["obs"], out["ctfs"], self.gs, out=out["spec"])
+        out["records"] = np.asarray(records)
+        out["event"] = torch.cuda.Event()
+        out["event"].record(stream)
+        return out
+
+    def begin_epoch(self, order, next_order=None) -> None:
+        """Make this rank's records of the epoch visiting ``order`` resident (residency "epoch";
+        no-op for "full").  The records are this rank's shards of the epoch's global batches
+        (parallel.epoch_records), 1/world of the dataset.  With ``next_order`` the next epoch's
+        records are prefetched on a copy stream while this epoch runs.  The resident buffers are
+        refilled in place, so captured step graphs stay valid."""
+        if self.residency != "epoch":
+            return
+        torch = _torch()
+        recs = parallel.epoch_records(order, self.global_batch, self.rank, self.world)
+        compute = torch.cuda.current_stream(self.ctx.device)
+        if self.obs is None:  # first epoch: allocate the live set
+            live = self._load_records(recs, {}, compute)
+            self.obs, self.poses, self.ctfs, self.obs_spec = live["obs"], live["poses"], live["ctfs"], live["spec"]
+            self._live = live
+        else:
+            st = self._staged
+            if st is not None and np.array_equal(st["records"], recs):
+                compute.wait_event(st["event"])
+                for k in ("obs", "poses", "ctfs", "spec"):
+                    if self._live.get(k) is not None:
+                        self._live[k].copy_(st[k])
+            else:
+                self._load_records(recs, self._live, compute)
+                compute.wait_event(self._live["event"])
+        self._slot.fill(-1)
+        self._slot[recs] = np.arange(len(recs))
+        if next_order is not None:
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream(self.ctx.device)
+            self._copy_stream.wait_stream(compute)
+            nxt = parallel.epoch_records(next_order, self.global_batch, self.rank, self.world)
+            self._staged = self._load_records(nxt, self._staged or {}, self._copy_stream)
+
+    # -- one step --------------------------------------------------------------
+    def _segments(self, b: int, global_batch: int, inputs, hyper, events=None):
+        """The step for ``b`` local images (``inputs()`` -> obs, poses, ctfs, obs_spec on the
+        device) as runner segments: K0..K5 (+ the accumulator in the exchange layout), the
+        exchange, epilogue + Adam (+ the parameter all-gather when sharded)."""
+        cfg = self.config
+        pipe = self.pipeline(b) if b > 0 else None
+        scale = 1.0 / global_batch
+        mode = _lib.CGS_MODE[self.mode]
+        xch = self.xch
+        ptr = engine._ptr
+
+        def local():
+            if pipe is not None:
+                o, p, c, s = inputs()
+                pipe.clear_status()
+                pipe.forward_backward(self.params, p, o, c, events=events, obs_spec=s)
+            if xch is not None:
+                _lib.call("cgs_reduce_partials_sliced", ptr(pipe.partial) if pipe else 0, pipe.G if pipe else 0,
+                          self.n, xch.per, ptr(pipe.status) if pipe else 0, ptr(xch.acc), self.ctx.stream)
+
+        def update():
+            if xch is None:
+                acc, G, a, bb, skip = pipe.partial, pipe.G, 0, self.n, pipe.status
+            else:
+                (acc, a, bb), G, skip = xch.own(), 1, xch.skip
+            if bb > a:
+                _lib.call("cgs_epilogue_adam_dev", ptr(acc), G, bb - a, ptr(self.params[a:bb]), ptr(self.m[a:bb]),
+                          ptr(self.v[a:bb]), mode, float(scale), float(cfg.adam_beta1), float(cfg.adam_beta2),
+                          float(cfg.adam_epsilon), ptr(hyper), ptr(skip), self.ctx.stream)
+
+        segs = [("dev", local)]
+        if xch is not None:
+            segs.append(("coll", xch.run))
+        segs.append(("dev", update))
+        if xch is not None and self.sharded:
+            segs.append(("coll", lambda: xch.gather_rows(self._store)))
+        return segs, pipe
+
+    def _hyper(self, lr: float, t: int):
+        torch = _torch()
+        cfg = self.config
+        return torch.tensor([lr, 1.0 - cfg.adam_beta1 ** t, 1.0 - cfg.adam_beta2 ** t], dtype=torch.float64)
+
+    def step(self, indices, lr: float):
+        """One step over the global batch ``indices``; returns this rank's per-image losses (device).
+
+        The step (batch gather from the HBM-resident set by a device index buffer, status clear,
+        K0..K5, exchange, K6) is a CUDA graph per local batch size, replayed with this step's
+        slots and Adam scalars written into its static inputs (CGS_GRAPHS=0: eager)."""
+        torch = _torch()
+        dev = self.ctx.device
+        indices = np.asarray(indices)
+        local = self.local_slice(indices)
+        slots = self.slots(local)
+        b = len(slots)
+        key = (b, len(indices))
         sl = self._idx_slots.get(key)
         if sl is None:
             D = self.grid.size
             spec = self.obs_spec is not None
             sl = self._idx_slots[key] = {
-                "idx": torch.empty(b, dtype=torch.int64, device=dev),
-                "o": None if spec else torch.empty((b, D, D), dtype=torch.float32, device=dev),
-                "s": torch.empty((b, self.obs_spec.shape[1]), dtype=torch.float32, device=dev) if spec else None,
-                "p": torch.empty((b, 12), dtype=torch.float64, device=dev),
-                "c": None if self.ctfs is None else torch.empty((b, 8), dtype=torch.float64, device=dev),
-                "hyper": torch.empty(3, dtype=torch.float64, device=dev), "graph": None}
-        cfg, t = self.config, self.t + 1
-        sl["idx"].copy_(torch.as_tensor(np.asarray(local, dtype=np.int64)), non_blocking=True)
-        sl["hyper"].copy_(torch.tensor([lr, 1.0 - cfg.adam_beta1 ** t, 1.0 - cfg.adam_beta2 ** t],
-                                       dtype=torch.float64), non_blocking=True)
-        pipe = self.pipeline(b)
-        scale = 1.0 / global_batch
+                "idx": torch.zeros(max(b, 1), dtype=torch.int64, device=dev),
+                "o": None if spec or b == 0 else torch.empty((b, D, D), dtype=torch.float32, device=dev),
+                "s": torch.empty((b, self.obs_spec.shape[1]), dtype=torch.float32, device=dev) if spec and b else None,
+                "p": torch.empty((max(b, 1), 12), dtype=torch.float64, device=dev),
+                "c": None if self.ctfs is None else torch.empty((max(b, 1), 8), dtype=torch.float64, device=dev),
+                "hyper": torch.empty(3, dtype=torch.float64, device=dev)}
 
-        def body():
-            if sl["s"] is not None:
-                torch.index_select(self.obs_spec, 0, sl["idx"], out=sl["s"])
-            else:
-                torch.index_select(self.obs, 0, sl["idx"], out=sl["o"])
-            torch.index_select(self.poses, 0, sl["idx"], out=sl["p"])
-            if sl["c"] is not None:
-                torch.index_select(self.ctfs, 0, sl["idx"], out=sl["c"])
-            pipe.clear_status()
-            pipe.forward_backward(self.params, sl["p"], sl["o"], sl["c"], obs_spec=sl["s"])
-            pipe.adam_dev(self.params, self.m, self.v, sl["hyper"], scale=scale, beta1=cfg.adam_beta1,
-                          beta2=cfg.adam_beta2, eps=cfg.adam_epsilon)
+            def inputs(sl=sl):
+                i = sl["idx"]
+                if sl["s"] is not None:
+                    torch.index_select(self.obs_spec, 0, i, out=sl["s"])
+                else:
+                    torch.index_select(self.obs, 0, i, out=sl["o"])
+                torch.index_select(self.poses, 0, i, out=sl["p"])
+                if sl["c"] is not None:
+                    torch.index_select(self.ctfs, 0, i, out=sl["c"])
+                return sl["o"], sl["p"], sl["c"], sl["s"]
 
-        if sl["graph"] is None:
-            body()  # eager first use (one-time kernel attribute setup outside the capture)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                body()
-            sl["graph"] = g
-        else:
-            sl["graph"].replay()
+            segs, pipe = self._segments(b, len(indices), inputs, sl["hyper"])
+            sl["runner"] = _StepRunner(segs, self.use_graphs, self._whole_graph)
+            sl["pipe"] = pipe
+        t = self.t + 1
+        if b:
+            sl["idx"][:b].copy_(torch.as_tensor(slots, dtype=torch.int64), non_blocking=True)
+        sl["hyper"].copy_(self._hyper(lr, t), non_blocking=True)
+        sl["runner"].run()
         self.t = t
-        return pipe.loss
+        return sl["pipe"].loss if sl["pipe"] is not None else self._empty_loss
 
     def step_host(self, obs, poses, ctfs, lr: float, *, global_batch: int, loss_out=None):
         """Public end-to-end step from (pinned) HOST buffers of this rank's batch.
@@ -342,109 +546,68 @@ class Reconstructor:
         losses device->host into ``loss_out`` (pinned).  Nothing synchronises the
         host, so back-to-back calls overlap the next batch's H2D (PCIe) with
         this batch's kernels; the caller synchronises when it needs the numbers.
+        Each input slot's step is one CUDA graph (captured on first use).
         """
         torch = _torch()
         dev = self.ctx.device
         compute = torch.cuda.current_stream(dev)
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(dev)
-        # two preallocated device slots per batch shape, alternating: no allocator
-        # traffic per step; a slot is refilled only after the step that read it
-        key = (tuple(obs.shape), ctfs is None)
+        # two preallocated device slots per (batch shape, global batch), alternating: no
+        # allocator traffic per step; a slot is refilled only after the step that read it
+        key = (tuple(obs.shape), ctfs is None, int(global_batch))
         slots = self._h2d_slots.get(key)
         if slots is None:
             def slot():
-                return {"o": torch.empty(obs.shape, dtype=obs.dtype, device=dev),
-                        "p": torch.empty(poses.shape, dtype=poses.dtype, device=dev),
-                        "c": None if ctfs is None else torch.empty(ctfs.shape, dtype=ctfs.dtype, device=dev),
-                        "hyper": torch.empty(3, dtype=torch.float64, device=dev),
-                        "graph": None, "done": None}
+                sl = {"o": torch.empty(obs.shape, dtype=obs.dtype, device=dev),
+                      "p": torch.empty(poses.shape, dtype=poses.dtype, device=dev),
+                      "c": None if ctfs is None else torch.empty(ctfs.shape, dtype=ctfs.dtype, device=dev),
+                      "hyper": torch.empty(3, dtype=torch.float64, device=dev), "done": None}
+                segs, pipe = self._segments(obs.shape[0], global_batch,
+                                            lambda: (sl["o"], sl["p"], sl["c"], None), sl["hyper"])
+                sl["runner"], sl["pipe"] = _StepRunner(segs, self.use_graphs, self._whole_graph), pipe
+                return sl
             slots = self._h2d_slots[key] = [slot(), slot(), 0]
         sl = slots[slots[2]]
         slots[2] ^= 1
         cs = self._copy_stream
         if sl["done"] is not None:
             cs.wait_event(sl["done"])
-        graphs = self.use_graphs and self.world == 1
+        t = self.t + 1
         with torch.cuda.stream(cs):
-            if graphs:  # Adam's per-step scalars travel with the batch
-                cfg, t = self.config, self.t + 1
-                sl["hyper"].copy_(torch.tensor([lr, 1.0 - cfg.adam_beta1 ** t, 1.0 - cfg.adam_beta2 ** t],
-                                               dtype=torch.float64), non_blocking=True)
+            # Adam's per-step scalars travel with the batch
+            sl["hyper"].copy_(self._hyper(lr, t), non_blocking=True)
             sl["o"].copy_(obs, non_blocking=True)
             sl["p"].copy_(poses, non_blocking=True)
             if ctfs is not None:
                 sl["c"].copy_(ctfs, non_blocking=True)
         compute.wait_stream(cs)
-        o, p, c = sl["o"], sl["p"], sl["c"]
-        if graphs:
-            loss = self._graph_step(sl, o, p, c, global_batch)
-        else:
-            loss = self.step_batch(o, p, c, lr, global_batch=global_batch)
+        sl["runner"].run()
+        self.t = t
+        loss = sl["pipe"].loss if sl["pipe"] is not None else self._empty_loss
         if sl["done"] is None:
             sl["done"] = torch.cuda.Event()
         sl["done"].record(compute)
-        if loss_out is not None:
+        if loss_out is not None and loss.numel():
             loss_out.copy_(loss, non_blocking=True)
-        del torch
         return loss
 
-    def _graph_step(self, sl, o, p, c, global_batch: int):
-        """One step of a step_host slot as a CUDA graph replay: the first use of a
-        slot runs eagerly and captures status clear, K0..K5 and K6 (with its
-        scalars in sl["hyper"]); later steps replay it with one launch."""
-        torch = _torch()
-        pipe = self.pipeline(o.shape[0])
-        cfg = self.config
-        scale = 1.0 / global_batch
-
-        def body():
-            pipe.clear_status()
-            pipe.forward_backward(self.params, p, o, c)
-            pipe.adam_dev(self.params, self.m, self.v, sl["hyper"], scale=scale, beta1=cfg.adam_beta1,
-                          beta2=cfg.adam_beta2, eps=cfg.adam_epsilon)
-
-        if sl["graph"] is None:
-            body()  # eager: also performs one-time kernel attribute setup outside the capture
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                body()
-            sl["graph"] = g
-        else:
-            sl["graph"].replay()
-        self.t += 1
-        return pipe.loss
-
     def step_batch(self, obs, poses, ctfs, lr: float, *, global_batch: int, events=None, obs_spec=None):
-        """One step on device tensors of this rank's batch (obs f32 [b][D][D],
+        """One eager step on device tensors of this rank's batch (obs f32 [b][D][D],
         poses f64 [b][12], ctfs f64 [b][8] or None); ``global_batch`` sets the
         1/B loss scale.  ``obs_spec``: the batch's precomputed observation spectra
-        (batch_spectra); obs may then be None.  Returns the device tensor of
-        per-image losses."""
-        pipe = self.pipeline(poses.shape[0])
-        cfg = self.config
-        pipe.clear_status()
-        pipe.forward_backward(self.params, poses, obs, ctfs, events=events, obs_spec=obs_spec)
-        scale = 1.0 / global_batch
-        self.t += 1
-        if self.sharded:
-            acc = pipe.reduce()
-            part, skip = parallel.reduce_scatter_accumulator(acc, self.n, self.pg, status=pipe.status)
-            a, b, per = parallel.gaussian_slice(self.n, self.rank, self.world)
-            if b > a:
-                pipe.adam(self.params[a:b], self.m[a:b], self.v[a:b], scale=scale, lr=lr, beta1=cfg.adam_beta1,
-                          beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t, acc=part, groups=1, skip=skip,
-                          n=b - a)
-            parallel.all_gather_rows(self.params, per, self.pg)
-        elif self.world > 1:
-            acc = pipe.reduce()
-            skip = parallel.allreduce_accumulator(acc, self.pg, status=pipe.status)
-            pipe.adam(self.params, self.m, self.v, scale=scale, lr=lr, beta1=cfg.adam_beta1,
-                      beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t, acc=acc, groups=1, skip=skip)
-        else:
-            pipe.adam(self.params, self.m, self.v, scale=scale, lr=lr, beta1=cfg.adam_beta1,
-                      beta2=cfg.adam_beta2, eps=cfg.adam_epsilon, t=self.t)
-        return pipe.loss
+        (batch_spectra); obs may then be None.  ``events``: CUDA events per stage
+        (bench).  Returns the device tensor of per-image losses."""
+        torch = _torch()
+        b = 0 if poses is None else poses.shape[0]
+        t = self.t + 1
+        hyper = self._hyper(lr, t).to(self.ctx.device, non_blocking=True)
+        segs, pipe = self._segments(b, global_batch, lambda: (obs, poses, ctfs, obs_spec), hyper, events=events)
+        for _, fn in segs:
+            fn()
+        self.t = t
+        del torch
+        return pipe.loss if pipe is not None else self._empty_loss
 
     def check_status(self) -> None:
         for pipe in self._pipes.values():
@@ -457,6 +620,17 @@ class Reconstructor:
         out[self.perm] = self.params.cpu().numpy()
         return out
 
+    def moments_host(self):
+        """(m, v) in the caller's Gaussian order (gathered from their owners when sharded)."""
+        if self.sharded:
+            self.xch.gather_rows(self._m_store)
+            self.xch.gather_rows(self._v_store)
+        m = np.empty((self.n, 11))
+        v = np.empty((self.n, 11))
+        m[self.perm] = self.m.cpu().numpy()
+        v[self.perm] = self.v.cpu().numpy()
+        return m, v
+
     def reorder(self) -> None:
         """Re-sort the device-resident Gaussians (and Adam moments) by Morton code
         of their current means, e.g. once per epoch as they move."""
@@ -464,9 +638,8 @@ class Reconstructor:
         local = morton_order(self.params[:, :3].cpu().numpy(), self.grid.extent)
         idx = torch.as_tensor(local, device=self.params.device)
         if self.sharded:  # the moments are current only on their owner: replicate before permuting
-            per = parallel.gaussian_slice(self.n, self.rank, self.world)[2]
-            parallel.all_gather_rows(self.m, per, self.pg)
-            parallel.all_gather_rows(self.v, per, self.pg)
+            self.xch.gather_rows(self._m_store)
+            self.xch.gather_rows(self._v_store)
         # in place: captured step graphs keep pointing at these buffers
         self.params.copy_(self.params.index_select(0, idx))
         self.m.copy_(self.m.index_select(0, idx))
@@ -586,17 +759,22 @@ def train(dataset: Dataset, config: TrainConfig, *, n_gaussians: int, out_dir: s
                         config=config, process_group=process_group)
     R = len(dataset)
     B = config.batch_size
+    if rec.world > 1 and B < rec.world:
+        raise ValueError(f"batch_size {B} is smaller than the {rec.world} data-parallel ranks")
     is_root = rec.rank == 0
     trace, epoch_losses = [], []
     epoch0_median = None
     history0: list = []
     torch = _torch()
 
+    order = shuffle_rng.permutation(R)
     for epoch in range(config.epochs):
         lr = config.epoch_lr(epoch)
         if epoch > 0:
             rec.reorder()  # keep the device order spatial as the means move
-        order = shuffle_rng.permutation(R)
+        # the next epoch's order is drawn now (same rng sequence) so its records can be prefetched
+        next_order = shuffle_rng.permutation(R) if epoch + 1 < config.epochs else None
+        rec.begin_epoch(order, next_order)
         batches = [order[i:i + B] for i in range(0, R, B)]
         if epoch == 0:
             sizes = {}
@@ -614,6 +792,7 @@ def train(dataset: Dataset, config: TrainConfig, *, n_gaussians: int, out_dir: s
                 losses[s] = val
                 ridx = int(bidx[0]) if B == 1 else -1
                 if not math.isfinite(val):
+                    rec.check_status()  # a degenerate rotation is the reference's first error (splat.py:191-193)
                     raise DivergenceError("non-finite loss", epoch=epoch, step=s, record_index=ridx)
                 if epoch0_median is not None:
                     ref = epoch0_median
@@ -642,6 +821,8 @@ def train(dataset: Dataset, config: TrainConfig, *, n_gaussians: int, out_dir: s
         if out_dir is not None and is_root:
             mixture.params[...] = rec.params_host()
             save_checkpoint(mixture, os.path.join(out_dir, f"checkpoint_epoch_{epoch}.cgs"))
+        if next_order is not None:
+            order = next_order
     mixture.params[...] = rec.params_host()
     if out_dir is not None and is_root:
         with open(os.path.join(out_dir, "loss_trace.txt"), "w") as fh:
@@ -655,7 +836,7 @@ def train(dataset: Dataset, config: TrainConfig, *, n_gaussians: int, out_dir: s
 def _global_batch_loss(dev_loss, n_local: int, n_global: int, rec: Reconstructor) -> float:
     """Mean per-image loss of the global batch (sum over ranks when distributed)."""
     torch = _torch()
-    total = dev_loss[:n_local].sum()
+    total = dev_loss[:n_local].sum() if n_local else torch.zeros((), dtype=torch.float64, device=rec.ctx.device)
     if rec.world > 1:
         import torch.distributed as dist
 

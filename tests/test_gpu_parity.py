@@ -716,6 +716,35 @@ def test_full_size_c2_properties(oracle):
     assert int(status.item()) == 0
 
 
+DP_R, DP_B, DP_N = 25, 8, 2000  # 25 records in batches of 8: the last batch (1 image) leaves rank 0 empty
+
+
+def _dp_inputs(cs2, eng, poison=False):
+    grid = cs2.GridSpec(64, 0.5, 1.5)
+    rng = np.random.default_rng(21)
+    params = cs2.init_random(DP_N, 0, grid).params
+    rot = np.stack([cs2.sample_pose(np.random.default_rng(700 + i)).rotation for i in range(DP_R)])
+    obs = (rng.standard_normal((DP_R, 64, 64)) * 1e-3).astype(np.float32)
+    ctfs = eng.ctf_array([cs2.CtfParams(12000.0 + 300 * i, 12500.0 + 300 * i) for i in range(DP_R)])
+    orders = [np.random.default_rng(5).permutation(DP_R), np.random.default_rng(6).permutation(DP_R)]
+    if poison:  # the second record of epoch 0's first batch: rank 0's shard, step 0 only
+        obs[orders[0][1], 0, 0] = np.nan
+    return params, obs, eng.pose_array(rot), ctfs, grid, orders
+
+
+def _dp_run(rec, orders, lr=1e-3):
+    """Two epochs of global batches with a Morton reorder between them (the train() loop)."""
+    losses = []
+    for e, order in enumerate(orders):
+        if e:
+            rec.params[:, :3] += 0.002  # move the means so the reorder permutes
+            rec.reorder()
+        rec.begin_epoch(order, orders[e + 1] if e + 1 < len(orders) else None)
+        for i in range(0, DP_R, DP_B):
+            losses.append(rec.step(order[i:i + DP_B], lr * (1 + e)).clone())
+    return losses
+
+
 def _dp_gpu_worker(rank, world, port, out_path, poison, sharded=False):
     import os
     import sys
@@ -733,41 +762,31 @@ def _dp_gpu_worker(rank, world, port, out_path, poison, sharded=False):
     from paper_2508_04929_b200.optimize import Reconstructor
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    params, obs, poses, ctfs, grid = _dp_inputs(cs2, eng)
-    if poison and rank == 1:
-        obs = obs.copy()
-        obs[5, 0, 0] = np.nan  # image 5 is in rank 1's half of the batch
-    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=8, process_group=dist.group.WORLD)
-    assert rec.sharded == sharded
-    idx = rec.local_slice(np.arange(8))
-    dev = rec.ctx.device
-    sel = torch.as_tensor(idx, device=dev)
-    rec.step_batch(rec.obs.index_select(0, sel).contiguous(), rec.poses.index_select(0, sel).contiguous(),
-                   rec.ctfs.index_select(0, sel).contiguous(), 1e-3, global_batch=8)
+    params, obs, poses, ctfs, grid, orders = _dp_inputs(cs2, eng, poison)
+    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=DP_B, process_group=dist.group.WORLD)
+    assert rec.sharded == sharded and rec.residency == "epoch" and rec.use_graphs
+    losses = _dp_run(rec, orders)
     torch.cuda.synchronize()
-    if rank == 0:
-        np.save(out_path, rec.params_host())
+    resident = rec.obs.shape[0]
+    m, v = rec.moments_host()
+    np.savez(out_path + f".{rank}.npz", params=rec.params_host(), m=m, v=v, resident=resident,
+             losses=np.concatenate([x.cpu().numpy() for x in losses]),
+             nloc=np.array([len(x) for x in losses]))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def _dp_inputs(cs2, eng):
-    grid = cs2.GridSpec(64, 0.5, 1.5)
-    rng = np.random.default_rng(21)
-    params = cs2.init_random(2000, 0, grid).params
-    rot = np.stack([cs2.sample_pose(np.random.default_rng(700 + i)).rotation for i in range(8)])
-    obs = (rng.standard_normal((8, 64, 64)) * 1e-3).astype(np.float32)
-    ctfs = eng.ctf_array([cs2.CtfParams(12000.0 + 500 * i, 12500.0 + 500 * i) for i in range(8)])
-    return params, obs, eng.pose_array(rot), ctfs, grid
-
-
 @pytest.mark.parametrize("sharded", [False, True])
 @pytest.mark.parametrize("poison", [False, True])
-def test_data_parallel_step_two_ranks(tmp_path, poison, sharded):
-    """Reconstructor.step_batch with a 2-rank process group (gloo; both ranks on this GPU, host-level
-    collectives only, no kernel waits on another rank) equals the single-process full-batch step;
-    a NaN observation on one rank makes both ranks skip the update.  sharded: the ZeRO-1 style
-    epilogue (reduce-scatter, Adam on each rank's Gaussian slice, all-gather of the parameters)."""
+def test_data_parallel_two_ranks_graphs_and_epoch_residency(tmp_path, poison, sharded):
+    """Reconstructor.step with a 2-rank process group (gloo: both ranks on this GPU, collectives
+    outside the captured graph segments, no kernel waits on another rank), epoch residency (each
+    rank holds only its shards of the epoch's batches, refilled in place from a prefetch),
+    a Morton reorder between epochs and a 1-image last batch that leaves rank 0 with an empty
+    shard: every rank ends with identical parameters, equal (to fp32 reduction order) to the
+    single-process run of the same global batches; the gathered Adam moments too.  sharded: the
+    ZeRO-1 exchange (reduce-scatter, Adam on the rank's slice, in-place parameter all-gather).
+    poison: a NaN observation on rank 0 makes both ranks skip that step's update."""
     import socket
 
     import torch.multiprocessing as mp
@@ -777,17 +796,82 @@ def test_data_parallel_step_two_ranks(tmp_path, poison, sharded):
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    out = str(tmp_path / "dp.npy")
+    out = str(tmp_path / "dp")
     mp.spawn(_dp_gpu_worker, args=(2, port, out, poison, sharded), nprocs=2, join=True)
-    got = np.load(out)
-    params, obs, poses, ctfs, grid = _dp_inputs(cs, engine)
-    if poison:
-        np.testing.assert_array_equal(got, params)
-        return
-    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=8)
-    rec.step_batch(rec.obs, rec.poses, rec.ctfs, 1e-3, global_batch=8)
+    r0, r1 = np.load(out + ".0.npz"), np.load(out + ".1.npz")
+    assert np.array_equal(r0["params"], r1["params"])
+    assert int(r0["resident"]) + int(r1["resident"]) == DP_R  # each rank holds its half of an epoch
+    assert list(r0["nloc"])[3] == 0 and list(r1["nloc"])[3] == 1  # the 1-image batch
+    params, obs, poses, ctfs, grid, orders = _dp_inputs(cs, engine, poison)
+    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=DP_B)
+    assert rec.residency == "full"
+    ref_losses = np.concatenate([x.cpu().numpy() for x in _dp_run(rec, orders)])
     ref = rec.params_host()
-    assert rel_l2(got - params, ref - params) < 1e-5
+    got_losses = np.concatenate([np.split(r0["losses"], np.cumsum(r0["nloc"])[:-1])[k].tolist()
+                                 + np.split(r1["losses"], np.cumsum(r1["nloc"])[:-1])[k].tolist()
+                                 for k in range(len(r0["nloc"]))])
+    finite = np.isfinite(ref_losses)
+    assert np.array_equal(finite, np.isfinite(got_losses))
+    np.testing.assert_allclose(got_losses[finite], ref_losses[finite], rtol=1e-5)
+    assert rel_l2(r0["params"] - params, ref - params) < 1e-4
+    m, v = rec.moments_host()
+    assert rel_l2(r0["m"], m) < 1e-4 and rel_l2(r0["v"], v) < 1e-4
+    if poison:  # the poisoned step was skipped on both ranks: fewer Adam steps than a clean run
+        assert not finite.all()
+
+
+def _dp_train_worker(rank, world, port, out_path):
+    import os
+    import sys
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    from conftest import ROOT
+
+    sys.path.insert(0, ROOT)
+    import paper_2508_04929_b200 as cs2
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ds, cfg = _dp_train_inputs(cs2)
+    mix, losses = cs2.train(ds, cfg, n_gaussians=600, process_group=dist.group.WORLD,
+                            out_dir=os.path.dirname(out_path) if rank == 0 else None)
+    np.savez(out_path + f".{rank}.npz", params=mix.params, losses=np.stack(losses))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _dp_train_inputs(cs2):
+    grid = cs2.GridSpec(32, 0.5, 3.0)
+    truth = cs2.make_phantom("two-lobe", 8, 0)
+    res = cs2.simulate(cs2.SimSpec(truth=truth, num_particles=21, grid=grid,
+                                   ctf_distribution=cs2.DefocusRange(1e4, 2e4), noise=cs2.NoiseModel(snr=10.0),
+                                   seed=4))
+    return res.dataset, cs2.TrainConfig(batch_size=4, epochs=3, learning_rate=5e-3, seed=2)
+
+
+def test_train_two_ranks_matches_single_process(tmp_path):
+    """cs.train with a 2-rank process group (gloo on this GPU): per-epoch residency, graph
+    segments around the collectives, 21 records in batches of 4 (a 1-image last batch): the
+    per-step global losses and the final mixture equal the single-process train() run, and only
+    rank 0 writes the trace and checkpoints."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = str(tmp_path / "train")
+    mp.spawn(_dp_train_worker, args=(2, port, out), nprocs=2, join=True)
+    r0, r1 = np.load(out + ".0.npz"), np.load(out + ".1.npz")
+    assert np.array_equal(r0["params"], r1["params"]) and np.array_equal(r0["losses"], r1["losses"])
+    ds, cfg = _dp_train_inputs(cs)
+    mix, losses = cs.train(ds, cfg, n_gaussians=600)
+    np.testing.assert_allclose(r0["losses"], np.stack(losses), rtol=1e-5)
+    assert rel_l2(r0["params"], mix.params) < 1e-5
+    assert (tmp_path / "loss_trace.txt").exists() and (tmp_path / "checkpoint_epoch_2.cgs").exists()
 
 
 def test_graft_entry_smoke():

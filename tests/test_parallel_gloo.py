@@ -143,7 +143,22 @@ def test_skip_decision_is_shared_by_all_ranks(tmp_path):
     assert res[:, 2].tolist() == [0.0, 0.0]
 
 
-def _shard_worker(rank, world, port, out_path):
+def _exchange_layout(n, per, rank, flag):
+    """What cgs_reduce_partials_sliced writes on a rank (host restatement for the CPU test):
+    slices of per Gaussians (per * 10 + 2 floats), Gaussian g's 10 values = (10 g + j) * (rank + 1),
+    every slice's flag slot = this rank's skip flag, padding and rows past n zero."""
+    world_slices = -(-n // per)
+    S = per * 10 + 2
+    out = np.zeros(world_slices * S, np.float32)
+    for g in range(n):
+        k, r = divmod(g, per)
+        out[k * S + r * 10:k * S + r * 10 + 10] = (10 * g + np.arange(10)) * (rank + 1)
+    for k in range(world_slices):
+        out[k * S + per * 10] = flag
+    return out
+
+
+def _shard_worker(rank, world, port, out_path, sharded):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import sys
@@ -153,34 +168,68 @@ def _shard_worker(rank, world, port, out_path):
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     n = 7
-    acc = torch.arange(n * 10 + 1, dtype=torch.float32) * (rank + 1)
-    status = torch.tensor([4 if rank == 2 else 0], dtype=torch.int32)
-    part, skip = parallel.reduce_scatter_accumulator(acc, n, status=status)
-    a, b, per = parallel.gaussian_slice(n, rank, world)
-    full = torch.full((n, 11), float(rank))
-    parallel.all_gather_rows(full, per)
-    res = [part[: (b - a) * 10].clone(), skip.clone(), full.clone()]
+    xch = parallel.Exchange(n, sharded=sharded)
+    assert not xch.capturable  # gloo: collectives stay outside captured graphs
+    lay = _exchange_layout(n, xch.per, rank, 1.0 if rank == 2 else 0.0)
+    xch.acc[: lay.size].copy_(torch.from_numpy(lay))
+    xch.run()
+    own, a, b = xch.own()
+    store = torch.full((xch.per * world if sharded else n, 11), -1.0, dtype=torch.float64)
+    ra, rb, per = parallel.gaussian_slice(n, rank, world)
+    store[ra:rb] = float(rank)
+    if sharded:
+        xch.gather_rows(store)
+    res = [own[: (b - a) * 10].clone().numpy(), xch.skip.clone().numpy(), store[:n].clone().numpy(),
+           np.array([a, b])]
     gathered = [None] * world
-    dist.all_gather_object(gathered, [t.numpy() for t in res])
+    dist.all_gather_object(gathered, res)
     if rank == 0:
         np.save(out_path, np.array(gathered, dtype=object), allow_pickle=True)
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_sharded_epilogue_collectives(tmp_path):
-    """The ZeRO-1 style exchange on 3 ranks: each rank receives the rank-sum of its own Gaussian
-    slice (ceil(7/3) = 3, 3, 1 rows), the skip flag is shared, and every rank ends with every
-    slice's rows."""
+@pytest.mark.parametrize("sharded", [True, False])
+def test_sharded_epilogue_collectives(tmp_path, sharded):
+    """parallel.Exchange on 3 ranks over gloo.  Sharded (ZeRO-1 style): each rank receives the
+    rank-sum of its own Gaussian slice (ceil(7/3) = 3, 3, 1 rows) in place in the slice layout,
+    the skip flag raised by one rank is shared, and the in-place all-gather leaves every rank with
+    every slice's rows.  Replicated: every rank receives the whole sum."""
     out = str(tmp_path / "shard.npy")
-    mp.spawn(_shard_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    mp.spawn(_shard_worker, args=(3, _free_port(), out, sharded), nprocs=3, join=True)
     res = np.load(out, allow_pickle=True)
     from paper_2508_04929_b200 import parallel
 
-    total = np.arange(7 * 10 + 1, dtype=np.float32) * (1 + 2 + 3)
+    total = (10 * np.arange(7)[:, None] + np.arange(10)).ravel().astype(np.float32) * (1 + 2 + 3)
     for r in range(3):
-        a, b, _ = parallel.gaussian_slice(7, r, 3)
+        a, b = (int(x) for x in res[r][3])
+        if sharded:
+            assert (a, b) == parallel.gaussian_slice(7, r, 3)[:2]
+        else:
+            assert (a, b) == (0, 7)
         np.testing.assert_array_equal(res[r][0], total[a * 10:b * 10])
         assert int(res[r][1][0]) == parallel.SKIP_BITS
-        rows = np.concatenate([np.full((min(7, (k + 1) * 3) - min(7, k * 3), 11), float(k)) for k in range(3)])
-        np.testing.assert_array_equal(res[r][2], rows)
+        if sharded:
+            rows = np.concatenate([np.full((min(7, (k + 1) * 3) - min(7, k * 3), 11), float(k)) for k in range(3)])
+            np.testing.assert_array_equal(res[r][2], rows)
+
+
+def test_epoch_records_cover_each_batch_shard_once():
+    """Per-epoch particle residency: the records a rank loads for an epoch are
+    exactly its shards of that epoch's global batches (train.py:228-232 order), the ranks'
+    sets partition the dataset, and every rank's count is the same every epoch (so the resident
+    buffers are refilled in place)."""
+    from paper_2508_04929_b200 import parallel
+
+    for R, B, world in [(100, 8, 2), (101, 16, 3), (37, 5, 4), (1000, 256, 8)]:
+        counts = None
+        for seed in range(3):
+            order = np.random.default_rng(seed).permutation(R)
+            sets = [parallel.epoch_records(order, B, r, world) for r in range(world)]
+            assert sorted(np.concatenate(sets).tolist()) == list(range(R))
+            for r in range(world):
+                want = np.concatenate([parallel.shard(order[i:i + B], r, world) for i in range(0, R, B)])
+                assert np.array_equal(sets[r], want)
+            c = [len(x) for x in sets]
+            assert counts is None or c == counts
+            counts = c
