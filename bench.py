@@ -39,9 +39,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "particle images/sec (fwd+bwd step, 128² px, 50k Gaussians)"
-N_GAUSS, D, BATCH, DATASET = 50000, 128, 256, 2048
+N_GAUSS, D, BATCH_PER_GPU, DATASET = 50000, 128, 256, 2048
+GLOBAL_BATCH_STRONG = 256  # --scaling strong: C3's fixed global batch
 PIXEL_A = 1.5
 WORKLOAD = "C2: 50k init_random Gaussians, 128x128 particles, batch 256/GPU, known poses + CTF, fwd+bwd+Adam"
+WORKLOAD_STRONG = ("C3-style strong scaling: 50k init_random Gaussians, 128x128 particles, fixed global batch 256 "
+                   "split over the GPUs, known poses + CTF, fwd+bwd+all-reduce+Adam")
 
 
 # ---------------------------------------------------------------------------
@@ -85,24 +88,98 @@ def _cpu_sample(i0: int, seconds: float):
     return done, spent
 
 
-def cpu_baseline(seconds: float = 12.0):
+# ---------------------------------------------------------------------------
+# The reference itself (cryosplat, pure Python + Numba), installed into
+# baseline/_ref by `pip install --no-index --no-build-isolation --no-deps --target
+# baseline/_ref <copy of /root/reference/pkg>`.  One step = the
+# reference's public train_step on one C2 record (ctf_evaluate + rasterize +
+# apply_ctf + loss + apply_ctf + rasterize_backward + AdamState.update,
+# train.py:136-191), i.e. the per-image unit of the GPU step.
+# ---------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+_R = {}
+
+
+def reference_available() -> bool:
+    if not os.path.isdir(os.path.join(REF_DIR, "cryosplat")):
+        return False
+    try:
+        import numba  # noqa: F401
+    except ImportError:
+        return False
+    return True
+
+
+def _ref_init():
+    """Import the reference and JIT its kernels once (in the parent, before forking)."""
+    if _R:
+        return
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/cgs_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import cryosplat as rc
+
+    grid = rc.GridSpec(D, 0.5, PIXEL_A)
+    _R.update(rc=rc, grid=grid, mix=rc.init_random(N_GAUSS, 0, grid), cfg=rc.TrainConfig(),
+              adam=rc.AdamState(N_GAUSS))
+    _ref_one_image(0)  # JIT compilation (cache=True kernels), excluded from every timing
+
+
+def _ref_one_image(i: int) -> float:
+    rc = _R["rc"]
+    pose = rc.sample_pose(np.random.default_rng(1000 + i))
+    d = float(np.random.default_rng(3000 + i).uniform(1e4, 2.5e4))
+    rec = rc.ParticleRecord(image=np.zeros((D, D)), pose=pose, ctf=rc.CtfParams(defocus_u=d, defocus_v=d))
+    t0 = time.perf_counter()
+    rc.train_step(_R["mix"], rec, _R["cfg"], _R["adam"], lr=1e-3, grid=_R["grid"])
+    return time.perf_counter() - t0
+
+
+def _ref_sample(i0: int, seconds: float):
+    _ref_one_image(i0)
+    done, spent, i = 0, 0.0, i0 + 1
+    while spent < seconds:
+        spent += _ref_one_image(i)
+        done += 1
+        i += 1
+    return done, spent
+
+
+def _pool_rate(init, sample, seconds: float, parent_init=None):
     import multiprocessing as mp
 
     cores = os.cpu_count() or 1
+    if parent_init is not None:
+        parent_init()
     ctx = mp.get_context("fork")
-    with ctx.Pool(cores, initializer=_cpu_worker_init) as pool:
-        res = pool.starmap(_cpu_sample, [(100000 + 1000 * k, seconds) for k in range(cores)])
+    with ctx.Pool(cores, initializer=init) as pool:
+        res = pool.starmap(sample, [(100000 + 1000 * k, seconds) for k in range(cores)])
     images = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
     per_img_ms = 1e3 * statistics.median(r[1] / max(r[0], 1) for r in res)
-    return {
-        "value": images / wall,
-        "unit": "images/s",
-        "cores": cores,
-        "kind": "port",
+    return images / wall, images, cores, per_img_ms
+
+
+def cpu_baseline(seconds: float = 12.0):
+    """The CPU path on all host cores: the reference itself (baseline/_ref, kind "reference") when
+    installed, beside the oracle port (kind "port", the reference's algorithm in fp64 NumPy + C)."""
+    v, images, cores, ms = _pool_rate(_cpu_worker_init, _cpu_sample, seconds)
+    port = {
+        "value": v, "unit": "images/s", "cores": cores, "kind": "port",
         "sample": (f"{images} C2 images (50k Gaussians, 128^2, CTF, fp64 project+bin+forward+CTF+MSE+CTF^T+"
-                   f"backward+chain) over {cores} fork workers x ~{seconds:.0f}s; median {per_img_ms:.0f} ms/image/core"),
+                   f"backward+chain) over {cores} fork workers x ~{seconds:.0f}s; median {ms:.0f} ms/image/core"),
         "cpu_model": _cpu_model(),
+    }
+    if not reference_available():
+        return port
+    v, images, cores, ms = _pool_rate(lambda: None, _ref_sample, seconds, parent_init=_ref_init)
+    return {
+        "value": v, "unit": "images/s", "cores": cores, "kind": "reference",
+        "sample": (f"{images} C2 records through the reference's own train_step (cryosplat from baseline/_ref, "
+                   f"Numba kernels, fp64: ctf_evaluate, rasterize, apply_ctf x2, loss, rasterize_backward, Adam) "
+                   f"over {cores} fork workers x ~{seconds:.0f}s; median {ms:.0f} ms/image/core"),
+        "cpu_model": _cpu_model(),
+        "port": port,
     }
 
 
@@ -117,32 +194,40 @@ def _cpu_model() -> str:
 
 
 def run_reference(args, rank: int, world: int):
-    """The reference arm: the CPU path on all host cores, K timed steps of P images."""
+    """The reference arm: the reference's CPU path on all host cores, K timed steps of one image
+    per core (cryosplat itself from baseline/_ref when installed, else the oracle port)."""
     if rank != 0:
         return
     import multiprocessing as mp
 
     cores = os.cpu_count() or 1
+    ref = reference_available()
+    if ref:
+        _ref_init()
+        init, one, kind = None, _ref_one_image, "reference"
+        what = "cryosplat train_step from baseline/_ref (Numba, fp64), one C2 record per core"
+    else:
+        init, one, kind = _cpu_worker_init, _cpu_one_image, "port"
+        what = "fp64 oracle port (NumPy + C restatement of the reference), one C2 image per core"
     ctx = mp.get_context("fork")
-    with ctx.Pool(cores, initializer=_cpu_worker_init) as pool:
+    with ctx.Pool(cores, initializer=init) as pool:
         idx = iter(range(10**7))
         for _ in range(args.warmup):
-            pool.map(_cpu_one_image, [next(idx) for _ in range(cores)])
+            pool.map(one, [next(idx) for _ in range(cores)])
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            pool.map(_cpu_one_image, [next(idx) for _ in range(cores)])
+            pool.map(one, [next(idx) for _ in range(cores)])
         dt = time.perf_counter() - t0
     value = cores * args.steps / dt
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD + " (CPU oracle port, one image per core per step)",
-                   "n_gaussians": N_GAUSS, "image_px": D, "images_per_step": cores},
+        "config": {"workload": WORKLOAD + f" ({what} per step)", "n_gaussians": N_GAUSS, "image_px": D,
+                   "images_per_step": cores},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} steps x {cores} images (one per core), fp64 oracle",
-                         "cpu_model": _cpu_model()},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} steps x {cores} images: {what}", "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -251,8 +336,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     grid, obs, poses, ctfs = _dataset(rank)
     mix = cs.init_random(N_GAUSS, 0, grid)
+    # weak: 256 images per GPU; strong: a fixed global batch of 256 split over the ranks
+    BATCH = BATCH_PER_GPU if args.scaling == "weak" else GLOBAL_BATCH_STRONG // world
     global_batch = BATCH * world
-    rec = Reconstructor(grid, mix.params, obs, poses, ctfs, batch_size=global_batch)
+    # each rank's synthetic particles are its own (rank-seeded), all resident in HBM
+    rec = Reconstructor(grid, mix.params, obs, poses, ctfs, batch_size=global_batch, residency="full")
     dev = rec.ctx.device
     nb = DATASET // BATCH
     batches = [np.arange(k * BATCH, (k + 1) * BATCH) for k in range(nb)]
@@ -348,9 +436,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32 (fp64 binning bbox, fp64 Adam master params)", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_gaussians": N_GAUSS, "image_px": D, "batch_per_gpu": BATCH,
+        "config": {"workload": WORKLOAD if args.scaling == "weak" else WORKLOAD_STRONG, "n_gaussians": N_GAUSS,
+                   "image_px": D, "batch_per_gpu": BATCH,
                    "global_batch": global_batch, "parallelism": f"dp{world}", "ctf": True,
                    "l2": (f"inputs larger than L2: {DATASET}-particle dataset cycled ("
                           + (f"observation spectra {DATASET * D * (D // 2 + 1) * 8 >> 20} MiB"
@@ -385,6 +474,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: 256 images per GPU (default); strong: global batch 256 split over the GPUs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

@@ -448,7 +448,7 @@ class Reconstructor:
             self._staged = self._load_records(nxt, self._staged or {}, self._copy_stream)
 
     # -- one step --------------------------------------------------------------
-    def _segments(self, b: int, global_batch: int, inputs, hyper, events=None):
+    def _segments(self, b: int, global_batch: int, inputs, hyper, events=None, scalars=None):
         """The step for ``b`` local images (``inputs()`` -> obs, poses, ctfs, obs_spec on the
         device) as runner segments: K0..K5 (+ the accumulator in the exchange layout), the
         exchange, epilogue + Adam (+ the parameter all-gather when sharded)."""
@@ -473,7 +473,15 @@ class Reconstructor:
                 acc, G, a, bb, skip = pipe.partial, pipe.G, 0, self.n, pipe.status
             else:
                 (acc, a, bb), G, skip = xch.own(), 1, xch.skip
-            if bb > a:
+            if bb <= a:
+                return
+            if scalars is not None:  # eager step: Adam's per-step scalars as kernel arguments
+                lr, bc1, bc2 = scalars
+                _lib.call("cgs_epilogue_adam", ptr(acc), G, bb - a, ptr(self.params[a:bb]), ptr(self.m[a:bb]),
+                          ptr(self.v[a:bb]), mode, float(scale), float(lr), float(cfg.adam_beta1),
+                          float(cfg.adam_beta2), float(cfg.adam_epsilon), float(bc1), float(bc2), ptr(skip),
+                          self.ctx.stream)
+            else:  # graph replay: read from the static device tensor hyper
                 _lib.call("cgs_epilogue_adam_dev", ptr(acc), G, bb - a, ptr(self.params[a:bb]), ptr(self.m[a:bb]),
                           ptr(self.v[a:bb]), mode, float(scale), float(cfg.adam_beta1), float(cfg.adam_beta2),
                           float(cfg.adam_epsilon), ptr(hyper), ptr(skip), self.ctx.stream)
@@ -598,15 +606,14 @@ class Reconstructor:
         1/B loss scale.  ``obs_spec``: the batch's precomputed observation spectra
         (batch_spectra); obs may then be None.  ``events``: CUDA events per stage
         (bench).  Returns the device tensor of per-image losses."""
-        torch = _torch()
         b = 0 if poses is None else poses.shape[0]
         t = self.t + 1
-        hyper = self._hyper(lr, t).to(self.ctx.device, non_blocking=True)
-        segs, pipe = self._segments(b, global_batch, lambda: (obs, poses, ctfs, obs_spec), hyper, events=events)
+        cfg = self.config
+        segs, pipe = self._segments(b, global_batch, lambda: (obs, poses, ctfs, obs_spec), None, events=events,
+                                    scalars=(lr, 1.0 - cfg.adam_beta1 ** t, 1.0 - cfg.adam_beta2 ** t))
         for _, fn in segs:
             fn()
         self.t = t
-        del torch
         return pipe.loss if pipe is not None else self._empty_loss
 
     def check_status(self) -> None:
