@@ -306,9 +306,14 @@ int cgs_epilogue_adam_dev(const float *acc, int32_t G, int64_t n, double *params
 
 /* ---- measurement ----------------------------------------------------------
  * In-ellipse (image, Gaussian, pixel) pairs q < 6.5^2: the algorithmic work
- * unit of SURVEY.md 8(d).  pairs int64 [B] (accumulated, caller zeroes). */
+ * unit of SURVEY.md 8(d).  pairs int64 [B] (accumulated, caller zeroes).
+ * cgs_count_pairs_cut counts q < cut_sq instead; cgs_bwd_cut_sq() is the cut
+ * of the backward's walk (q < -2 ln 1e-7, the pairs K5 evaluates). */
 int cgs_count_pairs(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
                     int64_t *pairs, void *stream);
+int cgs_count_pairs_cut(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
+                        double cut_sq, int64_t *pairs, void *stream);
+double cgs_bwd_cut_sq(void);
 
 #ifdef __cplusplus
 }

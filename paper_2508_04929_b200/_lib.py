@@ -93,6 +93,8 @@ PROTOTYPES = {
     "cgs_epilogue_adam": (ctypes.c_int, [P, I32, I64, P, P, P, I32, F64, F64, F64, F64, F64, F64, F64, P, P]),
     "cgs_epilogue_adam_dev": (ctypes.c_int, [P, I32, I64, P, P, P, I32, F64, F64, F64, F64, P, P, P]),
     "cgs_count_pairs": (ctypes.c_int, [P, I64, P, I32, G, P, P]),
+    "cgs_count_pairs_cut": (ctypes.c_int, [P, I64, P, I32, G, F64, P, P]),
+    "cgs_bwd_cut_sq": (F64, []),
     "cgs_gather_rows": (ctypes.c_int, [P, P, I64, I64, P, P]),
 }
 

@@ -150,6 +150,18 @@ __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, 
 constexpr int kChunk = 32;
 constexpr float kMinSeedLog2 = -100.f;  // joint row-pair walks need every live seed e >= 2^-100
 
+// Tail cut of the region kernel's walk (bwd_rowpairs): q < kBwdCut instead of
+// q < 6.5^2, i.e. e >= t = exp(-kBwdCut / 2) of the Gaussian's own peak.  The
+// dropped annulus carries a fraction t (1 + kBwdCut / 2) of any moment sum
+// g e q^j (j <= 1) of the footprint -- 1.7e-6 at kBwdCut = 32.24 (t = 1e-7),
+// the size of the fp32 rounding already in those sums and 600x below the
+// 1e-3 gradient tolerance -- while the walked area shrinks by kBwdCut / 42.25.
+// CGS_BWD_CUT=0 walks the reference's whole q < 6.5^2 ellipse.
+#ifndef CGS_BWD_CUT
+#define CGS_BWD_CUT 32.236191f  /* -2 ln(1e-7) */
+#endif
+constexpr float kBwdCut = (CGS_BWD_CUT > 0.f && CGS_BWD_CUT < kCutoffSq) ? CGS_BWD_CUT : kCutoffSq;
+
 __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int b0, int W, int xlo, int xhi,
                                              int ya, int yb, const Splat2 &s, float c, Moments &M) {
     const float nk = -s.k, A = s.A, Ck = s.Ck, isp = s.inv_sqrt_p00, m2s = -2.f * s.slope;
@@ -159,7 +171,7 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
     const float2 *prow = blk + ((y - b0) >> 1) * W - xlo;
     for (; y <= yb; y += 2, DY = f2add(DY, f2pack(2.f, 2.f)), XC = f2add(XC, f2pack(m2s, m2s)), prow += W) {
         const bool v0 = y >= ya, v1 = y + 1 <= yb;
-        const float2 REM = f2fma(f2mul(DY, f2pack(nk, nk)), DY, f2pack(kCutoffSq, kCutoffSq));
+        const float2 REM = f2fma(f2mul(DY, f2pack(nk, nk)), DY, f2pack(kBwdCut, kBwdCut));
         float2 H = f2mul(f2pack(sqrt_approx(fmaxf(REM.x, 0.f)), sqrt_approx(fmaxf(REM.y, 0.f))),
                          f2pack(isp, isp));
         // a row outside [ya, yb] gets the empty span [~1e9, ~-1e9]: neutral in the union's min/max
@@ -301,14 +313,17 @@ __device__ __forceinline__ void accumulate_world(const Moments &M, const Splat2 
     acc[9] += u2 * P.w0[2] + v2 * P.w1[2];
 }
 
-__device__ __forceinline__ void footprint_rows(const Splat2 &s, int D, int &ylo, int &yhi) {
+__device__ __forceinline__ void footprint_rows(const Splat2 &s, int D, int &ylo, int &yhi, float f = 1.f) {
     ylo = 1;
     yhi = 0;
     if (s.w > 0.f) {
-        ylo = max((int)ceilf(s.mpy - s.hy), 0);
-        yhi = min((int)floorf(s.mpy + s.hy), D - 1);
+        const float hy = s.hy * f;
+        ylo = max((int)ceilf(s.mpy - hy), 0);
+        yhi = min((int)floorf(s.mpy + hy), D - 1);
     }
 }
+
+
 
 __device__ __forceinline__ void store_partial(float *__restrict__ partial, int grp, int64_t n, int64_t g,
                                               const float acc[CGS_ACC_STRIDE]) {
@@ -464,6 +479,8 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
     const bool valid = g < n;
     const int grp = blockIdx.y;
     const int b_begin = grp * ipg, b_end = min(B, b_begin + ipg);
+    // extents under the tail cut: half-extents scale by sqrt(kBwdCut / 6.5^2) (+1e-4 margin)
+    const float ext = kBwdCut < kCutoffSq ? 1.0001f * sqrtf(kBwdCut / kCutoffSq) : 1.f;
     constexpr bool pose_smem = kPoseSmem;  // host guarantees ipg <= kMaxPoseImages when set
     if (pose_smem)
         for (int i = threadIdx.x; i < (b_end - b_begin) * 8; i += kRegThreads) {
@@ -489,7 +506,8 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
         int ylo = 1, yhi = 0;
         if (valid) {
             s = project2(load_splat(splat, g), pose(b), G);
-            footprint_rows(s, D, ylo, yhi);
+            footprint_rows(s, D, ylo, yhi, ext);
+            s.hx *= ext;
         }
         // its barrier also retires every thread's reads of reg for the previous image
         const Box R = block_union(footprint_box(s, valid, ylo, yhi, D), red, b);
@@ -552,9 +570,11 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
     }
 }
 
-// In-ellipse pair count per image (same row spans as the backward).
+// (image, Gaussian, pixel) pairs with q < cut per image: cut = 6.5^2 counts the
+// reference's in-ellipse pairs; cut = kBwdCut counts the pairs
+// the backward evaluates.
 __global__ void __launch_bounds__(256) count_pairs_kernel(const float *__restrict__ splat, int64_t n,
-                                                          const double *__restrict__ poses, GridF G,
+                                                          const double *__restrict__ poses, GridF G, float cut,
                                                           int64_t *__restrict__ pairs) {
     const int b = blockIdx.y;
     const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -564,11 +584,15 @@ __global__ void __launch_bounds__(256) count_pairs_kernel(const float *__restric
         Splat2 s = project2(load_splat(splat, g), P, G);
         const int D = G.D;
         int ylo, yhi;
-        footprint_rows(s, D, ylo, yhi);
+        footprint_rows(s, D, ylo, yhi, sqrtf(cut / kCutoffSq));
         for (int iy = ylo; iy <= yhi; ++iy) {
-            int xa, xb;
-            float dx;
-            if (row_span(s, (float)iy - s.mpy, 0, D - 1, xa, xb, dx)) cnt += xb - xa + 1;
+            const float dy = (float)iy - s.mpy;
+            const float rem = fmaf(-s.k * dy, dy, cut);
+            if (rem <= 0.f) continue;
+            const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
+            const float xc = fmaf(-s.slope, dy, s.mpx);
+            const int xa = max((int)ceilf(xc - half), 0), xb = min((int)floorf(xc + half), D - 1);
+            if (xa <= xb) cnt += xb - xa + 1;
         }
     }
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -642,10 +666,18 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
     return check_launch("raster_bwd_band_kernel");
 }
 
-extern "C" int cgs_count_pairs(const float *splat, int64_t n, const double *poses, int32_t B,
-                               cgs_grid grid, int64_t *pairs, void *stream) {
-    if (n <= 0 || B <= 0 || !splat || !poses || !pairs) return CGS_ERR_ARG;
+extern "C" int cgs_count_pairs_cut(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
+                                   double cut_sq, int64_t *pairs, void *stream) {
+    if (n <= 0 || B <= 0 || !splat || !poses || !pairs || !(cut_sq > 0.0)) return CGS_ERR_ARG;
     dim3 g((unsigned)((n + 255) / 256), (unsigned)B);
-    count_pairs_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(splat, n, poses, make_grid_f(grid), pairs);
+    count_pairs_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(splat, n, poses, make_grid_f(grid), (float)cut_sq,
+                                                             pairs);
     return check_launch("count_pairs_kernel");
 }
+
+extern "C" int cgs_count_pairs(const float *splat, int64_t n, const double *poses, int32_t B,
+                               cgs_grid grid, int64_t *pairs, void *stream) {
+    return cgs_count_pairs_cut(splat, n, poses, B, grid, (double)kCutoffSq, pairs, stream);
+}
+
+extern "C" double cgs_bwd_cut_sq(void) { return (double)kBwdCut; }

@@ -83,26 +83,24 @@ __device__ __forceinline__ double weight_bound(const float *__restrict__ splat, 
     return 1.001 * amp / (2.0 * kPiD * sqrt(det));
 }
 
-// One CTA per chunk: sum and max of wb over the chunk's Gaussians, in the
-// chunk's scrambled order g = (i * A) mod n, i in [c chunk, (c+1) chunk),
-// stepped incrementally like the raster kernel.  Fixed-order reduction: the
-// scales are deterministic.
+// Sum and max of wb over 1024 consecutive logical indices of one chunk (the
+// chunk's scrambled order g = (i * A) mod n, i in [c chunk, (c+1) chunk)):
+// CTA (c, sub) covers i in [c chunk + 1024 sub, ...), one index per thread, so
+// the pass is one dependent load deep.  Fixed-order reductions: the scales
+// are deterministic.
 __global__ void __launch_bounds__(kWbThreads) wbound_chunk_kernel(const float *__restrict__ splat, int64_t n,
                                                                   double h, int64_t mulA, int chunk,
                                                                   double *__restrict__ csum,
                                                                   float *__restrict__ cmax) {
     const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(n, i0 + chunk);
-    const double fl = (0.1 * h) * (0.1 * h);
-    const int64_t stepA = (kWbThreads * mulA) % n;
-    int64_t g = ((i0 + threadIdx.x) % n) * mulA % n;
+    const int64_t i = i0 + (int64_t)blockIdx.y * kWbThreads + threadIdx.x;
     double t = 0.0;
     float m = 0.f;
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += kWbThreads) {
-        const double wb = weight_bound(splat, g, fl);
-        g += stepA;
-        if (g >= n) g -= n;
-        t += wb;
-        m = fmaxf(m, (float)wb);
+    if (i < i1) {
+        const double wb = weight_bound(splat, (int64_t)(((unsigned long long)i * (unsigned long long)mulA) %
+                                                       (unsigned long long)n), (0.1 * h) * (0.1 * h));
+        t = wb;
+        m = (float)wb;
     }
     __shared__ double ws[kWbThreads / 32];
     __shared__ float wm[kWbThreads / 32];
@@ -125,8 +123,8 @@ __global__ void __launch_bounds__(kWbThreads) wbound_chunk_kernel(const float *_
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         }
         if (threadIdx.x == 0) {
-            csum[blockIdx.x] = s;
-            cmax[blockIdx.x] = mx;
+            csum[(int64_t)blockIdx.x * gridDim.y + blockIdx.y] = s;
+            cmax[(int64_t)blockIdx.x * gridDim.y + blockIdx.y] = mx;
         }
     }
 }
@@ -139,8 +137,9 @@ __device__ __forceinline__ double unit_scale(double sum, double mx) {
 
 // Image-wide unit S from all chunks (fixed order), then per chunk its own unit
 // scale_c >= S and the band -> image factor S / scale_c <= 1.
+// csum / cmax hold nch x nsub sub-block partials (chunk-major).
 __global__ void __launch_bounds__(256) wbound_scale_kernel(const double *__restrict__ csum,
-                                                           const float *__restrict__ cmax, int nch,
+                                                           const float *__restrict__ cmax, int nch, int nsub,
                                                            float *__restrict__ gscale, float *__restrict__ cscale,
                                                            float *__restrict__ cratio) {
     __shared__ double ws[8];
@@ -148,7 +147,7 @@ __global__ void __launch_bounds__(256) wbound_scale_kernel(const double *__restr
     __shared__ float S;
     double t = 0.0;
     float m = 0.f;
-    for (int i = threadIdx.x; i < nch; i += 256) {
+    for (int i = threadIdx.x; i < nch * nsub; i += 256) {
         t += csum[i];
         m = fmaxf(m, cmax[i]);
     }
@@ -174,8 +173,14 @@ __global__ void __launch_bounds__(256) wbound_scale_kernel(const double *__restr
     }
     __syncthreads();
     for (int c = threadIdx.x; c < nch; c += 256) {
+        double cs = 0.0;
+        float cm = 0.f;
+        for (int k = 0; k < nsub; ++k) {
+            cs += csum[c * nsub + k];
+            cm = fmaxf(cm, cmax[c * nsub + k]);
+        }
         // scale_c >= S by construction (a chunk's sum and max are <= the image's); fmaxf guards rounding
-        const float sc = fmaxf((float)unit_scale(csum[c], cmax[c]), S);
+        const float sc = fmaxf((float)unit_scale(cs, cm), S);
         cscale[c] = sc;
         cratio[c] = S / sc;
     }
@@ -442,13 +447,15 @@ static int64_t fwd_chunks(int64_t n, int64_t ctas_per_chunk, int slots) {
     return best;
 }
 
-// Workspace: [0] image-wide scale (float), [1] pad, then csum f64 [mc], then
-// cmax, cscale, cratio f32 [mc] each; mc = the most chunks any split uses.
+// Workspace: [0] image-wide scale (float), [1] pad, then csum f64 [kSubMax mc],
+// cmax f32 [kSubMax mc], cscale, cratio f32 [mc]; mc = the most chunks any
+// split uses, kSubMax = the most 1024-index sub-blocks per chunk.
 static int64_t max_chunks(int64_t n) { return (n + kRChunkMin - 1) / kRChunkMin; }
+constexpr int64_t kSubMax = (kRChunk + kWbThreads - 1) / kWbThreads;
 
 extern "C" size_t cgs_render_workspace_bytes(int64_t n) {
     const int64_t mc = max_chunks(n);
-    return (size_t)(8 + 8 * mc + 3 * 4 * mc);
+    return (size_t)(8 + 12 * kSubMax * mc + 2 * 4 * mc);
 }
 
 static int render_impl(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
@@ -474,9 +481,11 @@ static int render_impl(const float *splat, int64_t n, const double *poses, int32
     const int64_t mc = max_chunks(n);
     float *gscale = (float *)ws;
     double *csum = (double *)((char *)ws + 8);
-    float *cmax = (float *)(csum + mc), *cscale = cmax + mc, *cratio = cscale + mc;
-    wbound_chunk_kernel<<<(unsigned)nchunks, kWbThreads, 0, st>>>(splat, n, h, mulA, chunk, csum, cmax);
-    wbound_scale_kernel<<<1, 256, 0, st>>>(csum, cmax, (int)nchunks, gscale, cscale, cratio);
+    float *cmax = (float *)(csum + kSubMax * mc), *cscale = cmax + kSubMax * mc, *cratio = cscale + mc;
+    const int nsub = (chunk + kWbThreads - 1) / kWbThreads;
+    wbound_chunk_kernel<<<dim3((unsigned)nchunks, (unsigned)nsub), kWbThreads, 0, st>>>(splat, n, h, mulA, chunk,
+                                                                                       csum, cmax);
+    wbound_scale_kernel<<<1, 256, 0, st>>>(csum, cmax, (int)nchunks, nsub, gscale, cscale, cratio);
     const int64_t count = (int64_t)B * D * D;
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int) * count, st);
     if (e != cudaSuccess) {

@@ -32,8 +32,22 @@ except ImportError:  # pragma: no cover - torch is in the image
 DEFAULT_TILE = 32
 # images per backward CTA (K5 partial groups): 10 balances the grid (5k CTAs on C2) against the
 # partials the epilogue reads (measured 4..64 on C2, 6..12 within 1%; CGS_IMAGES_PER_GROUP
-# overrides for A/B)
+# overrides for A/B).  Large mixtures take more images per group (images_per_group()).
 DEFAULT_IMAGES_PER_GROUP = int(os.environ.get("CGS_IMAGES_PER_GROUP", "10"))
+_BWD_THREADS = 256        # Gaussians per K5 CTA (raster_bwd.cu kRegThreads)
+_BWD_TARGET_CTAS = 4736   # 8 waves of 148 SMs x 4 resident CTAs
+_MAX_POSE_IMAGES = 64     # groups up to this size keep their poses in shared memory
+
+
+def images_per_group_auto(n: int, B: int) -> int:
+    """K5 image-group size for n Gaussians and B images: the default 10, raised for large n
+    while the grid still has ~8 waves of CTAs, so the fp32 partials the epilogue reads
+    (groups x n x 40 B: 1 GB at 1M Gaussians with groups of 10) stay few."""
+    if "CGS_IMAGES_PER_GROUP" in os.environ:
+        return DEFAULT_IMAGES_PER_GROUP
+    blocks = -(-int(n) // _BWD_THREADS)
+    groups = max(1, -(-_BWD_TARGET_CTAS // blocks))
+    return int(min(_MAX_POSE_IMAGES, max(DEFAULT_IMAGES_PER_GROUP, -(-int(B) // groups))))
 
 
 def require_cuda():
@@ -180,10 +194,12 @@ def render_direct(ctx, splat, n, poses, grid_s, out, clamp=None):
     return out
 
 
-def raster_bwd(ctx, splat, n, poses, grid_s, upstream, ipg=DEFAULT_IMAGES_PER_GROUP, out=None,
+def raster_bwd(ctx, splat, n, poses, grid_s, upstream, ipg=None, out=None,
                layout=_lib.CGS_LAYOUT_NATURAL):
-    """K5: partial world-frame accumulators f32 [G][N][10]."""
+    """K5: partial world-frame accumulators f32 [G][N][10] (ipg: images per group, default
+    images_per_group_auto(n, B))."""
     B = poses.shape[0]
+    ipg = images_per_group_auto(n, B) if ipg is None else ipg
     G = int(ctx.lib.cgs_bwd_groups(B, ipg))
     partial = out if out is not None else ctx.buf("bwd_partial", G * n * 10, torch.float32)
     _lib.call("cgs_raster_bwd", _ptr(splat), n, _ptr(poses), B, grid_s, _ptr(upstream), layout,
@@ -254,9 +270,15 @@ def gather_rows(ctx, src, idx, out):
     return out
 
 
-def count_pairs(ctx, splat, n, poses, grid_s) -> "torch.Tensor":
+def count_pairs(ctx, splat, n, poses, grid_s, cut_sq=None) -> "torch.Tensor":
+    """Per-image (Gaussian, pixel) pairs with q < cut_sq (default 6.5^2: the reference's
+    in-ellipse pairs)."""
     pairs = torch.zeros(poses.shape[0], dtype=torch.int64, device=ctx.device)
-    _lib.call("cgs_count_pairs", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, _ptr(pairs), ctx.stream)
+    if cut_sq is None:
+        _lib.call("cgs_count_pairs", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, _ptr(pairs), ctx.stream)
+    else:
+        _lib.call("cgs_count_pairs_cut", _ptr(splat), n, _ptr(poses), poses.shape[0], grid_s, float(cut_sq),
+                  _ptr(pairs), ctx.stream)
     return pairs
 
 
@@ -272,13 +294,13 @@ class StepPipeline:
     """
 
     def __init__(self, ctx: DeviceContext, n: int, batch: int, grid_s, *, tile=DEFAULT_TILE,
-                 images_per_group=DEFAULT_IMAGES_PER_GROUP, mode="anisotropic", item_capacity=None,
+                 images_per_group=None, mode="anisotropic", item_capacity=None,
                  render="direct"):
         self.ctx = ctx
         self.n, self.B, self.grid = int(n), int(batch), grid_s
         self.D = grid_s.size
         self.tile = tile
-        self.ipg = images_per_group
+        self.ipg = images_per_group or images_per_group_auto(n, batch)
         self.mode = _lib.CGS_MODE[mode]
         self.render_mode = render
         dev = ctx.device

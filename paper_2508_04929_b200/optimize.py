@@ -254,7 +254,7 @@ class Reconstructor:
 
     def __init__(self, grid: GridSpec, params: np.ndarray, obs, poses, ctfs, *, batch_size: int,
                  mode: str = "anisotropic", config: TrainConfig | None = None, process_group=None,
-                 images_per_group: int = engine.DEFAULT_IMAGES_PER_GROUP, tile: int = engine.DEFAULT_TILE,
+                 images_per_group: int | None = None, tile: int = engine.DEFAULT_TILE,
                  residency: str | None = None):
         torch = _torch()
         self.ctx = engine.DeviceContext.get()

@@ -707,7 +707,7 @@ def test_full_size_c2_properties(oracle):
         assert rel_l2(full[k].cpu().numpy(), ref) < RENDER_TOL
     gen = torch.Generator(device="cuda").manual_seed(7)
     up = torch.randn((B, D, D), generator=gen, device="cuda", dtype=torch.float32) * 1e-3
-    G = int(ctx.lib.cgs_bwd_groups(B, engine.DEFAULT_IMAGES_PER_GROUP))
+    G = int(ctx.lib.cgs_bwd_groups(B, engine.images_per_group_auto(n, B)))
     part1 = torch.empty(G * n * 10, dtype=torch.float32, device="cuda")
     part2 = torch.empty_like(part1)
     engine.raster_bwd(ctx, splat, n, P, gs, up, out=part1)
@@ -902,7 +902,7 @@ def test_backward_rowpair_layout_is_bitwise_natural(oracle):
     gen = torch.Generator(device="cuda").manual_seed(3)
     up = torch.randn((B, D, D), generator=gen, device="cuda", dtype=torch.float32) * 1e-3
     up_rp = up.view(B, D // 2, 2, D).transpose(2, 3).contiguous()
-    G = int(ctx.lib.cgs_bwd_groups(B, engine.DEFAULT_IMAGES_PER_GROUP))
+    G = int(ctx.lib.cgs_bwd_groups(B, engine.images_per_group_auto(n, B)))
     a = torch.empty(G * n * 10, dtype=torch.float32, device="cuda")
     b = torch.empty_like(a)
     engine.raster_bwd(ctx, splat, n, P, gs, up, out=a)

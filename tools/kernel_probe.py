@@ -46,7 +46,7 @@ def main():
     out = torch.empty((a.B, a.D, a.D), dtype=torch.float32, device="cuda")
     ws = torch.empty(ctx.lib.cgs_render_workspace_bytes(a.n) // 4 + 1, dtype=torch.float32, device="cuda")
     up = torch.randn((a.B, a.D, a.D), generator=torch.Generator(device="cuda").manual_seed(1), device="cuda") * 1e-3
-    G = int(ctx.lib.cgs_bwd_groups(a.B, engine.DEFAULT_IMAGES_PER_GROUP))
+    G = int(ctx.lib.cgs_bwd_groups(a.B, engine.images_per_group_auto(a.n, a.B)))
     part = torch.empty(G * a.n * 10, dtype=torch.float32, device="cuda")
     s = ctx.stream
 
@@ -56,7 +56,7 @@ def main():
 
     def bwd():
         _lib.call("cgs_raster_bwd", splat.data_ptr(), a.n, P.data_ptr(), a.B, gs, up.data_ptr(),
-                  _lib.CGS_LAYOUT_ROWPAIR, part.data_ptr(), engine.DEFAULT_IMAGES_PER_GROUP, s)
+                  _lib.CGS_LAYOUT_ROWPAIR, part.data_ptr(), engine.images_per_group_auto(a.n, a.B), s)
 
     res = {"tag": os.path.basename(a.tag), "n": a.n, "D": a.D, "B": a.B}
     for name, fn in (("fwd", fwd), ("bwd", bwd)):
