@@ -250,88 +250,6 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
     }
 }
 
-#ifndef CGS_FWD_ROWPAIR
-#define CGS_FWD_ROWPAIR 0
-#endif
-// Rows [ya, yb] of one footprint whose rows are all shorter than 32 px, walked
-// two rows at a time: the f32x2 lanes are rows (y, y+1), so the per-row setup
-// (span, exp seeds) runs packed once per two rows and each packed step adds
-// one pixel of each row.  Both rows walk n = max(n0, n1) pixels; the shorter
-// row's extra pixels lie just past its own cut (q > cut), where they add that
-// row's true (tail) contribution: the image gets closer to the reference, never
-// farther.  A walk that would run past the right image edge starts further
-// left instead (again on the row's own tail), so every pixel written is in the
-// image.  An odd last row walks alone.
-__device__ __forceinline__ void fwd_rowpairs_band(int *__restrict__ acc, int r0, int ld, int xhi, int ya, int yb,
-                                                  const Splat2 &s, float scale, float cut) {
-    constexpr float kM = 12582912.0f;
-    constexpr float kHalfL2e = 0.5f * 1.4426950408889634f;
-    const float wSd = s.w * scale * 0x1p-75f;
-    const float2 WS = f2pack(wSd, wSd);
-    const float c = ex2_approx(2.f * s.A);
-    const float2 CC = f2pack(c, c);
-    const float A2 = 2.f * s.A, nHcut = -kHalfL2e * cut - 74.f, xhiM = kM + (float)xhi;
-    const float nk = -s.k, isp = s.inv_sqrt_p00, m2s = -2.f * s.slope;
-    float2 DY = f2pack((float)ya - s.mpy, (float)(ya + 1) - s.mpy);
-    float2 XC = f2pack(fmaf(-s.slope, DY.x, s.mpx), fmaf(-s.slope, DY.y, s.mpx));
-    int *row = acc + (ya - r0) * ld;
-    int y = ya;
-    for (; y < yb; y += 2, DY = f2add(DY, f2pack(2.f, 2.f)), XC = f2add(XC, f2pack(m2s, m2s)), row += 2 * ld) {
-        const float2 REM = f2fma(f2mul(DY, f2pack(nk, nk)), DY, f2pack(cut, cut));
-        const float2 H = f2mul(f2pack(sqrt_approx(fmaxf(REM.x, 0.f)), sqrt_approx(fmaxf(REM.y, 0.f))),
-                               f2pack(isp, isp));
-        const float fa0 = fmaxf(__fadd_ru(XC.x - H.x, kM), kM), fb0 = fminf(__fadd_rd(XC.x + H.x, kM), xhiM);
-        const float fa1 = fmaxf(__fadd_ru(XC.y - H.y, kM), kM), fb1 = fminf(__fadd_rd(XC.y + H.y, kM), xhiM);
-        // pixels per row (as floats: exact small integers); n = the longer row
-        const float n = fmaxf(fb0 - fa0, fb1 - fa1) + 1.f;
-        if (!(n > 0.f)) continue;
-#if CGS_FWD_ROWPAIR == 2
-        // exact spans: the shorter row's extra steps are predicated off
-        const float sa0 = fa0, sa1 = fa1;
-#else
-        // a start past xhi - n + 1 moves left (onto the row's own left tail)
-        const float lim = xhiM - n + 1.f;
-        const float sa0 = fminf(fa0, lim), sa1 = fminf(fa1, lim);
-#endif
-        const float2 DX = f2pack((sa0 - kM) - XC.x, (sa1 - kM) - XC.y);
-        const float2 CK = f2fma(f2pack(kHalfL2e, kHalfL2e), REM, f2pack(nHcut, nHcut));
-        const float2 DXA = f2mul(DX, f2pack(s.A, s.A));
-        const float2 L = f2fma(DXA, DX, CK);
-        const float2 GL = f2fma(f2pack(A2, A2), DX, f2pack(s.A, s.A));
-        float2 E = f2pack(ex2_approx(L.x), ex2_approx(L.y));
-        float2 G = f2pack(ex2_approx(GL.x), ex2_approx(GL.y));
-#if CGS_FWD_ROWPAIR == 2
-        uint32_t a0 = smem_u32(row + (__float_as_int(sa0) - 0x4B400000));
-        uint32_t a1 = smem_u32(row + ld + (__float_as_int(sa1) - 0x4B400000));
-        const uint32_t e0 = a0 + 4u * (uint32_t)(int)(fb0 - fa0 + 1.f), e1 = a1 + 4u * (uint32_t)(int)(fb1 - fa1 + 1.f);
-        const uint32_t ae = a0 + 4u * (uint32_t)(int)n;
-#pragma unroll 1
-        for (; a0 < ae; a0 += 4u, a1 += 4u) {
-            const float2 v = f2mul_keep_denorm(WS, E);
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %0, %1;\n\t@p red.shared.add.u32 [%0], %2;\n\t}"
-                         :: "r"(a0), "r"(e0), "r"(__float_as_int(v.x)) : "memory");
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %0, %1;\n\t@p red.shared.add.u32 [%0], %2;\n\t}"
-                         :: "r"(a1), "r"(e1), "r"(__float_as_int(v.y)) : "memory");
-            f2scale(E, G);
-            f2scale(G, CC);
-        }
-#else
-        int *p0 = row + (__float_as_int(sa0) - 0x4B400000);
-        int *p1 = row + ld + (__float_as_int(sa1) - 0x4B400000);
-        int *pe = p0 + (int)n;
-#pragma unroll 1
-        for (; p0 < pe; ++p0, ++p1) {
-            const float2 v = f2mul_keep_denorm(WS, E);
-            atomicAdd(p0, __float_as_int(v.x));
-            atomicAdd(p1, __float_as_int(v.y));
-            f2scale(E, G);
-            f2scale(G, CC);
-        }
-#endif
-    }
-    if (y == yb) fwd_rows_band<true>(acc, r0, ld, xhi, y, y, s, scale, cut);
-}
-
 // CTA = (chunk of Gaussians, image, band of rows); the band's int32
 // accumulator (whole 128^2 image in 64 KB) lives in shared memory, in the
 // chunk's unit, and is added to the global image (image-wide unit) once at
@@ -380,12 +298,8 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
         const int yhi = min(min((int)floorf(s.mpy + hy), D - 1), r1 - 1);
         if (ylo > yhi) continue;
         // widest row = 2 sqrt(cut / p00) = 2 * 6.5 sqrt(cut / 6.5^2) / sqrt(p00)
-        if (13.f * sqrt_approx(cut * (1.f / kCutoffSq)) * s.inv_sqrt_p00 < 31.f) {
-            if (CGS_FWD_ROWPAIR)
-                fwd_rowpairs_band(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
-            else
-                fwd_rows_band<true>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
-        }
+        if (13.f * sqrt_approx(cut * (1.f / kCutoffSq)) * s.inv_sqrt_p00 < 31.f)
+            fwd_rows_band<true>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
         else
             fwd_rows_band<false>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
     }
