@@ -24,7 +24,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import paper_2508_04929_b200 as cs  # noqa: E402
-from paper_2508_04929_b200 import engine, parallel  # noqa: E402
+from paper_2508_04929_b200 import engine  # noqa: E402
 from paper_2508_04929_b200.optimize import Reconstructor  # noqa: E402
 
 
@@ -57,9 +57,12 @@ def main():
     poses = engine.pose_array(np.stack([r.pose.rotation for r in recs]))
     ctfs = engine.ctf_array([r.ctf for r in recs])
     params = cs.init_random(args.gaussians, 0, grid).params
+    # one GPU: the whole stack in HBM; N ranks: each holds its shards of the epoch's batches
     rec = Reconstructor(grid, params, res.images, poses, ctfs, batch_size=args.batch, process_group=pg)
     del res
-    batches = parallel.epoch_batches(args.particles, args.batch, np.random.default_rng(0))
+    order = np.random.default_rng(0).permutation(args.particles)  # train.py:228-232
+    rec.begin_epoch(order)
+    batches = [order[i:i + args.batch] for i in range(0, args.particles, args.batch)]
     for b in batches[:50]:  # warm-up (pipelines, graphs, clocks)
         rec.step(b, args.lr)
     torch.cuda.synchronize()
@@ -77,7 +80,7 @@ def main():
         ms = float(t.item())
     first = float(losses[0].mean().item())
     last = float(torch.cat([x.reshape(-1) for x in losses[-10:]]).mean().item())
-    out = {"config": "C3", "particles": args.particles, "n_gaussians": args.gaussians, "image_px": 128,
+    out = {"config": "C3", "particles": args.particles, "residency": rec.residency, "n_gaussians": args.gaussians, "image_px": 128,
            "global_batch": args.batch, "steps": len(batches), "n_gpus": world, "epoch_s": ms / 1e3,
            "images_per_s": args.particles / (ms / 1e3), "ms_per_step": ms / len(batches),
            "generate_s": gen_s, "generate_images_per_s": args.particles / gen_s,
