@@ -118,6 +118,7 @@ def _ref_init():
     if REF_DIR not in sys.path:
         sys.path.insert(0, REF_DIR)
     import cryosplat as rc
+    import cryosplat.bench  # noqa: F401  (the stock benchmark frame)
 
     grid = rc.GridSpec(D, 0.5, PIXEL_A)
     _R.update(rc=rc, grid=grid, mix=rc.init_random(N_GAUSS, 0, grid), cfg=rc.TrainConfig(),
@@ -173,6 +174,9 @@ def cpu_baseline(seconds: float = 12.0):
     if not reference_available():
         return port
     v, images, cores, ms = _pool_rate(lambda: None, _ref_sample, seconds, parent_init=_ref_init)
+    # the reference's own benchmark frame (cryosplat/bench.py:43-103: its mid-training bench
+    # mixture, rasterize + CTF + backward, no Adam), one core, median of 5 after a warm-up
+    stock = _R["rc"].bench.benchmark_case(N_GAUSS, D, 5, seed=0)
     return {
         "value": v, "unit": "images/s", "cores": cores, "kind": "reference",
         "sample": (f"{images} C2 records through the reference's own train_step (cryosplat from baseline/_ref, "
@@ -180,6 +184,8 @@ def cpu_baseline(seconds: float = 12.0):
                    f"over {cores} fork workers x ~{seconds:.0f}s; median {ms:.0f} ms/image/core"),
         "cpu_model": _cpu_model(),
         "port": port,
+        "stock_bench_frame": {"ms_per_image_one_core": 1e3 * stock.median_seconds, "fps_one_core": stock.fps,
+                              "what": "cryosplat.bench.benchmark_case(50000, 128, repeats=5): bench.py:43-103"},
     }
 
 
