@@ -273,10 +273,13 @@ class Reconstructor:
             self.world = dist.get_world_size(process_group)
             self.rank = dist.get_rank(process_group)
         # multi-GPU: CGS_DP_SHARDED=1 reduce-scatters the accumulator, runs the epilogue + Adam
-        # on this rank's Gaussian slice only and all-gathers the parameters (ZeRO-1 style)
-        self.sharded = self.world > 1 and os.environ.get("CGS_DP_SHARDED", "0") == "1"
+        # on this rank's Gaussian slice only and all-gathers the parameters (ZeRO-1 style).
+        # CGS_DP_EXCHANGE=1 keeps the exchange even in a 1-rank group (exercises the collective
+        # path, e.g. NCCL graph capture, on a single GPU).
+        dp = self.world > 1 or (self.pg is not None and os.environ.get("CGS_DP_EXCHANGE", "0") == "1")
+        self.sharded = dp and os.environ.get("CGS_DP_SHARDED", "0") == "1"
         self.xch = None
-        if self.world > 1:
+        if dp:
             per = parallel.gaussian_slice(self.n, self.rank, self.world)[2] if self.sharded else self.n
             self.xch = parallel.Exchange(self.n, process_group, sharded=self.sharded, device=dev,
                                          slice_floats=int(self.ctx.lib.cgs_acc_slice_floats(self.n, per)))

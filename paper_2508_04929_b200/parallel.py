@@ -113,12 +113,12 @@ class Exchange:
         import torch
         import torch.distributed as dist
 
-        if self.world > 1:
-            if self.sharded and self.backend != "gloo":
-                part = self.acc[self.rank * self.slice:(self.rank + 1) * self.slice]
-                dist.reduce_scatter_tensor(part, self.acc, op=dist.ReduceOp.SUM, group=self.group)
-            else:  # replicated layout, or gloo (no reduce-scatter): the own slice is summed in place
-                dist.all_reduce(self.acc, op=dist.ReduceOp.SUM, group=self.group)
+        # (also in a 1-rank group, CGS_DP_EXCHANGE=1: the collective path itself runs)
+        if self.sharded and self.backend != "gloo":
+            part = self.acc[self.rank * self.slice:(self.rank + 1) * self.slice]
+            dist.reduce_scatter_tensor(part, self.acc, op=dist.ReduceOp.SUM, group=self.group)
+        else:  # replicated layout, or gloo (no reduce-scatter): the own slice is summed in place
+            dist.all_reduce(self.acc, op=dist.ReduceOp.SUM, group=self.group)
         part = self.own()[0]
         flag = part[self.per * 10:self.per * 10 + 1]
         self.skip.copy_(torch.where(flag > 0, SKIP_BITS, 0).to(torch.int32))
@@ -127,8 +127,6 @@ class Exchange:
         """All-gather [world * per][k] ``store`` in place from every rank's rows."""
         import torch.distributed as dist
 
-        if self.world == 1:
-            return
         per = self.per
         mine = store[self.rank * per:(self.rank + 1) * per]
         if self.backend == "gloo":  # no in-place all_gather_into_tensor: gather into the row views

@@ -1172,3 +1172,65 @@ def test_degenerate_rotation_raises_on_device():
         cs.train_step(mix, records[0], cs.TrainConfig(), cs.AdamState(8), grid=grid)
     with pytest.raises(cs.DegenerateRotationError):
         cs.train(cs.Dataset(records, grid), cs.TrainConfig(epochs=1), n_gaussians=8, initial=mix)
+
+
+def _nccl_one_rank_worker(rank, world, port, out_path, sharded):
+    import os
+    import sys
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["CGS_DP_EXCHANGE"] = "1"
+    os.environ["CGS_DP_SHARDED"] = "1" if sharded else "0"
+    from conftest import ROOT
+
+    sys.path.insert(0, ROOT)
+    import paper_2508_04929_b200 as cs2
+    from paper_2508_04929_b200 import engine as eng
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    params, obs, poses, ctfs, grid, orders = _dp_inputs(cs2, eng)
+    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=DP_B, process_group=dist.group.WORLD,
+                        residency="full")
+    assert rec.xch is not None and rec.xch.capturable and rec._whole_graph and rec.sharded == sharded
+    losses = _dp_run(rec, orders)
+    torch.cuda.synchronize()
+    captured = all(sl["runner"].captured for sl in rec._idx_slots.values())
+    m, v = rec.moments_host()
+    np.savez(out_path, params=rec.params_host(), m=m, v=v, captured=captured,
+             losses=np.concatenate([x.cpu().numpy() for x in losses]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("sharded", [False, True])
+def test_nccl_exchange_captured_in_step_graph(tmp_path, sharded):
+    """The NCCL branch on real hardware: a 1-rank NCCL group with the exchange forced on
+    (CGS_DP_EXCHANGE=1) runs the data-parallel step with its collectives (all-reduce, or
+    reduce-scatter + parameter all-gather) captured inside the step's CUDA graph, over two
+    epochs with a reorder and a short batch; it equals the plain single-GPU run (the exchange
+    rounds the fp64 group sums to fp32 once, hence a tolerance)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = str(tmp_path / "nccl.npz")
+    mp.spawn(_nccl_one_rank_worker, args=(1, port, out, sharded), nprocs=1, join=True)
+    r = np.load(out)
+    assert bool(r["captured"])
+    params, obs, poses, ctfs, grid, orders = _dp_inputs(cs, engine)
+    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=DP_B)
+    ref_losses = np.concatenate([x.cpu().numpy() for x in _dp_run(rec, orders)])
+    np.testing.assert_allclose(r["losses"], ref_losses, rtol=1e-5)
+    assert rel_l2(r["params"] - params, rec.params_host() - params) < 1e-4
+    m, v = rec.moments_host()
+    assert rel_l2(r["m"], m) < 1e-4 and rel_l2(r["v"], v) < 1e-4
