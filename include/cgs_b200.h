@@ -271,6 +271,29 @@ int cgs_reduce_partials_sliced(const float *partial, int32_t G, int64_t n, int64
 /* cgs_reduce_partials_sliced with per = n and no status: acc f32 [n][10] + 2. */
 int cgs_reduce_partials(const float *partial, int32_t G, int64_t n, float *acc, void *stream);
 
+/* Fused peer-memory exchange (data parallel over NVLink / NVSwitch): ONE
+ * launch per rank does reduce-scatter + epilogue + Adam + parameter all-gather
+ * for its Gaussian slice.  accs[p] (device array of `world` pointers) = rank
+ * p's accumulator in the reduce-scatter layout above (per = ceil(n / world)),
+ * mapped into this process; stores[p] = rank p's fp64 parameter store of
+ * world * per rows x 11; flags[p] = rank p's u32 [world + 1] handshake array
+ * (zero-initialised; arrive slots, done counter), or flags = nullptr for a
+ * single-process simulation that launches the ranks one after another on one
+ * device (no handshake).  m, v: this rank's moments for its `per` rows.
+ * hyper f64 [4] on the device = (lr, bc1, bc2, epoch): the epoch is the step
+ * counter, identical on every rank, +1 per step, starting at 1.  Rank r sums
+ * slice r of every peer's accumulator in rank order (fp64), skips the update
+ * when any peer's flag is set, runs the chain + Adam as cgs_epilogue_adam_dev
+ * and stores the new rows into every peer's store.  Replaces the exchange of
+ * train.py:136-161 over ranks (all-reduce or reduce-scatter, AdamState.update
+ * train.py:93-111, parameter broadcast).  Every rank must launch it each step
+ * with the same n, per, world (the grid is cgs_peer_blocks(per) CTAs, all
+ * co-resident). */
+int32_t cgs_peer_blocks(int64_t per);
+int cgs_peer_epilogue_adam(const float *const *accs, double *const *stores, uint32_t *const *flags, int32_t rank,
+                           int32_t world, int64_t n, int64_t per, double *m, double *v, int32_t mode, double scale,
+                           double beta1, double beta2, double eps, const double *hyper, void *stream);
+
 /* ---- particle residency -----------------------------------
  * dst[i] = src[idx[i]] for i < rows, rows of row_bytes (multiple of 16; src,
  * dst 16-byte aligned); idx int64 on the device.  src may be device memory or

@@ -88,6 +88,8 @@ PROTOTYPES = {
     "cgs_reduce_partials": (ctypes.c_int, [P, I32, I64, P, P]),
     "cgs_acc_slice_floats": (I64, [I64, I64]),
     "cgs_reduce_partials_sliced": (ctypes.c_int, [P, I32, I64, I64, P, P, P]),
+    "cgs_peer_blocks": (I32, [I64]),
+    "cgs_peer_epilogue_adam": (ctypes.c_int, [P, P, P, I32, I32, I64, I64, P, P, I32, F64, F64, F64, F64, P, P]),
     "cgs_epilogue_grads": (ctypes.c_int, [P, I32, I64, P, I32, F64, P, P]),
     "cgs_adam": (ctypes.c_int, [P, P, P, P, I64, F64, F64, F64, F64, F64, F64, P]),
     "cgs_epilogue_adam": (ctypes.c_int, [P, I32, I64, P, P, P, I32, F64, F64, F64, F64, F64, F64, F64, P, P]),

@@ -207,9 +207,140 @@ __global__ void epilogue_adam_kernel(const float *__restrict__ part, int G, int6
     }
 }
 
+// ---- fused peer-memory exchange: reduce-scatter + epilogue + Adam + parameter broadcast ----
+//
+// Data parallel over NVLink / NVSwitch without NCCL on the step's data path
+// (SURVEY.md 8(e)).  Every rank's accumulator (the cgs_reduce_partials_sliced
+// layout, one slice of `per` Gaussians per rank, each slice carrying the
+// rank's skip flag) and its fp64 parameter store (world x per rows) are mapped
+// into every peer (symmetric memory).  Rank r's launch:
+//   1. arrive: block 0 stores the step's epoch into slot r of every peer's
+//      flag array (release, system scope); every block waits until its own
+//      array shows the epoch for all peers (acquire): every accumulator is
+//      complete (each was written by the kernel before this one on its rank);
+//   2. reads slice r of every peer's accumulator over peer memory and sums it
+//      in fp64 in rank order (deterministic), runs the chain + Adam for those
+//      Gaussians (the owner keeps their moments) and stores the new parameter
+//      rows into every peer's store;
+//   3. done: each block adds 1 to every peer's done counter (release), and
+//      block 0 returns only when its own counter has every block of every rank
+//      for this epoch (acquire): no rank starts its next step (K0 reads the
+//      parameters; the exchange rewrites the accumulator peers read) before
+//      all writes into it and all reads from it are finished.
+// One launch replaces reduce-scatter + epilogue + parameter all-gather.  The
+// epoch is hyper[3] (the step counter, identical on every rank and advanced
+// by the host before each step or graph replay), so counters never reset.
+// Flags per rank: u32 [world] arrive slots, then the done counter.
+// With flags == nullptr the launch skips both handshakes: a single-process
+// simulation of `world` ranks (ranks launched one after another on one
+// device) that checks the arithmetic and the layouts.
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_sys_add(uint32_t *p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_at_least(const uint32_t *p, uint32_t target) {
+    while ((int32_t)(ld_acquire_sys(p) - target) < 0) __nanosleep(64);
+}
+
+constexpr int kPeerThreads = 128;
+constexpr int kPeerMaxWorld = 64;
+
+__global__ void __launch_bounds__(kPeerThreads) peer_epilogue_adam_kernel(
+    const float *const *__restrict__ accs, double *const *__restrict__ stores, uint32_t *const *__restrict__ flags,
+    int rank, int world, int64_t n, int64_t per, double *__restrict__ m, double *__restrict__ v, int mode,
+    double scale, double b1, double b2, double eps, const double *__restrict__ hyper) {
+    const uint32_t epoch = (uint32_t)hyper[3];
+    if (flags) {
+        if (blockIdx.x == 0 && threadIdx.x < world) {
+            __threadfence_system();
+            st_release_sys(flags[threadIdx.x] + rank, epoch);
+        }
+        if (threadIdx.x == 0)
+            for (int p = 0; p < world; ++p) wait_at_least(flags[rank] + p, epoch);
+        __syncthreads();
+    }
+    const int64_t slice = per * CGS_ACC_STRIDE + 2;
+    const int64_t off = (int64_t)rank * slice;
+    bool skip = false;
+    for (int p = 0; p < world; ++p) skip |= accs[p][off + per * CGS_ACC_STRIDE] > 0.f;
+    const int64_t a = (int64_t)rank * per;
+    const int64_t rows = a < n ? min(per, n - a) : 0;
+    if (!skip) {
+        const double lr = hyper[0], bc1 = hyper[1], bc2 = hyper[2];
+        const double *own = stores[rank];
+        for (int64_t i = blockIdx.x * (int64_t)kPeerThreads + threadIdx.x; i < rows;
+             i += (int64_t)gridDim.x * kPeerThreads) {
+            double acc[10];
+#pragma unroll
+            for (int c = 0; c < 10; ++c) acc[c] = 0.0;
+            for (int p = 0; p < world; ++p) {  // rank order: the same sum on every run
+                const float2 *src = reinterpret_cast<const float2 *>(accs[p] + off + i * CGS_ACC_STRIDE);
+#pragma unroll
+                for (int c = 0; c < 5; ++c) {
+                    const float2 w = src[c];
+                    acc[2 * c] += (double)w.x;
+                    acc[2 * c + 1] += (double)w.y;
+                }
+            }
+            double raw[11], gr[11];
+#pragma unroll
+            for (int j = 0; j < 11; ++j) raw[j] = own[(a + i) * 11 + j];
+            chain_grads(raw, acc, scale, mode, gr);
+            double *mg = m + i * 11, *vg = v + i * 11;
+#pragma unroll
+            for (int j = 0; j < 11; ++j) {
+                double mj = mg[j], vj = vg[j];
+                adam_elem(raw[j], gr[j], mj, vj, lr, b1, b2, eps, bc1, bc2);
+                mg[j] = mj;
+                vg[j] = vj;
+            }
+            for (int q = 0; q < world; ++q) {  // the row into every rank's store (own included)
+                double *dst = stores[q] + (a + i) * 11;
+#pragma unroll
+                for (int j = 0; j < 11; ++j) dst[j] = raw[j];
+            }
+        }
+    }
+    if (flags) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            for (int q = 0; q < world; ++q) red_release_sys_add(flags[q] + world, 1u);
+            if (blockIdx.x == 0) wait_at_least(flags[rank] + world, epoch * (uint32_t)world * gridDim.x);
+        }
+    }
+}
+
 }  // namespace cgs
 
 using namespace cgs;
+
+extern "C" int32_t cgs_peer_blocks(int64_t per) {
+    if (per <= 0) return 0;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (int32_t)std::min<int64_t>((per + kPeerThreads - 1) / kPeerThreads, sms);
+}
+
+extern "C" int cgs_peer_epilogue_adam(const float *const *accs, double *const *stores, uint32_t *const *flags,
+                                      int32_t rank, int32_t world, int64_t n, int64_t per, double *m, double *v,
+                                      int32_t mode, double scale, double beta1, double beta2, double eps,
+                                      const double *hyper, void *stream) {
+    if (!accs || !stores || !m || !v || !hyper || world < 1 || world > kPeerMaxWorld || rank < 0 ||
+        rank >= world || n <= 0 || per <= 0 || per * world < n)
+        return CGS_ERR_ARG;
+    const int32_t blocks = cgs_peer_blocks(per);
+    peer_epilogue_adam_kernel<<<blocks, kPeerThreads, 0, (cudaStream_t)stream>>>(
+        accs, stores, flags, rank, world, n, per, m, v, mode, scale, beta1, beta2, eps, hyper);
+    return check_launch("peer_epilogue_adam_kernel");
+}
 
 extern "C" int64_t cgs_acc_slice_floats(int64_t n, int64_t per) {
     if (n <= 0 || per <= 0) return 0;

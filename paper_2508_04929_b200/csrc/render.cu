@@ -194,6 +194,29 @@ __global__ void __launch_bounds__(256) wbound_scale_kernel(const double *__restr
 // low mantissa bits; the clamps also absorb spans beyond +-2^22 px), and the
 // row term C_k dy^2 comes from the span's own remainder,
 // -log2(e)/2 k dy^2 = log2(e)/2 (rem - cut).
+// Timing experiments only (wrong images): CGS_FWD_EXP 1 = non-atomic
+// read-add-write, 2 = plain store, 3 = no memory op (values folded into a
+// register), 4 = atomics at conflict-free addresses (bank = lane).
+#if !defined(CGS_FWD_EXP) || CGS_FWD_EXP == 0 || CGS_FWD_EXP >= 5
+#define CGS_BAND_ADD(p, v) atomicAdd((p), (v))
+#elif CGS_FWD_EXP == 1
+#define CGS_BAND_ADD(p, v) (*(volatile int *)(p) += (v))
+#elif CGS_FWD_EXP == 2
+#define CGS_BAND_ADD(p, v) (*(volatile int *)(p) = (v))
+#elif CGS_FWD_EXP == 3
+#define CGS_BAND_ADD(p, v) (g_sink ^= (v) + (int)(size_t)(p))
+#elif CGS_FWD_EXP == 4
+#define CGS_BAND_ADD(p, v) atomicAdd(acc + ((((p) - acc) & ~31) | (threadIdx.x & 31)), (v))
+#endif
+#if defined(CGS_FWD_EXP) && CGS_FWD_EXP == 3
+__device__ int g_sink_dummy;
+#define CGS_SINK_DECL int g_sink = 0;
+#define CGS_SINK_FLUSH if (g_sink == 0x7fffffff) g_sink_dummy = g_sink;
+#else
+#define CGS_SINK_DECL
+#define CGS_SINK_FLUSH
+#endif
+
 template <bool kRecur>
 __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int ld, int xhi, int ya, int yb,
                                               const Splat2 &s, float scale, float cut) {
@@ -215,6 +238,7 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
     float dy = (float)ya - s.mpy;
     float xcv = fmaf(-s.slope, dy, s.mpx);
     int *row = acc + (ya - r0) * ld;
+    CGS_SINK_DECL
     for (int nr = yb - ya; nr >= 0; --nr, dy += 1.f, xcv -= s.slope, row += ld) {
         // rem <= 0 (a row at the cut's tip) leaves an empty span or one pixel
         // at q >= cut, whose contribution rounds to 0: no branch for it
@@ -236,18 +260,19 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
 #pragma unroll 1
             for (; x < xb; x += 2) {
                 const float2 v = f2mul_keep_denorm(WS, E);
-                atomicAdd(row + x, __float_as_int(v.x));
-                atomicAdd(row + x + 1, __float_as_int(v.y));
+                CGS_BAND_ADD(row + x, __float_as_int(v.x));
+                CGS_BAND_ADD(row + x + 1, __float_as_int(v.y));
                 f2scale(E, R);
                 f2scale(R, C4);
             }
-            if (x == xb) atomicAdd(row + x, __float_as_int(fmul_keep_denorm(wSd, E.x)));
+            if (x == xb) CGS_BAND_ADD(row + x, __float_as_int(fmul_keep_denorm(wSd, E.x)));
         } else {
             float d = dx;
             for (int x = xa; x <= xb; ++x, d += 1.f)
                 atomicAdd(row + x, __float_as_int(fmul_keep_denorm(wSd, ex2_approx(fmaf(s.A * d, d, Ckdy2)))));
         }
     }
+    CGS_SINK_FLUSH
 }
 
 // CTA = (chunk of Gaussians, image, band of rows); the band's int32
@@ -275,7 +300,11 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     const float scale = cscale[blockIdx.x];
     const PoseF P = load_pose_f(poses, b);
     const int64_t i_begin = (int64_t)blockIdx.x * chunk;
+#if defined(CGS_FWD_EXP) && CGS_FWD_EXP == 6
+    const int64_t i_end = i_begin;  // band init + flush only (timing experiment)
+#else
     const int64_t i_end = min(n, i_begin + chunk);
+#endif
     const int64_t stepA = (kRThreads * mulA) % n;
     int64_t g = ((i_begin + threadIdx.x) % n) * mulA % n;
     int nclamp = 0;
@@ -297,6 +326,10 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
         const int ylo = max(max((int)ceilf(s.mpy - hy), 0), r0);
         const int yhi = min(min((int)floorf(s.mpy + hy), D - 1), r1 - 1);
         if (ylo > yhi) continue;
+#if defined(CGS_FWD_EXP) && CGS_FWD_EXP == 5
+        if (ylo + yhi == -12345 || cut == 1.2345f) band[0] += 1;  // projection only (timing experiment)
+        continue;
+#endif
         // widest row = 2 sqrt(cut / p00) = 2 * 6.5 sqrt(cut / 6.5^2) / sqrt(p00)
         if (13.f * sqrt_approx(cut * (1.f / kCutoffSq)) * s.inv_sqrt_p00 < 31.f)
             fwd_rows_band<true>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);

@@ -276,13 +276,18 @@ class Reconstructor:
         # on this rank's Gaussian slice only and all-gathers the parameters (ZeRO-1 style).
         # CGS_DP_EXCHANGE=1 keeps the exchange even in a 1-rank group (exercises the collective
         # path, e.g. NCCL graph capture, on a single GPU).
+        # CGS_DP_PEER=1: the sharded exchange as one kernel over peer memory (parallel.PeerExchange).
         dp = self.world > 1 or (self.pg is not None and os.environ.get("CGS_DP_EXCHANGE", "0") == "1")
-        self.sharded = dp and os.environ.get("CGS_DP_SHARDED", "0") == "1"
+        self.peer = dp and os.environ.get("CGS_DP_PEER", "0") == "1"
+        self.sharded = dp and (self.peer or os.environ.get("CGS_DP_SHARDED", "0") == "1")
         self.xch = None
         if dp:
             per = parallel.gaussian_slice(self.n, self.rank, self.world)[2] if self.sharded else self.n
-            self.xch = parallel.Exchange(self.n, process_group, sharded=self.sharded, device=dev,
-                                         slice_floats=int(self.ctx.lib.cgs_acc_slice_floats(self.n, per)))
+            sf = int(self.ctx.lib.cgs_acc_slice_floats(self.n, per))
+            if self.peer:
+                self.xch = parallel.PeerExchange(self.n, process_group, device=dev, slice_floats=sf)
+            else:
+                self.xch = parallel.Exchange(self.n, process_group, sharded=self.sharded, device=dev, slice_floats=sf)
         # Gaussians live on the device in spatial (Morton) order: a CTA's
         # Gaussians then project into a small region of each image, which is
         # what the region-staged kernels exploit.  Per-Gaussian math does not
@@ -293,7 +298,7 @@ class Reconstructor:
         self.perm = morton_order(np.asarray(params)[:, :3], grid.extent)
         params = np.asarray(params, dtype=np.float64)[self.perm]
         rows = self.xch.per * self.world if self.sharded else self.n
-        self._store = torch.zeros((rows, 11), dtype=torch.float64, device=dev)
+        self._store = self.xch.store if self.peer else torch.zeros((rows, 11), dtype=torch.float64, device=dev)
         self._m_store = torch.zeros_like(self._store)
         self._v_store = torch.zeros_like(self._store)
         self._store[: self.n].copy_(torch.as_tensor(np.ascontiguousarray(params)))
@@ -489,6 +494,16 @@ class Reconstructor:
                           ptr(self.v[a:bb]), mode, float(scale), float(cfg.adam_beta1), float(cfg.adam_beta2),
                           float(cfg.adam_epsilon), ptr(hyper), ptr(skip), self.ctx.stream)
 
+        def fused():  # PeerExchange: reduce-scatter + epilogue + Adam + parameter all-gather, one launch
+            per, r = xch.per, self.rank
+            h = hyper if hyper is not None else self._scalar_hyper(*scalars)
+            _lib.call("cgs_peer_epilogue_adam", ptr(xch.acc_ptrs), ptr(xch.store_ptrs), ptr(xch.flag_ptrs), r,
+                      self.world, self.n, per, ptr(self._m_store[r * per:(r + 1) * per]),
+                      ptr(self._v_store[r * per:(r + 1) * per]), mode, float(scale), float(cfg.adam_beta1),
+                      float(cfg.adam_beta2), float(cfg.adam_epsilon), ptr(h), self.ctx.stream)
+
+        if self.peer:
+            return [("dev", local), ("dev", fused)], pipe
         segs = [("dev", local)]
         if xch is not None:
             segs.append(("coll", xch.run))
@@ -498,9 +513,19 @@ class Reconstructor:
         return segs, pipe
 
     def _hyper(self, lr: float, t: int):
+        """Adam's per-step scalars (lr, bc1, bc2) and the step counter t (the peer exchange's epoch)."""
         torch = _torch()
         cfg = self.config
-        return torch.tensor([lr, 1.0 - cfg.adam_beta1 ** t, 1.0 - cfg.adam_beta2 ** t], dtype=torch.float64)
+        return torch.tensor([lr, 1.0 - cfg.adam_beta1 ** t, 1.0 - cfg.adam_beta2 ** t, float(t)],
+                            dtype=torch.float64)
+
+    def _scalar_hyper(self, lr: float, bc1: float, bc2: float):
+        """Eager steps of the peer exchange: this step's scalars in a device tensor (stream-ordered)."""
+        torch = _torch()
+        if getattr(self, "_hyper_dev", None) is None:
+            self._hyper_dev = torch.empty(4, dtype=torch.float64, device=self.ctx.device)
+        self._hyper_dev.copy_(torch.tensor([lr, bc1, bc2, float(self.t + 1)], dtype=torch.float64))
+        return self._hyper_dev
 
     def step(self, indices, lr: float):
         """One step over the global batch ``indices``; returns this rank's per-image losses (device).
@@ -525,7 +550,7 @@ class Reconstructor:
                 "s": torch.empty((b, self.obs_spec.shape[1]), dtype=torch.float32, device=dev) if spec and b else None,
                 "p": torch.empty((max(b, 1), 12), dtype=torch.float64, device=dev),
                 "c": None if self.ctfs is None else torch.empty((max(b, 1), 8), dtype=torch.float64, device=dev),
-                "hyper": torch.empty(3, dtype=torch.float64, device=dev)}
+                "hyper": torch.empty(4, dtype=torch.float64, device=dev)}
 
             def inputs(sl=sl):
                 i = sl["idx"]
@@ -573,7 +598,7 @@ class Reconstructor:
                 sl = {"o": torch.empty(obs.shape, dtype=obs.dtype, device=dev),
                       "p": torch.empty(poses.shape, dtype=poses.dtype, device=dev),
                       "c": None if ctfs is None else torch.empty(ctfs.shape, dtype=ctfs.dtype, device=dev),
-                      "hyper": torch.empty(3, dtype=torch.float64, device=dev), "done": None}
+                      "hyper": torch.empty(4, dtype=torch.float64, device=dev), "done": None}
                 segs, pipe = self._segments(obs.shape[0], global_batch,
                                             lambda: (sl["o"], sl["p"], sl["c"], None), sl["hyper"])
                 sl["runner"], sl["pipe"] = _StepRunner(segs, self.use_graphs, self._whole_graph), pipe

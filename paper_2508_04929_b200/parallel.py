@@ -135,6 +135,60 @@ class Exchange:
             dist.all_gather_into_tensor(store, mine, group=self.group)
 
 
+class PeerExchange(Exchange):
+    """The exchange as ONE kernel over peer memory (``cgs_peer_epilogue_adam``, ``CGS_DP_PEER=1``).
+
+    The accumulator (reduce-scatter layout), the fp64 parameter store (``store``: world x per
+    rows) and a u32 [world + 1] handshake array are allocated in symmetric memory
+    (``torch.distributed._symmetric_memory``) and mapped into every rank; ``acc_ptrs``,
+    ``store_ptrs`` and ``flag_ptrs`` are device arrays of the peers' addresses.  Per step each
+    rank's launch sums its slice of every peer's accumulator (fp64, rank order), runs the
+    epilogue + Adam on it and stores the new rows into every peer's store, with a release /
+    acquire handshake before and after: reduce-scatter, Adam and parameter all-gather in one
+    launch, no NCCL call on the step's data path (the NCCL collectives stay for
+    the rare moment gathers of ``reorder`` / ``moments_host``).  Everything is preallocated and
+    the step has no host-side collective, so it is captured whole in the step's CUDA graph."""
+
+    def __init__(self, n: int, group=None, *, device=None, slice_floats=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        super().__init__(n, group, sharded=True, device=device, slice_floats=slice_floats)
+        grp = group if group is not None else dist.group.WORLD
+        if hasattr(symm_mem, "is_symm_mem_enabled_for_group") and not symm_mem.is_symm_mem_enabled_for_group(
+                grp.group_name):
+            symm_mem.enable_symm_mem_for_group(grp.group_name)
+        self.acc = symm_mem.empty(self.world * self.slice, dtype=torch.float32, device=device)
+        self.store = symm_mem.empty((self.world * self.per, 11), dtype=torch.float64, device=device)
+        # arrive slots + done counter, padded to 16 words
+        self.flags = symm_mem.empty(max(16, self.world + 1), dtype=torch.int32, device=device)
+        self.acc.zero_()
+        self.store.zero_()
+        self.flags.zero_()
+        torch.cuda.synchronize(device)  # zeroed on every rank before any peer can signal into it
+        self.acc_ptrs = self._peer_ptrs(self.acc, grp, device)
+        self.store_ptrs = self._peer_ptrs(self.store, grp, device)
+        self.flag_ptrs = self._peer_ptrs(self.flags, grp, device)
+        dist.barrier(group=group)
+
+    def _peer_ptrs(self, t, group, device):
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+
+        h = symm_mem.rendezvous(t, group)
+        base = h.buffer_ptrs
+        off = t.data_ptr() - base[self.rank]
+        return torch.tensor([int(b) + off for b in base], dtype=torch.int64, device=device)
+
+    @property
+    def capturable(self) -> bool:
+        return True
+
+    def run(self) -> None:  # the exchange is inside cgs_peer_epilogue_adam
+        raise RuntimeError("PeerExchange has no separate collective: the step launches cgs_peer_epilogue_adam")
+
+
 def allreduce_accumulator(acc, group=None, status=None):
     """Sum a flat N*10 (+1) accumulator over ranks in place (one collective); with ``status`` the
     trailing slot carries this rank's skip flag.  Returns the int32 skip status (SKIP_BITS if any

@@ -1174,7 +1174,7 @@ def test_degenerate_rotation_raises_on_device():
         cs.train(cs.Dataset(records, grid), cs.TrainConfig(epochs=1), n_gaussians=8, initial=mix)
 
 
-def _nccl_one_rank_worker(rank, world, port, out_path, sharded):
+def _nccl_one_rank_worker(rank, world, port, out_path, sharded, peer=False):
     import os
     import sys
 
@@ -1184,6 +1184,7 @@ def _nccl_one_rank_worker(rank, world, port, out_path, sharded):
     os.environ["MASTER_PORT"] = str(port)
     os.environ["CGS_DP_EXCHANGE"] = "1"
     os.environ["CGS_DP_SHARDED"] = "1" if sharded else "0"
+    os.environ["CGS_DP_PEER"] = "1" if peer else "0"
     from conftest import ROOT
 
     sys.path.insert(0, ROOT)
@@ -1196,7 +1197,8 @@ def _nccl_one_rank_worker(rank, world, port, out_path, sharded):
     params, obs, poses, ctfs, grid, orders = _dp_inputs(cs2, eng)
     rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=DP_B, process_group=dist.group.WORLD,
                         residency="full")
-    assert rec.xch is not None and rec.xch.capturable and rec._whole_graph and rec.sharded == sharded
+    assert rec.xch is not None and rec.xch.capturable and rec._whole_graph and rec.sharded == (sharded or peer)
+    assert rec.peer == peer
     losses = _dp_run(rec, orders)
     torch.cuda.synchronize()
     captured = all(sl["runner"].captured for sl in rec._idx_slots.values())
@@ -1225,6 +1227,117 @@ def test_nccl_exchange_captured_in_step_graph(tmp_path, sharded):
         port = sk.getsockname()[1]
     out = str(tmp_path / "nccl.npz")
     mp.spawn(_nccl_one_rank_worker, args=(1, port, out, sharded), nprocs=1, join=True)
+    r = np.load(out)
+    assert bool(r["captured"])
+    params, obs, poses, ctfs, grid, orders = _dp_inputs(cs, engine)
+    rec = Reconstructor(grid, params, obs, poses, ctfs, batch_size=DP_B)
+    ref_losses = np.concatenate([x.cpu().numpy() for x in _dp_run(rec, orders)])
+    np.testing.assert_allclose(r["losses"], ref_losses, rtol=1e-5)
+    assert rel_l2(r["params"] - params, rec.params_host() - params) < 1e-4
+    m, v = rec.moments_host()
+    assert rel_l2(r["m"], m) < 1e-4 and rel_l2(r["v"], v) < 1e-4
+
+
+def _peer_sim_step(params, poses, obs, ctfs, grid, world, lr=1e-3, t=1):
+    """One data-parallel step of `world` simulated ranks on one GPU through the fused peer
+    exchange (cgs_peer_epilogue_adam with flags = NULL: ranks launched one after another, no
+    handshake). Returns (stores [world] of [n][11], moments m, v over all rows, skip flags)."""
+    import torch
+
+    from paper_2508_04929_b200 import parallel
+
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(grid.size, grid.extent, grid.pixel_size)
+    n, B = len(params), len(poses)
+    per = parallel.gaussian_slice(n, 0, world)[2]
+    slice_f = int(ctx.lib.cgs_acc_slice_floats(n, per))
+    p_dev = torch.as_tensor(params).cuda()
+    accs, stores, ms, vs = [], [], [], []
+    for r in range(world):
+        acc = torch.zeros(world * slice_f, dtype=torch.float32, device="cuda")
+        idx = parallel.shard(np.arange(B), r, world)
+        if len(idx):
+            pipe = engine.StepPipeline(ctx, n, len(idx), gs)
+            P = torch.as_tensor(poses[idx]).cuda()
+            pipe.clear_status()
+            pipe.forward_backward(p_dev, P, torch.as_tensor(obs[idx]).cuda(), torch.as_tensor(ctfs[idx]).cuda())
+            _lib.call("cgs_reduce_partials_sliced", engine._ptr(pipe.partial), pipe.G, n, per,
+                      engine._ptr(pipe.status), engine._ptr(acc), ctx.stream)
+        else:
+            _lib.call("cgs_reduce_partials_sliced", 0, 0, n, per, 0, engine._ptr(acc), ctx.stream)
+        accs.append(acc)
+        st = torch.zeros((world * per, 11), dtype=torch.float64, device="cuda")
+        st[:n].copy_(p_dev)
+        stores.append(st)
+        ms.append(torch.zeros((per, 11), dtype=torch.float64, device="cuda"))
+        vs.append(torch.zeros((per, 11), dtype=torch.float64, device="cuda"))
+    cfg = cs.TrainConfig()
+    hyper = torch.tensor([lr, 1 - cfg.adam_beta1 ** t, 1 - cfg.adam_beta2 ** t, float(t)], dtype=torch.float64,
+                         device="cuda")
+    acc_p = torch.tensor([a.data_ptr() for a in accs], dtype=torch.int64, device="cuda")
+    st_p = torch.tensor([s.data_ptr() for s in stores], dtype=torch.int64, device="cuda")
+    for r in range(world):
+        _lib.call("cgs_peer_epilogue_adam", engine._ptr(acc_p), engine._ptr(st_p), 0, r, world, n, per,
+                  engine._ptr(ms[r]), engine._ptr(vs[r]), _lib.CGS_MODE["anisotropic"], 1.0 / B,
+                  cfg.adam_beta1, cfg.adam_beta2, cfg.adam_epsilon, engine._ptr(hyper), ctx.stream)
+    torch.cuda.synchronize()
+    m = torch.cat(ms)[:n].cpu().numpy()
+    v = torch.cat(vs)[:n].cpu().numpy()
+    flags = [float(a[r * slice_f + per * 10]) for r, a in enumerate(accs)]
+    return [s[:n].cpu().numpy() for s in stores], m, v, flags
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("poison", [False, True])
+def test_peer_exchange_simulated_ranks_match_single_gpu(world, poison):
+    """The fused peer-memory exchange (reduce-scatter + epilogue + Adam + parameter broadcast in
+    one kernel, cgs_peer_epilogue_adam) for 2 and 3 ranks simulated on one GPU (their launches
+    serialised, no handshake): every rank's parameter store ends bitwise identical, and equals the
+    single-GPU step on the whole batch (the exchange sums per-rank fp32 accumulators, hence the
+    tolerance); a non-finite loss on one rank skips the update on every rank."""
+    import torch
+
+    params, obs, poses, ctfs, grid, _ = _dp_inputs(cs, engine)
+    B = 7
+    obs, poses, ctfs = obs[:B].copy(), poses[:B], ctfs[:B]
+    if poison:
+        obs[B - 1, 3, 3] = np.nan  # the last rank's shard
+    stores, m, v, _ = _peer_sim_step(params, poses, obs, ctfs, grid, world)
+    for s in stores[1:]:
+        assert np.array_equal(s, stores[0])
+    if poison:
+        assert np.array_equal(stores[0], params) and not m.any() and not v.any()
+        return
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(grid.size, grid.extent, grid.pixel_size)
+    cfg = cs.TrainConfig()
+    pipe = engine.StepPipeline(ctx, len(params), B, gs)
+    p = torch.as_tensor(params).cuda()
+    mm, vv = torch.zeros_like(p), torch.zeros_like(p)
+    pipe.forward_backward(p, torch.as_tensor(poses).cuda(), torch.as_tensor(obs).cuda(), torch.as_tensor(ctfs).cuda())
+    pipe.adam(p, mm, vv, scale=1.0 / B, lr=1e-3, beta1=cfg.adam_beta1, beta2=cfg.adam_beta2, eps=cfg.adam_epsilon,
+              t=1)
+    ref = p.cpu().numpy()
+    assert rel_l2(stores[0] - params, ref - params) < 1e-4
+    assert rel_l2(m, mm.cpu().numpy()) < 1e-4 and rel_l2(v, vv.cpu().numpy()) < 1e-4
+
+
+def test_peer_exchange_one_rank_nccl_graph(tmp_path):
+    """The fused peer exchange through Reconstructor (CGS_DP_PEER=1) on real hardware: a 1-rank
+    NCCL group, symmetric-memory buffers (torch.distributed._symmetric_memory), the step with its
+    release/acquire handshakes captured whole in a CUDA graph, two epochs with a reorder (NCCL
+    moment gathers) and a short batch; it equals the plain single-GPU run."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = str(tmp_path / "peer.npz")
+    mp.spawn(_nccl_one_rank_worker, args=(1, port, out, False, True), nprocs=1, join=True)
     r = np.load(out)
     assert bool(r["captured"])
     params, obs, poses, ctfs, grid, orders = _dp_inputs(cs, engine)
