@@ -453,6 +453,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "config": {"workload": WORKLOAD if args.scaling == "weak" else WORKLOAD_STRONG, "n_gaussians": N_GAUSS,
                    "image_px": D, "batch_per_gpu": BATCH,
                    "global_batch": global_batch, "parallelism": f"dp{world}", "ctf": True,
+                   "exchange": (None if world == 1 else args.exchange),
                    "l2": (f"inputs larger than L2: {DATASET}-particle dataset cycled ("
                           + (f"observation spectra {DATASET * D * (D // 2 + 1) * 8 >> 20} MiB"
                              if rec.obs_spec is not None else f"{DATASET * D * D * 4 >> 20} MiB") + ")")},
@@ -491,8 +492,13 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: 256 images per GPU (default); strong: global batch 256 split over the GPUs")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="multi-GPU exchange: NCCL all-reduce (default) or the fused peer-memory kernel "
+                         "(cgs_peer_epilogue_adam, CGS_DP_PEER=1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.exchange == "peer":
+        os.environ["CGS_DP_PEER"] = "1"
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -150,7 +150,8 @@ int cgs_raster_fwd(const float *splat, int64_t n, const double *poses, int32_t B
  * the reference's -sub per pixel, 6.7e-10 of the peak, is below that).
  * Integer sums make the result bitwise deterministic.
  * out f32 [B][D][D] natural layout (used as int32 scratch first); ws holds
- * cgs_render_workspace_bytes(n) bytes.  clamp_count (nullable, device int64)
+ * cgs_render_workspace_bytes(n) bytes, zero-initialised once before its first
+ * use (it carries a completion counter that every launch leaves at 0).  clamp_count (nullable, device int64)
  * is incremented by the number of (image, Gaussian) projections that hit the
  * eigenvalue floor: CLAMP_EVENTS.count += proj.n_clamped per image
  * (splat.py:276-277).  Replaces rasterize (splat.py:263-298) inside the
@@ -165,6 +166,13 @@ int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cg
 int cgs_render_fixed(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, int32_t *out,
                      int64_t *clamp_count, void *ws, void *stream);
 int64_t cgs_render_scale_offset(int64_t n);
+/* K0 (cgs_prepare) and cgs_render_fixed in one: the Gaussians are prepared
+ * into splat (and status) by the render's weight-bound pass, which visits
+ * every Gaussian once in the render's scrambled chunk order; the image is
+ * bitwise that of cgs_prepare + cgs_render_fixed.  Two launches + the output
+ * memset (the training step's K0 + K3). */
+int cgs_prepare_render_fixed(const double *params, int64_t n, float *splat, int32_t *status, const double *poses,
+                             int32_t B, cgs_grid grid, int32_t *out, int64_t *clamp_count, void *ws, void *stream);
 
 /* ---- K4: CTF, centred FFTs and MSE (optics.py:78-141, train.py:114-121,153)
  * ctf_evaluate (optics.py:93-121): H f64 [B][D][D], centred layout. */

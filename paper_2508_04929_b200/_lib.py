@@ -69,6 +69,7 @@ PROTOTYPES = {
     "cgs_render": (ctypes.c_int, [P, I64, P, I32, G, P, P, P, P]),
     "cgs_render_fixed": (ctypes.c_int, [P, I64, P, I32, G, P, P, P, P]),
     "cgs_render_scale_offset": (I64, [I64]),
+    "cgs_prepare_render_fixed": (ctypes.c_int, [P, I64, P, P, P, I32, G, P, P, P, P]),
     "cgs_ctf_evaluate": (ctypes.c_int, [P, I32, G, P, P]),
     "cgs_fft_plan_create": (ctypes.c_int, [I32, I32, ctypes.POINTER(ctypes.c_void_p)]),
     "cgs_fft_plan_destroy": (ctypes.c_int, [P]),

@@ -44,6 +44,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "prepare.cuh"
 
 namespace cgs {
 
@@ -63,7 +64,7 @@ constexpr int kRChunkMin = 512;
 #define CGS_FWD_BAND_KB 64
 #endif
 constexpr int kRBandBytes = CGS_FWD_BAND_KB * 1024;  // int32 accumulator rows per CTA
-constexpr int kWbThreads = 1024;
+constexpr int kWbThreads = 256;  // weight-bound pass: CTA = 256 logical indices (one wave over the SMs at C2)
 constexpr double kFixedRange = 1073741824.0;  // 2^30
 constexpr double kContribRange = 4194304.0;   // 2^22
 #ifndef CGS_FWD_TAIL
@@ -71,39 +72,97 @@ constexpr double kContribRange = 4194304.0;   // 2^22
 #endif
 constexpr float kTailFrac = CGS_FWD_TAIL;      // walk each footprint down to this fraction of its peak
 
-// View-independent peak-weight bound of one Gaussian (see the header); slots
-// 14 / 15 of the splat record hold the smallest and middle activated scale
-// (cgs_prepare).
-__device__ __forceinline__ double weight_bound(const float *__restrict__ splat, int64_t g, double fl) {
-    const float *r = splat + g * CGS_SPLAT_STRIDE;
-    const float2 lm = __ldg(reinterpret_cast<const float2 *>(r + 14));
-    const double lo = lm.x, mid = lm.y, amp = __ldg(r + 3);
+// View-independent peak-weight bound of one Gaussian (see the header) from
+// its f32 record slots amp (3), s_min (14) and s_mid (15) (cgs_prepare).
+__device__ __forceinline__ double weight_bound(float amp_f, float lo_f, float mid_f, double fl) {
+    const double lo = lo_f, mid = mid_f, amp = amp_f;
     const double det = fmax(mid * mid, fl) * fmax(lo * lo, fl);
     // 1.001: headroom for the fp32 evaluation of w inside the kernels
     return 1.001 * amp / (2.0 * kPiD * sqrt(det));
 }
 
-// Sum and max of wb over 1024 consecutive logical indices of one chunk (the
-// chunk's scrambled order g = (i * A) mod n, i in [c chunk, (c+1) chunk)):
-// CTA (c, sub) covers i in [c chunk + 1024 sub, ...), one index per thread, so
-// the pass is one dependent load deep.  Fixed-order reductions: the scales
-// are deterministic.
-__global__ void __launch_bounds__(kWbThreads) wbound_chunk_kernel(const float *__restrict__ splat, int64_t n,
-                                                                  double h, int64_t mulA, int chunk,
-                                                                  double *__restrict__ csum,
-                                                                  float *__restrict__ cmax) {
+__device__ __forceinline__ double unit_scale(double sum, double mx) {
+    double sc = sum > 0.0 ? kFixedRange / sum : 1.0;
+    if (mx > 0.0) sc = fmin(sc, kContribRange / mx);
+    return sc;
+}
+
+// The image-wide unit S from all chunks' sub-block sums / maxima (csum, cmax:
+// total values), run by one warp in a fixed order: lane l of tree w sums the
+// strided entries 32 w + l + 256 k, eight xor-shuffle trees (interleaved for
+// latency), then a serial sum over the trees.
+__device__ __forceinline__ float image_scale(const double *__restrict__ csum, const float *__restrict__ cmax,
+                                             int total) {
+    const int lane = threadIdx.x & 31;
+    double t[8];
+    float m[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        t[w] = 0.0;
+        m[w] = 0.f;
+        for (int i = 32 * w + lane; i < total; i += 256) {
+            t[w] += __ldcg(csum + i);
+            m[w] = fmaxf(m[w], __ldcg(cmax + i));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            t[w] += __shfl_xor_sync(0xffffffffu, t[w], o);
+            m[w] = fmaxf(m[w], __shfl_xor_sync(0xffffffffu, m[w], o));
+        }
+    double s = 0.0;
+    float mx = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        s += t[w];
+        mx = fmaxf(mx, m[w]);
+    }
+    return (float)unit_scale(s, mx);
+}
+
+// Weight-bound pass.  CTA (c, sub) sums wb and takes its max over kWbThreads
+// consecutive logical indices of chunk c (the chunk's scrambled order
+// g = (i * A) mod n, i in [c chunk, (c+1) chunk)), one index per thread, in a
+// fixed order.  The last CTA to finish (a self-resetting counter in the
+// workspace) then derives the units: the image-wide S (image_scale), and per
+// chunk its own unit scale_c = max(unit(chunk sum, chunk max), S) and the
+// band -> image factor S / scale_c.  Deterministic: every sum has a fixed
+// order.  kPrepare: the same CTA first prepares Gaussian g (K0, prepare.cuh)
+// and bounds it from the values it just computed, so the training step's K0,
+// weight bound and unit derivation are one launch (the scrambled order visits
+// every Gaussian exactly once).
+template <bool kPrepare>
+__global__ void __launch_bounds__(kWbThreads) wbound_chunk_kernel(const double *__restrict__ params,
+                                                                  float *__restrict__ splat, int32_t *status,
+                                                                  int64_t n, double h, int64_t mulA, int chunk,
+                                                                  double *__restrict__ csum, float *__restrict__ cmax,
+                                                                  unsigned *__restrict__ counter,
+                                                                  float *__restrict__ gscale,
+                                                                  float *__restrict__ cscale,
+                                                                  float *__restrict__ cratio) {
     const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(n, i0 + chunk);
     const int64_t i = i0 + (int64_t)blockIdx.y * kWbThreads + threadIdx.x;
     double t = 0.0;
     float m = 0.f;
     if (i < i1) {
-        const double wb = weight_bound(splat, (int64_t)(((unsigned long long)i * (unsigned long long)mulA) %
-                                                       (unsigned long long)n), (0.1 * h) * (0.1 * h));
+        const int64_t g = (int64_t)(((unsigned long long)i * (unsigned long long)mulA) % (unsigned long long)n);
+        float3 f;
+        if (kPrepare) {
+            f = prepare_one(params, g, splat, status);
+        } else {
+            const float *r = splat + g * CGS_SPLAT_STRIDE;
+            const float2 lm = __ldg(reinterpret_cast<const float2 *>(r + 14));
+            f = make_float3(__ldg(r + 3), lm.x, lm.y);
+        }
+        const double wb = weight_bound(f.x, f.y, f.z, (0.1 * h) * (0.1 * h));
         t = wb;
         m = (float)wb;
     }
     __shared__ double ws[kWbThreads / 32];
     __shared__ float wm[kWbThreads / 32];
+    __shared__ bool last;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -114,6 +173,7 @@ __global__ void __launch_bounds__(kWbThreads) wbound_chunk_kernel(const float *_
         wm[threadIdx.x >> 5] = m;
     }
     __syncthreads();
+    const int nch = (int)gridDim.x, nsub = (int)gridDim.y;
     if (threadIdx.x < 32) {
         double s = threadIdx.x < kWbThreads / 32 ? ws[threadIdx.x] : 0.0;
         float mx = threadIdx.x < kWbThreads / 32 ? wm[threadIdx.x] : 0.f;
@@ -123,66 +183,37 @@ __global__ void __launch_bounds__(kWbThreads) wbound_chunk_kernel(const float *_
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         }
         if (threadIdx.x == 0) {
-            csum[(int64_t)blockIdx.x * gridDim.y + blockIdx.y] = s;
-            cmax[(int64_t)blockIdx.x * gridDim.y + blockIdx.y] = mx;
+            csum[(int64_t)blockIdx.x * nsub + blockIdx.y] = s;
+            cmax[(int64_t)blockIdx.x * nsub + blockIdx.y] = mx;
+            __threadfence();
+            last = atomicAdd(counter, 1u) == (unsigned)(nch * nsub - 1);
         }
     }
-}
-
-__device__ __forceinline__ double unit_scale(double sum, double mx) {
-    double sc = sum > 0.0 ? kFixedRange / sum : 1.0;
-    if (mx > 0.0) sc = fmin(sc, kContribRange / mx);
-    return sc;
-}
-
-// Image-wide unit S from all chunks (fixed order), then per chunk its own unit
-// scale_c >= S and the band -> image factor S / scale_c <= 1.
-// csum / cmax hold nch x nsub sub-block partials (chunk-major).
-__global__ void __launch_bounds__(256) wbound_scale_kernel(const double *__restrict__ csum,
-                                                           const float *__restrict__ cmax, int nch, int nsub,
-                                                           float *__restrict__ gscale, float *__restrict__ cscale,
-                                                           float *__restrict__ cratio) {
-    __shared__ double ws[8];
-    __shared__ float wm[8];
-    __shared__ float S;
-    double t = 0.0;
-    float m = 0.f;
-    for (int i = threadIdx.x; i < nch * nsub; i += 256) {
-        t += csum[i];
-        m = fmaxf(m, cmax[i]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        t += __shfl_xor_sync(0xffffffffu, t, o);
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        ws[threadIdx.x >> 5] = t;
-        wm[threadIdx.x >> 5] = m;
-    }
     __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // every warp derives S (bitwise the same), then one warp per chunk: its nsub
+    // (<= 32) sub-block values, one per lane, in a fixed xor-shuffle tree
+    const float S = image_scale(csum, cmax, nch * nsub);
+    const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        float mx = 0.f;
-        for (int w = 0; w < 8; ++w) {
-            s += ws[w];
-            mx = fmaxf(mx, wm[w]);
-        }
-        S = (float)unit_scale(s, mx);
         *gscale = S;
+        *counter = 0u;  // ready for the next launch
     }
-    __syncthreads();
-    for (int c = threadIdx.x; c < nch; c += 256) {
-        double cs = 0.0;
-        float cm = 0.f;
-        for (int k = 0; k < nsub; ++k) {
-            cs += csum[c * nsub + k];
-            cm = fmaxf(cm, cmax[c * nsub + k]);
+    for (int c = threadIdx.x >> 5; c < nch; c += kWbThreads / 32) {
+        double cs = lane < nsub ? __ldcg(csum + c * nsub + lane) : 0.0;
+        float cm = lane < nsub ? __ldcg(cmax + c * nsub + lane) : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            cs += __shfl_xor_sync(0xffffffffu, cs, o);
+            cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
         }
-        // scale_c >= S by construction (a chunk's sum and max are <= the image's); fmaxf guards rounding
-        const float sc = fmaxf((float)unit_scale(cs, cm), S);
-        cscale[c] = sc;
-        cratio[c] = S / sc;
+        if (lane == 0) {
+            // scale_c >= S by construction (a chunk's sum and max are <= the image's); fmaxf guards rounding
+            const float sc = fmaxf((float)unit_scale(cs, cm), S);
+            cscale[c] = sc;
+            cratio[c] = S / sc;
+        }
     }
 }
 
@@ -297,7 +328,6 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     const int r0 = blockIdx.z * HB, r1 = min(D, r0 + HB);
     const int npx = (r1 - r0) * D;
     for (int i = threadIdx.x; i < npx; i += kRThreads) band[i] = 0;
-    const float scale = cscale[blockIdx.x];
     const PoseF P = load_pose_f(poses, b);
     const int64_t i_begin = (int64_t)blockIdx.x * chunk;
 #if defined(CGS_FWD_EXP) && CGS_FWD_EXP == 6
@@ -307,6 +337,7 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
 #endif
     const int64_t stepA = (kRThreads * mulA) % n;
     int64_t g = ((i_begin + threadIdx.x) % n) * mulA % n;
+    const float scale = cscale[blockIdx.x];
     int nclamp = 0;
     __syncthreads();
     for (int64_t i = i_begin + threadIdx.x; i < i_end; i += kRThreads) {
@@ -394,20 +425,27 @@ static int64_t fwd_chunks(int64_t n, int64_t ctas_per_chunk, int slots) {
     return best;
 }
 
-// Workspace: [0] image-wide scale (float), [1] pad, then csum f64 [kSubMax mc],
-// cmax f32 [kSubMax mc], cscale, cratio f32 [mc]; mc = the most chunks any
-// split uses, kSubMax = the most 1024-index sub-blocks per chunk.
+// Workspace: [0] image-wide scale (float), [1] the weight-bound pass's
+// completion counter (u32, zero-initialised once by the caller, left 0 by every
+// launch), then csum f64 [kSubMax mc], cmax f32 [kSubMax mc], cscale, cratio
+// f32 [mc]; mc = the most chunks any split uses, kSubMax = the most kWbThreads-index
+// sub-blocks per chunk.
 static int64_t max_chunks(int64_t n) { return (n + kRChunkMin - 1) / kRChunkMin; }
 constexpr int64_t kSubMax = (kRChunk + kWbThreads - 1) / kWbThreads;
+static_assert(kSubMax <= 32, "the weight-bound pass reduces a chunk's sub-blocks in one warp");
 
 extern "C" size_t cgs_render_workspace_bytes(int64_t n) {
     const int64_t mc = max_chunks(n);
     return (size_t)(8 + 12 * kSubMax * mc + 2 * 4 * mc);
 }
 
-static int render_impl(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
-                       int64_t *clamp_count, void *ws, void *stream, bool convert) {
-    if (n <= 0 || B <= 0 || grid.size < 1 || !splat || !poses || !out || !ws) return CGS_ERR_ARG;
+// Two launches (+ the output memset): the weight-bound pass (with params: K0
+// fused into it; its last CTA derives the units) and the render.
+static int render_impl(const double *params, int32_t *status, float *splat, int64_t n, const double *poses,
+                       int32_t B, cgs_grid grid, float *out, int64_t *clamp_count, void *ws, void *stream,
+                       bool convert) {
+    if (n <= 0 || B <= 0 || grid.size < 1 || !splat || !poses || !out || !ws || (params && !status))
+        return CGS_ERR_ARG;
     const int D = grid.size;
     cudaStream_t st = (cudaStream_t)stream;
     const double h = 2.0 * grid.extent / grid.size;
@@ -428,11 +466,18 @@ static int render_impl(const float *splat, int64_t n, const double *poses, int32
     const int64_t mc = max_chunks(n);
     float *gscale = (float *)ws;
     double *csum = (double *)((char *)ws + 8);
+    unsigned *counter = (unsigned *)ws + 1;
     float *cmax = (float *)(csum + kSubMax * mc), *cscale = cmax + kSubMax * mc, *cratio = cscale + mc;
     const int nsub = (chunk + kWbThreads - 1) / kWbThreads;
-    wbound_chunk_kernel<<<dim3((unsigned)nchunks, (unsigned)nsub), kWbThreads, 0, st>>>(splat, n, h, mulA, chunk,
-                                                                                       csum, cmax);
-    wbound_scale_kernel<<<1, 256, 0, st>>>(csum, cmax, (int)nchunks, nsub, gscale, cscale, cratio);
+    const dim3 wg((unsigned)nchunks, (unsigned)nsub);
+    if (params)
+        wbound_chunk_kernel<true><<<wg, kWbThreads, 0, st>>>(params, splat, status, n, h, mulA, chunk, csum, cmax,
+                                                             counter, gscale, cscale, cratio);
+    else
+        wbound_chunk_kernel<false><<<wg, kWbThreads, 0, st>>>(nullptr, splat, nullptr, n, h, mulA, chunk, csum,
+                                                              cmax, counter, gscale, cscale, cratio);
+    rc = check_launch("wbound_chunk_kernel");
+    if (rc) return rc;
     const int64_t count = (int64_t)B * D * D;
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int) * count, st);
     if (e != cudaSuccess) {
@@ -454,12 +499,22 @@ static int render_impl(const float *splat, int64_t n, const double *poses, int32
 
 extern "C" int cgs_render(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid, float *out,
                           int64_t *clamp_count, void *ws, void *stream) {
-    return render_impl(splat, n, poses, B, grid, out, clamp_count, ws, stream, true);
+    return render_impl(nullptr, nullptr, const_cast<float *>(splat), n, poses, B, grid, out, clamp_count, ws, stream,
+                       true);
 }
 
 extern "C" int cgs_render_fixed(const float *splat, int64_t n, const double *poses, int32_t B, cgs_grid grid,
                                 int32_t *out, int64_t *clamp_count, void *ws, void *stream) {
-    return render_impl(splat, n, poses, B, grid, reinterpret_cast<float *>(out), clamp_count, ws, stream, false);
+    return render_impl(nullptr, nullptr, const_cast<float *>(splat), n, poses, B, grid, reinterpret_cast<float *>(out),
+                       clamp_count, ws, stream, false);
+}
+
+extern "C" int cgs_prepare_render_fixed(const double *params, int64_t n, float *splat, int32_t *status,
+                                        const double *poses, int32_t B, cgs_grid grid, int32_t *out,
+                                        int64_t *clamp_count, void *ws, void *stream) {
+    if (!params || !status) return CGS_ERR_ARG;
+    return render_impl(params, status, splat, n, poses, B, grid, reinterpret_cast<float *>(out), clamp_count, ws,
+                       stream, false);
 }
 
 extern "C" int64_t cgs_render_scale_offset(int64_t) { return 0; }

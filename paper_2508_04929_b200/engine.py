@@ -106,10 +106,10 @@ class DeviceContext:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def buf(self, name: str, numel: int, dtype) -> "torch.Tensor":
-        """Grow-only scratch tensor (flat, at least ``numel`` elements)."""
+        """Grow-only scratch tensor (flat, at least ``numel`` elements; zeroed when allocated)."""
         t = self._bufs.get(name)
         if t is None or t.numel() < numel or t.dtype != dtype:
-            t = torch.empty(max(int(numel), 1), dtype=dtype, device=self.device)
+            t = torch.zeros(max(int(numel), 1), dtype=dtype, device=self.device)
             self._bufs[name] = t
         return t[: max(int(numel), 1)]
 
@@ -319,7 +319,8 @@ class StepPipeline:
         self.G = int(ctx.lib.cgs_bwd_groups(self.B, self.ipg))
         self.partial = torch.empty(self.G * n * 10, dtype=torch.float32, device=dev)
         self.plan = ctx.plan(D, self.B)
-        self.render_ws = torch.empty(ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, dtype=torch.float32, device=dev)
+        # zeroed once: the render's weight-bound pass keeps a self-resetting counter in it
+        self.render_ws = torch.zeros(ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, dtype=torch.float32, device=dev)
         spec_elems = int(ctx.lib.cgs_obs_spectrum_elems(D, self.B))
         self.obs_spec = None  # per-step observation records of the spectral K4 (None: real-space K4)
         if spec_elems and os.environ.get("CGS_CTF_SPATIAL", "0") != "1":
@@ -366,18 +367,19 @@ class StepPipeline:
                   _ptr(self.scan_ws), s)
 
     # kernels of libcgs_b200 launched by one forward_backward + adam (bench accounting), direct mode:
-    # prepare, wbound_partial, wbound_scale, raster_fwd_atomic, fixed_to_float, K4, raster_bwd,
+    # wbound (+ prepare), raster_fwd_atomic, fixed_to_float, K4, raster_bwd,
     # epilogue_adam.  K4 is one ctf_mse_fused kernel for D = 32 / 64 / 128; otherwise ctf_multiply x2 +
     # loss_resid around cuFFT's own R2C/C2R kernels (library launches, not counted).
     def own_launches_per_step(self, ctf: bool = True, obs_spectrum: bool = False) -> int:
-        """Kernels of this library per direct-mode step (bench accounting): prepare; weight bound
-        (2) + raster_fwd_atomic (+ fixed_to_float unless the spectral K4 converts on load); K4;
+        """Kernels of this library per direct-mode step (bench accounting): the weight-bound pass
+        (with K0 inside it when the spectral K4 follows, else after a separate prepare) +
+        raster_fwd_atomic (+ fixed_to_float unless the spectral K4 converts on load); K4;
         raster_bwd; epilogue + Adam.  K4 is one kernel (spectral, plus obs_spectrum when the
         batch's records are not precomputed; or the real-space kernel for D = 32/64/128), or
         multiply x2 + loss around cuFFT's own transforms; without a CTF it is the loss/residual
         kernel."""
         spectral = ctf and self.spectral
-        n = 1 + 3 + (0 if spectral else 1) + 1 + 1
+        n = 2 + (0 if spectral else 2) + 1 + 1
         if not ctf:
             return n + 1
         if spectral:
@@ -417,17 +419,19 @@ class StepPipeline:
                 events[name][which].record()
 
         mark("fwd", 0)
-        self._prepare(params)
-        # direct render feeding the spectral K4: the int32 fixed-point image is converted as K4 loads it
+        # direct render feeding the spectral K4: the int32 fixed-point image is converted as K4 loads it,
+        # and K0 runs inside the render's weight-bound pass (cgs_prepare_render_fixed)
         fixed = self.render_mode == "direct" and ctf is not None and self.spectral
         self._render_fixed = fixed
         if fixed:
-            _lib.call("cgs_render_fixed", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid,
-                      _ptr(self.render), _ptr(self.clamp), _ptr(self.render_ws), s)
+            _lib.call("cgs_prepare_render_fixed", _ptr(params), self.n, _ptr(self.splat), _ptr(self.status),
+                      _ptr(poses), self.B, self.grid, _ptr(self.render), _ptr(self.clamp), _ptr(self.render_ws), s)
         elif self.render_mode == "direct":
+            self._prepare(params)
             _lib.call("cgs_render", _ptr(self.splat), self.n, _ptr(poses), self.B, self.grid, _ptr(self.render),
                       _ptr(self.clamp), _ptr(self.render_ws), s)
         else:
+            self._prepare(params)
             self._count(params, poses)
             _lib.call("cgs_bin_scatter", _ptr(self.rects), self.n, self.B, self.D, self.tile, _ptr(self.offs),
                       _ptr(self.items), self.items.numel(), _ptr(self.status), s)

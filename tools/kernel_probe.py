@@ -44,7 +44,7 @@ def main():
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
     splat = engine.prepare(ctx, p, status)
     out = torch.empty((a.B, a.D, a.D), dtype=torch.float32, device="cuda")
-    ws = torch.empty(ctx.lib.cgs_render_workspace_bytes(a.n) // 4 + 1, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(ctx.lib.cgs_render_workspace_bytes(a.n) // 4 + 1, dtype=torch.float32, device="cuda")
     up = torch.randn((a.B, a.D, a.D), generator=torch.Generator(device="cuda").manual_seed(1), device="cuda") * 1e-3
     G = int(ctx.lib.cgs_bwd_groups(a.B, engine.images_per_group_auto(a.n, a.B)))
     part = torch.empty(G * a.n * 10, dtype=torch.float32, device="cuda")

@@ -43,7 +43,7 @@ def main():
     torch.cuda.synchronize()
     ptr = _lib._ptr if hasattr(_lib, "_ptr") else (lambda t: t.data_ptr())
     render2 = torch.empty_like(pipe.render)
-    ws2 = torch.empty_like(pipe.render_ws)
+    ws2 = torch.zeros_like(pipe.render_ws)
     partial2 = torch.empty_like(pipe.partial)
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
