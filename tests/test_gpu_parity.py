@@ -716,6 +716,61 @@ def test_full_size_c2_properties(oracle):
     assert int(status.item()) == 0
 
 
+_C2_POOL_STATE = {}
+
+
+def _c2_oracle_images(idx):
+    """Oracle worker (forked): loss and summed gradients of the C2 step's images ``idx``."""
+    from oracle import cgs_oracle as orc
+
+    st = _C2_POOL_STATE
+    grid, params = st["grid"], st["params"]
+    g = np.zeros_like(params)
+    losses = []
+    for i in idx:
+        W, t = st["poses"][i]
+        H = orc.ctf_evaluate(st["ctfs"][i], grid)
+        loss, gi, *_ = orc.image_step(params, W, t, grid, H, st["obs"][i])
+        losses.append(loss)
+        g += gi
+    return list(idx), losses, g
+
+
+def test_full_c2_batch_gradients_vs_oracle(oracle):
+    """BASELINE configs[1] (C2) at full size through the oracle: 50k init_random Gaussians,
+    B = 256 images of 128^2 with per-image CTFs and noisy observations.  The fused step's 256
+    losses and the batch-mean gradients of all 50k x 11 parameters against the fp64 oracle
+    (train.py:136-161 per image, summed over the batch; the oracle runs over a fork pool of the
+    host's cores), within the north-star tolerances."""
+    import multiprocessing as mp
+    import os
+
+    n, D, B = 50000, 128, 256
+    grid = oracle.Grid(D, 0.5, 1.5)
+    params = oracle.init_random(n, 0, grid)
+    poses = [oracle.sample_pose(np.random.default_rng(1000 + i)) for i in range(B)]
+    cp = []
+    for i in range(B):  # astigmatic: defocus_u != defocus_v at a random angle
+        r = np.random.default_rng(3000 + i)
+        cp.append(oracle.Ctf(*r.uniform(1e4, 2.5e4, 2), float(r.uniform(0.0, np.pi))))
+    ctfs = np.stack([c.as_array() for c in cp])
+    obs = (np.random.default_rng(11).standard_normal((B, D, D)) * 0.05).astype(np.float32)
+    losses, grads, _ = _full_step_device(params, poses, grid, obs, ctfs)
+    _C2_POOL_STATE.update(grid=grid, params=params, poses=poses, ctfs=cp, obs=obs)
+    workers = max(1, min(32, os.cpu_count() or 1))
+    chunks = [list(range(k, B, workers)) for k in range(workers)]
+    with mp.get_context("fork").Pool(workers) as pool:
+        res = pool.map(_c2_oracle_images, chunks)
+    ref_losses = np.empty(B)
+    ref_grads = np.zeros_like(params)
+    for idx, ls, g in res:
+        ref_losses[idx] = ls
+        ref_grads += g
+    ref_grads /= B
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
+
+
 DP_R, DP_B, DP_N = 25, 8, 2000  # 25 records in batches of 8: the last batch (1 image) leaves rank 0 empty
 
 
