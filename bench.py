@@ -253,10 +253,11 @@ class ClockSampler:
                ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
                ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, power: bool = False):
         import threading
 
         self.samples, self.reasons, self.max_mhz, self.nvml = [], set(), None, None
+        self.power, self.watts = power, []
         self._stop = threading.Event()
         self._thread = None
         try:
@@ -275,6 +276,8 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)))
+                if self.power:
+                    self.watts.append(nv.nvmlDeviceGetPowerUsage(self.handle) / 1e3)
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
                 for name, attr in self.REASONS:
                     if mask & getattr(nv, attr, 0):
@@ -303,8 +306,12 @@ class ClockSampler:
                 self.samples, self.max_mhz = [sm], mx
             except Exception:
                 return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+               "samples": len(self.samples)}
+        if self.watts:
+            out["power_w_median"] = statistics.median(self.watts)
+            out["power_w_max"] = max(self.watts)
+        return out
 
 
 def _dataset(rank: int):
@@ -425,6 +432,27 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
     e2e = global_batch * args.steps / (ms_e2e / 1e3)
+
+    # ---- sustained: the device-resident step for a few seconds (clocks and power under load) ----
+    sustained = None
+    if args.sustained_seconds > 0:
+        n_sus = max(args.steps, int(args.sustained_seconds / max(ms_max / args.steps / 1e3, 1e-6)))
+        psampler = ClockSampler(local_rank, power=True).start()
+        barrier()
+        start.record()
+        for k in range(n_sus):
+            o, p, c = dev_batches[k % nb]
+            rec.step_batch(o, p, c, lr, global_batch=global_batch, obs_spec=dev_spectra[k % nb])
+        end.record()
+        barrier()
+        pclk = psampler.stop()
+        ms_sus = start.elapsed_time(end)
+        if dist is not None:
+            t = torch.tensor([ms_sus], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_sus = float(t.item())
+        sustained = {"seconds": ms_sus / 1e3, "steps": n_sus, "value": global_batch * n_sus / (ms_sus / 1e3),
+                     "unit": "images/s", "clocks": pclk}
     h2d = BATCH * D * D * 4 + BATCH * 12 * 8 + BATCH * 8 * 8
     d2h = BATCH * 8
 
@@ -473,6 +501,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                           "peak_basis": "0.164 SM-clk per in-ellipse pair (fwd+bwd issue), SURVEY.md 8(d)"},
         "stage_ms": stage_ms,
         "clocks": clocks,
+        "sustained": sustained,
         "cpu_baseline": cpu,
     }
     if overflow:
@@ -492,6 +521,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: 256 images per GPU (default); strong: global batch 256 split over the GPUs")
+    ap.add_argument("--sustained-seconds", type=float, default=3.0,
+                    help="after the timed region, run the device-resident step this long and report it as "
+                         "'sustained' (clocks and power under load); 0 disables")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="multi-GPU exchange: NCCL all-reduce (default) or the fused peer-memory kernel "
                          "(cgs_peer_epilogue_adam, CGS_DP_PEER=1)")
