@@ -388,7 +388,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         rec.step_batch(o, p, c, lr, global_batch=global_batch, obs_spec=dev_spectra[k % nb])
     barrier()
     sampler = ClockSampler(local_rank).start()
-    stage = {n: [] for n in ("fwd", "ctf", "bwd")}
+    stage = {n: [] for n in ("fwd", "ctf", "bwd", "epi")}
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_pairs = step_bwd_pairs = 0
     start.record()

@@ -477,6 +477,13 @@ class Reconstructor:
                           self.n, xch.per, ptr(pipe.status) if pipe else 0, ptr(xch.acc), self.ctx.stream)
 
         def update():
+            if events is not None and "epi" in events:
+                events["epi"][0].record()
+            _update()
+            if events is not None and "epi" in events:
+                events["epi"][1].record()
+
+        def _update():
             if xch is None:
                 acc, G, a, bb, skip = pipe.partial, pipe.G, 0, self.n, pipe.status
             else:
