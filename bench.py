@@ -242,75 +242,83 @@ def run_reference(args, rank: int, world: int):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled DURING the timed region:
-    a thread polls NVML every 2 ms between start() and stop() (the recipe's
-    clocks line); falls back to one nvidia-smi query when NVML is missing."""
+_POLL_SCRIPT = r"""
+import json, sys, threading, time
+idx, power = int(sys.argv[1]), sys.argv[2] == "1"
+names = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+         ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+         ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+         ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+         ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(idx)
+mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+stop = threading.Event()
+threading.Thread(target=lambda: (sys.stdin.read(), stop.set()), daemon=True).start()
+clk, watts, reasons = [], [], set()
+print("ready", flush=True)
+while not stop.is_set():
+    try:
+        clk.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        if power:
+            watts.append(nv.nvmlDeviceGetPowerUsage(h) / 1e3)
+        m = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        for n, a in names:
+            if m & getattr(nv, a, 0):
+                reasons.add(n)
+    except Exception:
+        pass
+    time.sleep(0.002)
+print(json.dumps({"clk": clk, "watts": watts, "reasons": sorted(reasons), "max": mx}), flush=True)
+"""
 
-    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
-               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
-               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
-               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
-               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region (the
+    recipe's clocks line): a child process polls NVML every 2 ms between start() and stop(),
+    so the sampling does not compete with the launching thread for the GIL; optionally board
+    power.  Falls back to one nvidia-smi query when NVML is missing."""
 
     def __init__(self, index: int, power: bool = False):
-        import threading
-
-        self.samples, self.reasons, self.max_mhz, self.nvml = [], set(), None, None
-        self.power, self.watts = power, []
-        self._stop = threading.Event()
-        self._thread = None
-        try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            self.nvml = pynvml
-            self.handle = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
-        except Exception:
-            self.nvml = None
-        self.index = index
-
-    def _poll(self):
-        nv = self.nvml
-        while not self._stop.is_set():
-            try:
-                self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)))
-                if self.power:
-                    self.watts.append(nv.nvmlDeviceGetPowerUsage(self.handle) / 1e3)
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
-                for name, attr in self.REASONS:
-                    if mask & getattr(nv, attr, 0):
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            self._stop.wait(0.002)
+        self.index, self.power = index, power
+        self.proc = None
 
     def start(self):
-        import threading
-
-        if self.nvml is not None:
-            self._thread = threading.Thread(target=self._poll, daemon=True)
-            self._thread.start()
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _POLL_SCRIPT, str(self.index), "1" if self.power else "0"],
+                                         stdin=subprocess.PIPE, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            if self.proc.stdout.readline().strip() != "ready":
+                raise RuntimeError("sampler did not start")
+        except Exception:
+            if self.proc is not None:
+                self.proc.kill()
+            self.proc = None
         return self
 
     def stop(self):
-        if self._thread is not None:
-            self._stop.set()
-            self._thread.join()
-        if not self.samples:  # no NVML: one nvidia-smi query right after the region
+        res = None
+        if self.proc is not None:
+            try:
+                out, _ = self.proc.communicate(input="", timeout=30)
+                res = json.loads(out.strip().splitlines()[-1])
+            except Exception:
+                self.proc.kill()
+                res = None
+        if not res or not res["clk"]:  # no NVML: one nvidia-smi query right after the region
             try:
                 out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits",
                                       "-i", str(self.index)], capture_output=True, text=True, timeout=10).stdout
                 sm, mx = (float(v) for v in out.strip().split(",")[:2])
-                self.samples, self.max_mhz = [sm], mx
+                return {"sm_mhz": sm, "sm_max_mhz": mx, "reasons": [], "samples": 1, "source": "nvidia-smi after"}
             except Exception:
                 return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
-        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-               "samples": len(self.samples)}
-        if self.watts:
-            out["power_w_median"] = statistics.median(self.watts)
-            out["power_w_max"] = max(self.watts)
+        out = {"sm_mhz": statistics.median(res["clk"]), "sm_max_mhz": res["max"], "reasons": res["reasons"],
+               "samples": len(res["clk"])}
+        if res["watts"]:
+            out["power_w_median"] = statistics.median(res["watts"])
+            out["power_w_max"] = max(res["watts"])
         return out
 
 
