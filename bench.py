@@ -345,12 +345,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_2508_04929_b200 import engine
     from paper_2508_04929_b200.optimize import Reconstructor
 
+    if os.environ.get("CGS_BENCH_BACKEND", "nccl") != "nccl":  # test mode: ranks may share a GPU
+        local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # CGS_BENCH_BACKEND=gloo: host-side collectives, so several ranks can share one GPU to test
+        # the multi-rank bench logic (the numbers are not multi-GPU numbers)
+        backend = os.environ.get("CGS_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=torch.device("cuda", local_rank) if backend == "nccl" else None)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_seconds)
