@@ -17,6 +17,7 @@
 #include <cstdio>
 
 #include "common.cuh"
+#include "linefft.cuh"
 
 namespace cgs {
 
@@ -871,7 +872,9 @@ __global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kerne
         row[0] = v.x; row[1] = v.y; row[2] = v.z; row[3] = v.w;
     }
     __syncthreads();
+#if !defined(CGS_SPEC_EXP) || !(CGS_SPEC_EXP & 1)  // timing experiments only: 1 skips the forward, 2 the inverse
     r2c_2d<R>(X, F);
+#endif
     __syncthreads();
     // F(r) = H F(render) - O (H = Hh D^2, exact: D^2 is a power of two); loss; then
     // the CTF^T filter and the 2/D^2 residual scale in place
@@ -899,7 +902,11 @@ __global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kerne
         loss[b] = l;
         if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
     }
+#if !defined(CGS_SPEC_EXP) || !(CGS_SPEC_EXP & 2)
     c2r_2d<R>(X, F);
+#else
+    __syncthreads();
+#endif
     float4 *u4 = reinterpret_cast<float4 *>(upstream + (int64_t)b * D * D);
     if (kRowPair) {  // float4 i = pixels (2j, x), (2j+1, x), (2j, x+1), (2j+1, x+1)
         for (int i = threadIdx.x; i < D * D / 4; i += kR2cThreads) {
@@ -916,6 +923,257 @@ __global__ void __launch_bounds__(kR2cThreads, CGS_SPEC_MINB) ctf_mse_spec_kerne
     }
 }
 
+// ---------------------------------------------------------------------------
+// The spectral K4 and its observation records on line FFTs (linefft.cuh):
+// one length-D complex transform per group of 8 threads, natural order.
+// Shared memory: X complex [D][S], S = D/2 + 2, and the step-A twiddles.
+// Forward real 2-D transform of a real image:
+//  * rows: pair row j (rows 2j, 2j+1) sits in slots [2jS, 2jS + D) as
+//    z[x] = (img[2j][x], img[2j+1][x]); one line FFT gives Z = X_2j + i X_2j+1,
+//    separated into X_2j(k) = (Z(k) + conj Z(-k)) / 2 -> slot 2jS + k and
+//    X_2j+1(k) = (Z(k) - conj Z(-k)) / 2i -> slot (2j+1)S + k, k = 0..D/2;
+//  * columns kx = 1..D/2-1: one line each (natural ky).  Columns 0 and D/2
+//    are real sequences in y (the DC and Nyquist bins of real rows), so they
+//    share one line, z = X(., 0) + i X(., D/2), whose spectrum
+//    Zp = F0 + i F_D/2 stays packed in column 0: D/2 lines per pass, one per
+//    group of a CTA of 4D threads.
+// The filter acts on the packed column as on the pair kernel's two images
+// (ctf_mse_fused_kernel): H0 F0 + i HN F_D/2 = Pc Zp(ky) + Qc conj Zp(-ky)
+// with Pc, Qc = (H(ky, 0) +- H(ky, D/2)) / 2, and Parseval gives
+// sum_ky |F0|^2 + |F_D/2|^2 = sum_ky |Zp|^2.  The inverse runs the columns
+// (the packed line unpacks into columns 0 and D/2) and then the pair rows,
+// whose line output z[x] = (row 2j, row 2j+1) at x is exactly the row-pair
+// upstream layout.
+// Bank layout: S = D/2 + 2 = 2 mod 16 puts the 8 rows a column group reads
+// at once on distinct bank pairs, and pair rows j, j + 2 (the two groups of a
+// half warp in the row passes) 16 banks apart.
+template <int D>
+struct SpecLf {
+    static constexpr int V = D / 8, S = D / 2 + 2, P = D / 2 + 1, NT = 4 * D;
+    static constexpr size_t smem = (size_t)(D * S + V * 8) * sizeof(float2);
+    static __device__ __forceinline__ int pair_row() {  // this group's pair row, interleaved per warp
+        const int g = threadIdx.x >> 3, q = g & 3;
+        return (g & ~3) + ((q & 1) << 1) + (q >> 1);
+    }
+};
+
+// load pair rows: (img[2j][x], img[2j+1][x]) -> slot 2jS + x (float4 loads, 16-byte stores)
+template <int D, bool kFixed>
+__device__ __forceinline__ void lf_load_pairs(float2 *X, const float *__restrict__ img, float inv_scale) {
+    using G = SpecLf<D>;
+    const float4 *r4 = reinterpret_cast<const float4 *>(img);
+    for (int i = threadIdx.x; i < D * D / 8; i += G::NT) {
+        const int j = i / (D / 4), x = 4 * (i - j * (D / 4));
+        const float4 a = __ldg(r4 + (2 * j) * (D / 4) + x / 4), b = __ldg(r4 + (2 * j + 1) * (D / 4) + x / 4);
+        float4 u, w;
+        if (kFixed) {
+            u = make_float4((float)__float_as_int(a.x) * inv_scale, (float)__float_as_int(b.x) * inv_scale,
+                            (float)__float_as_int(a.y) * inv_scale, (float)__float_as_int(b.y) * inv_scale);
+            w = make_float4((float)__float_as_int(a.z) * inv_scale, (float)__float_as_int(b.z) * inv_scale,
+                            (float)__float_as_int(a.w) * inv_scale, (float)__float_as_int(b.w) * inv_scale);
+        } else {
+            u = make_float4(a.x, b.x, a.y, b.y);
+            w = make_float4(a.z, b.z, a.w, b.w);
+        }
+        float4 *dst = reinterpret_cast<float4 *>(X + 2 * j * G::S + x);
+        dst[0] = u;
+        dst[1] = w;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void lf_rows_forward(float2 *X, const float2 *twt) {
+    using G = SpecLf<D>;
+    constexpr int S = G::S, NK = D / 16 + 1;
+    const int t = threadIdx.x & 7;
+    float2 *reg = X + 2 * G::pair_row() * S;
+    lfft::line<D, -1, true>(
+        t, twt, [&](int n) { return reg[n]; }, [&](int s) { return reg + s; },
+        [&](int k, float2 v) { reg[k] = v; });
+    __syncwarp();
+    float2 a[NK], c[NK];
+#pragma unroll
+    for (int m = 0; m < NK; ++m) {
+        const int k = t + 8 * m;
+        if (k <= D / 2) {
+            const float2 zk = reg[k], zn = reg[(D - k) & (D - 1)];
+            a[m] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));  // (Z(k) + conj Z(-k)) / 2
+            c[m] = make_float2(0.5f * (zk.y + zn.y), 0.5f * (zn.x - zk.x));  // (Z(k) - conj Z(-k)) / 2i
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < NK; ++m) {
+        const int k = t + 8 * m;
+        if (k <= D / 2) {
+            reg[k] = a[m];
+            reg[S + k] = c[m];
+        }
+    }
+}
+
+template <int D, int SIGN>
+__device__ __forceinline__ void lf_cols(float2 *X, const float2 *twt) {
+    using G = SpecLf<D>;
+    constexpr int S = G::S;
+    const int c = threadIdx.x >> 3, t = threadIdx.x & 7;
+    float2 *col = X + c;
+    lfft::line<D, SIGN, true>(
+        t, twt,
+        [&](int n) {
+            float2 v = col[n * S];
+            if (SIGN < 0 && c == 0) v.y = col[n * S + D / 2].x;  // pack the real columns 0 and D/2
+            return v;
+        },
+        [&](int s) { return col + s * S; },
+        [&](int k, float2 v) {
+            if (SIGN > 0 && c == 0) {  // unpack
+                col[k * S] = make_float2(v.x, 0.f);
+                col[k * S + D / 2] = make_float2(v.y, 0.f);
+            } else {
+                col[k * S] = v;
+            }
+        });
+}
+
+// inverse pair rows (unscaled) straight to the upstream image in HBM
+template <int D, bool kRowPair>
+__device__ __forceinline__ void lf_rows_inverse(float2 *X, const float2 *twt, float *__restrict__ up) {
+    using G = SpecLf<D>;
+    constexpr int S = G::S;
+    const int t = threadIdx.x & 7, j = G::pair_row();
+    float2 *reg = X + 2 * j * S;
+    lfft::line<D, 1, false>(
+        t, twt,
+        [&](int k) {
+            const bool lo = k <= D / 2;
+            const int kk = lo ? k : D - k;
+            float2 a = reg[kk], c = reg[S + kk];
+            if (!lo) {
+                a.y = -a.y;
+                c.y = -c.y;
+            }
+            return make_float2(a.x - c.y, a.y + c.x);  // X_2j(k) + i X_2j+1(k)
+        },
+        [&](int s) { return reg + s; },
+        [&](int x, float2 v) {
+            if (kRowPair) {
+                reinterpret_cast<float2 *>(up)[j * D + x] = v;
+            } else {
+                up[(2 * j) * D + x] = v.x;
+                up[(2 * j + 1) * D + x] = v.y;
+            }
+        });
+}
+
+template <int D>
+__global__ void __launch_bounds__(SpecLf<D>::NT, 2) obs_spectrum_lf_kernel(const float *__restrict__ obs,
+                                                                            const double *__restrict__ ctf,
+                                                                            double pix, float2 *__restrict__ spec) {
+    using G = SpecLf<D>;
+    constexpr int S = G::S, P = G::P;
+    extern __shared__ float2 X[];
+    float2 *twt = X + D * S;
+    __shared__ CtfConst cc;
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        CtfConst c = load_ctf(ctf + 8 * (int64_t)b, D, pix);
+        c.inv_dA = 1.0 / c.dA;
+        c.pl = kPiD * c.lam;
+        c.cs3 = 0.5 * kPiD * c.cs * c.lam * c.lam * c.lam;
+        cc = c;
+    }
+    lfft::init_twiddles<D>(twt, threadIdx.x, G::NT);
+    lf_load_pairs<D, false>(X, obs + (int64_t)b * D * D, 1.f);
+    __syncthreads();
+    lf_rows_forward<D>(X, twt);
+    __syncthreads();
+    lf_cols<D, -1>(X, twt);
+    __syncthreads();
+    // record: F(obs) [D][P] natural (the packed column in kx = 0, kx = D/2 zero), then H_sym / D^2 [D][P]
+    float2 *dst = spec + (int64_t)b * (3 * D * P / 2);
+    float *hd = reinterpret_cast<float *>(dst + D * P);
+    for (int i = threadIdx.x; i < D * P; i += G::NT) {
+        const int ky = i / P, kx = i - ky * P;
+        dst[i] = kx == D / 2 ? make_float2(0.f, 0.f) : X[ky * S + kx];
+        hd[i] = ctf_sym(cc, D, ky, kx) * (1.f / ((float)D * (float)D));
+    }
+}
+
+template <int D, bool kFixed, bool kRowPair>
+__global__ void __launch_bounds__(SpecLf<D>::NT, 2) ctf_mse_spec_lf_kernel(
+    const float *__restrict__ render, const float *__restrict__ render_scale, const float2 *__restrict__ obs_spec,
+    float *__restrict__ upstream, double *__restrict__ loss, int32_t *status) {
+    using G = SpecLf<D>;
+    constexpr int S = G::S, P = G::P;
+    extern __shared__ float2 X[];
+    float2 *twt = X + D * S;
+    __shared__ double scratch[G::NT / 32];
+    const int b = blockIdx.x;
+    const float2 *O = obs_spec + (int64_t)b * (3 * D * P / 2);
+    const float *Hh = reinterpret_cast<const float *>(O + D * P);  // H_sym / D^2, natural [ky][kx]
+    {  // warm L2 with the observation record, read after the forward transform
+        const char *ob = reinterpret_cast<const char *>(O);
+        for (int off = threadIdx.x * 128; off < 3 * D * P * (int)sizeof(float); off += G::NT * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
+    }
+    lfft::init_twiddles<D>(twt, threadIdx.x, G::NT);
+    lf_load_pairs<D, kFixed>(X, render + (int64_t)b * D * D, kFixed ? 1.f / __ldg(render_scale) : 1.f);
+    __syncthreads();
+    lf_rows_forward<D>(X, twt);
+    __syncthreads();
+    lf_cols<D, -1>(X, twt);
+    __syncthreads();
+    // F(r) = H F(render) - O (H = Hh D^2, exact: D^2 is a power of two); loss by
+    // Parseval (weight 2 on kx = 1..D/2-1, 1 on the packed column); then CTF^T
+    // and the 2/D^2 residual scale in place
+    const float d2 = (float)(D * D), sc = 2.f / (float)(D * D);
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < D * P; i += G::NT) {
+        const int ky = i / P, kx = i - ky * P;
+        if (kx == 0 || kx == D / 2) continue;
+        const float h = __ldg(Hh + i);
+        const float2 z = X[ky * S + kx], o = __ldg(O + i);
+        const float hd = h * d2;
+        const float rx = fmaf(hd, z.x, -o.x), ry = fmaf(hd, z.y, -o.y);
+        acc += 2.0 * ((double)rx * rx + (double)ry * ry);
+        const float hs = h * sc;
+        X[ky * S + kx] = make_float2(hs * rx, hs * ry);
+    }
+    for (int ky = threadIdx.x; ky <= D / 2; ky += G::NT) {  // packed column, pairs (ky, -ky)
+        const int ny = (D - ky) & (D - 1);
+        const float2 zk = X[ky * S], zn = X[ny * S], ok = __ldg(O + ky * P), on = __ldg(O + ny * P);
+        const float h0k = __ldg(Hh + ky * P), hnk = __ldg(Hh + ky * P + D / 2);
+        const float h0n = __ldg(Hh + ny * P), hnn = __ldg(Hh + ny * P + D / 2);
+        const float pk = 0.5f * (h0k + hnk), qk = 0.5f * (h0k - hnk);
+        const float pn = 0.5f * (h0n + hnn), qn = 0.5f * (h0n - hnn);
+        // r(k) = d2 (Pc Zp(k) + Qc conj Zp(-k)) - Op(k)
+        const float2 rk = make_float2(fmaf(d2, fmaf(pk, zk.x, qk * zn.x), -ok.x),
+                                      fmaf(d2, fmaf(pk, zk.y, -qk * zn.y), -ok.y));
+        const float2 rn = make_float2(fmaf(d2, fmaf(pn, zn.x, qn * zk.x), -on.x),
+                                      fmaf(d2, fmaf(pn, zn.y, -qn * zk.y), -on.y));
+        acc += (double)rk.x * rk.x + (double)rk.y * rk.y;
+        if (ny != ky) acc += (double)rn.x * rn.x + (double)rn.y * rn.y;
+        // CTF^T on the packed residual, the same way, times 2/D^2
+        X[ky * S] = make_float2(sc * fmaf(pk, rk.x, qk * rn.x), sc * fmaf(pk, rk.y, -qk * rn.y));
+        if (ny != ky) X[ny * S] = make_float2(sc * fmaf(pn, rn.x, qn * rk.x), sc * fmaf(pn, rn.y, -qn * rk.y));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tsum = 0.0;
+        for (int w = 0; w < G::NT / 32; ++w) tsum += scratch[w];
+        const double l = poison_loss(tsum / ((double)D * D * (double)D * D), status);
+        loss[b] = l;
+        if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
+    }
+    lf_cols<D, 1>(X, twt);
+    __syncthreads();
+    lf_rows_inverse<D, kRowPair>(X, twt, upstream + (int64_t)b * D * D);
+}
+
 template <int R>
 static int launch_obs_spectrum(const float *obs, const double *ctf, double pix, float *spec, int B,
                                cudaStream_t st) {
@@ -923,8 +1181,17 @@ static int launch_obs_spectrum(const float *obs, const double *ctf, double pix, 
     const size_t smem = (size_t)D * P * sizeof(float2);
     const int rc = ensure_smem_limit((const void *)obs_spectrum_kernel<R>, smem, "obs_spectrum_kernel");
     if (rc) return rc;
+#ifdef CGS_SPEC_V1
     obs_spectrum_kernel<R><<<B, kR2cThreads, smem, st>>>(obs, ctf, pix, reinterpret_cast<float2 *>(spec));
     return check_launch("obs_spectrum_kernel");
+#else
+    (void)smem;
+    using G = SpecLf<D>;
+    const int rc2 = ensure_smem_limit((const void *)obs_spectrum_lf_kernel<D>, G::smem, "obs_spectrum_lf_kernel");
+    if (rc2) return rc2;
+    obs_spectrum_lf_kernel<D><<<B, G::NT, G::smem, st>>>(obs, ctf, pix, reinterpret_cast<float2 *>(spec));
+    return check_launch("obs_spectrum_lf_kernel");
+#endif
 }
 
 template <int R, bool kFixed, bool kRowPair>
@@ -934,9 +1201,20 @@ static int launch_ctf_mse_spec_t(const float *render, const float *render_scale,
     const size_t smem = (size_t)D * P * sizeof(float2);
     const int rc = ensure_smem_limit((const void *)ctf_mse_spec_kernel<R, kFixed, kRowPair>, smem, "ctf_mse_spec_kernel");
     if (rc) return rc;
+#ifdef CGS_SPEC_V1
     ctf_mse_spec_kernel<R, kFixed, kRowPair><<<B, kR2cThreads, smem, st>>>(
         render, render_scale, reinterpret_cast<const float2 *>(spec), upstream, loss, status);
     return check_launch("ctf_mse_spec_kernel");
+#else
+    (void)smem;
+    using G = SpecLf<D>;
+    const int rc2 = ensure_smem_limit((const void *)ctf_mse_spec_lf_kernel<D, kFixed, kRowPair>, G::smem,
+                                      "ctf_mse_spec_lf_kernel");
+    if (rc2) return rc2;
+    ctf_mse_spec_lf_kernel<D, kFixed, kRowPair><<<B, G::NT, G::smem, st>>>(
+        render, render_scale, reinterpret_cast<const float2 *>(spec), upstream, loss, status);
+    return check_launch("ctf_mse_spec_lf_kernel");
+#endif
 }
 
 template <int R, bool kFixed>
