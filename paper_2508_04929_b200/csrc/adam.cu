@@ -9,6 +9,7 @@
 // fp64 master copies, so tiny late-epoch updates survive as in the reference).
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include <algorithm>
 
@@ -22,21 +23,34 @@ __device__ __forceinline__ double sigmoid_e(double x) {
     return x >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
 }
 
-// grads[11] = scale * chain(acc) for one Gaussian
-__device__ void chain_grads(const double *__restrict__ raw, const double acc[10], double scale,
-                            int mode, double out[11]) {
-    double s[3], sig[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        s[j] = softplus_e(raw[3 + j]);
-        sig[j] = sigmoid_e(raw[3 + j]);
-    }
+// The transcendental part of the chain for one Gaussian (softplus / sigmoid of
+// the scales, sigmoid of the amplitude, the normalised quaternion): gmm.py:76-124.
+struct ChainPre {
+    double s[3], sig[3], sig_amp, inv, w, x, y, z;
+};
+
+__device__ __forceinline__ void chain_pre_scale(const double *__restrict__ raw, int j, double &s, double &sig) {
+    s = softplus_e(raw[3 + j]);
+    sig = sigmoid_e(raw[3 + j]);
+}
+
+__device__ __forceinline__ void chain_pre_quat(const double *__restrict__ raw, ChainPre &c) {
     double qw = raw[6], qx = raw[7], qy = raw[8], qz = raw[9];
     double qnorm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
     bool ok = qnorm > 0.0 && isfinite(qnorm);
     double inv = ok ? 1.0 / qnorm : 0.0;
-    double w = qw * inv, x = qx * inv, y = qy * inv, z = qz * inv;
-    if (!ok) w = 1.0;
+    c.inv = inv;
+    c.w = ok ? qw * inv : 1.0;
+    c.x = qx * inv;
+    c.y = qy * inv;
+    c.z = qz * inv;
+}
+
+// grads[11] = scale * chain(acc) from the transcendentals (splat.py:344-381)
+__device__ __forceinline__ void chain_post(const ChainPre &c, const double acc[10], double scale, int mode,
+                                           double out[11]) {
+    const double w = c.w, x = c.x, y = c.y, z = c.z, inv = c.inv;
+    const double *s = c.s, *sig = c.sig;
     double R[9];
     R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
     R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
@@ -72,11 +86,22 @@ __device__ void chain_grads(const double *__restrict__ raw, const double acc[10]
     out[7] = scale * (d1 - dot * x) * inv;
     out[8] = scale * (d2 - dot * y) * inv;
     out[9] = scale * (d3 - dot * z) * inv;
-    out[10] = scale * acc[0] * sigmoid_e(raw[10]);
+    out[10] = scale * acc[0] * c.sig_amp;
     if (mode == CGS_MODE_ISOTROPIC) {  // train.py:157-159
         double t = out[3] + out[4] + out[5];
         out[3] = out[4] = out[5] = t;
     }
+}
+
+// grads[11] = scale * chain(acc) for one Gaussian
+__device__ void chain_grads(const double *__restrict__ raw, const double acc[10], double scale,
+                            int mode, double out[11]) {
+    ChainPre c;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) chain_pre_scale(raw, j, c.s[j], c.sig[j]);
+    chain_pre_quat(raw, c);
+    c.sig_amp = sigmoid_e(raw[10]);
+    chain_post(c, acc, scale, mode, out);
 }
 
 __device__ __forceinline__ void sum_groups(const float *__restrict__ part, int G, int64_t n,
@@ -207,6 +232,125 @@ __global__ void epilogue_adam_kernel(const float *__restrict__ part, int G, int6
     }
 }
 
+// The epilogue + Adam spread over a CTA of 256 threads per 64 Gaussians (the
+// default; epilogue_adam_kernel above runs one thread per Gaussian end to end).
+// One thread per Gaussian left only ~10 warps per SM with ~3000 dependent
+// instructions each (26-group sums, seven fp64 transcendentals, 11 x Adam's
+// divisions and square root), so the launch was latency-bound (25 us at C2).
+// Here the work splits by kind, with the same arithmetic in the same order
+// (bitwise the same parameters):
+//  (1) transcendentals, 4 threads per Gaussian: scale j's softplus / sigmoid
+//      (j < 3), or the amplitude's sigmoid and the normalised quaternion;
+//  (2) group sums, coalesced: float f of the block's 64 x 10 contiguous
+//      accumulator floats, summed over the groups in order in fp64;
+//  (3) the chain's algebra, one thread per Gaussian;
+//  (4) Adam, one thread per element of the block's 64 x 11 contiguous
+//      parameters (coalesced p, m, v).
+constexpr int kEpiThreads = 256, kEpiGauss = 64;
+#ifndef CGS_EPI_MINB
+#define CGS_EPI_MINB 4
+#endif
+
+__global__ void __launch_bounds__(kEpiThreads, CGS_EPI_MINB) epilogue_adam_wide_kernel(
+    const float *__restrict__ part, int G, int64_t n, double *__restrict__ params, double *__restrict__ m,
+    double *__restrict__ v, int mode, double scale, double lr, double b1, double b2, double eps, double bc1,
+    double bc2, const int32_t *__restrict__ skip, const double *__restrict__ hyper) {
+    if (skip && (*skip & (CGS_STATUS_BIN_OVERFLOW | CGS_STATUS_NONFINITE_LOSS | CGS_STATUS_NONFINITE_PARAMS))) return;
+    if (hyper) {
+        lr = hyper[0];
+        bc1 = hyper[1];
+        bc2 = hyper[2];
+    }
+    __shared__ double sacc[kEpiGauss * 10];
+    __shared__ double sgr[kEpiGauss * 11];
+    __shared__ double ss[3][kEpiGauss], ssig[3][kEpiGauss], sq[6][kEpiGauss];
+    const int tid = threadIdx.x;
+    const int64_t g0 = (int64_t)blockIdx.x * kEpiGauss;
+    const int ng = (int)min((int64_t)kEpiGauss, n - g0);
+    {  // (1)
+        const int j = tid >> 6, i = tid & (kEpiGauss - 1);
+        if (i < ng) {
+            const double *raw = params + (g0 + i) * 11;
+            if (j < 3) {
+                chain_pre_scale(raw, j, ss[j][i], ssig[j][i]);
+            } else {
+                ChainPre c;
+                chain_pre_quat(raw, c);
+                sq[0][i] = c.inv;
+                sq[1][i] = c.w;
+                sq[2][i] = c.x;
+                sq[3][i] = c.y;
+                sq[4][i] = c.z;
+                sq[5][i] = sigmoid_e(raw[10]);
+            }
+        }
+    }
+    {  // (2): up to three floats per thread, three independent chains
+        const int nf = ng * 10;
+        const float *base = part + g0 * 10;
+        const int64_t gs = n * 10;
+        const int f0 = tid, f1 = tid + kEpiThreads, f2 = tid + 2 * kEpiThreads;
+        const bool u0 = f0 < nf, u1 = f1 < nf, u2 = f2 < nf;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        int k = 0;
+        for (; k + 4 <= G; k += 4) {
+            float x0[4], x1[4], x2[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float *p = base + (k + q) * gs;
+                x0[q] = u0 ? __ldg(p + f0) : 0.f;
+                x1[q] = u1 ? __ldg(p + f1) : 0.f;
+                x2[q] = u2 ? __ldg(p + f2) : 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a0 += (double)x0[q];
+                a1 += (double)x1[q];
+                a2 += (double)x2[q];
+            }
+        }
+        for (; k < G; ++k) {
+            const float *p = base + k * gs;
+            a0 += (double)(u0 ? __ldg(p + f0) : 0.f);
+            a1 += (double)(u1 ? __ldg(p + f1) : 0.f);
+            a2 += (double)(u2 ? __ldg(p + f2) : 0.f);
+        }
+        if (u0) sacc[f0] = a0;
+        if (u1) sacc[f1] = a1;
+        if (u2) sacc[f2] = a2;
+    }
+    __syncthreads();
+    if (tid < ng) {  // (3)
+        ChainPre c;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            c.s[j] = ss[j][tid];
+            c.sig[j] = ssig[j][tid];
+        }
+        c.inv = sq[0][tid];
+        c.w = sq[1][tid];
+        c.x = sq[2][tid];
+        c.y = sq[3][tid];
+        c.z = sq[4][tid];
+        c.sig_amp = sq[5][tid];
+        double acc[10], gr[11];
+#pragma unroll
+        for (int j = 0; j < 10; ++j) acc[j] = sacc[tid * 10 + j];
+        chain_post(c, acc, scale, mode, gr);
+#pragma unroll
+        for (int j = 0; j < 11; ++j) sgr[tid * 11 + j] = gr[j];
+    }
+    __syncthreads();
+    double *pb = params + g0 * 11, *mb = m + g0 * 11, *vb = v + g0 * 11;
+    for (int e = tid; e < ng * 11; e += kEpiThreads) {  // (4)
+        double pj = pb[e], mj = mb[e], vj = vb[e];
+        adam_elem(pj, sgr[e], mj, vj, lr, b1, b2, eps, bc1, bc2);
+        pb[e] = pj;
+        mb[e] = mj;
+        vb[e] = vj;
+    }
+}
+
 // ---- fused peer-memory exchange: reduce-scatter + epilogue + Adam + parameter broadcast ----
 //
 // Data parallel over NVLink / NVSwitch without NCCL on the step's data path
@@ -322,6 +466,12 @@ __global__ void __launch_bounds__(kPeerThreads) peer_epilogue_adam_kernel(
 
 using namespace cgs;
 
+// A/B switch: CGS_EPI_NARROW=1 runs the one-thread-per-Gaussian epilogue
+static bool getenv_flag(const char *name) {
+    const char *v = getenv(name);
+    return v && v[0] == '1';
+}
+
 extern "C" int32_t cgs_peer_blocks(int64_t per) {
     if (per <= 0) return 0;
     int dev = 0, sms = 148;
@@ -400,9 +550,14 @@ extern "C" int cgs_epilogue_adam(const float *acc, int32_t G, int64_t n, double 
                                  double beta2, double eps, double bc1, double bc2,
                                  const int32_t *skip_if_status, void *stream) {
     if (G <= 0 || n <= 0 || !acc || !params || !m || !v || (reinterpret_cast<uintptr_t>(acc) & 7)) return CGS_ERR_ARG;
-    epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+    if (getenv_flag("CGS_EPI_NARROW")) {
+        epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            acc, G, n, params, m, v, mode, scale, lr, beta1, beta2, eps, bc1, bc2, skip_if_status, nullptr);
+        return check_launch("epilogue_adam_kernel");
+    }
+    epilogue_adam_wide_kernel<<<(unsigned)((n + kEpiGauss - 1) / kEpiGauss), kEpiThreads, 0, (cudaStream_t)stream>>>(
         acc, G, n, params, m, v, mode, scale, lr, beta1, beta2, eps, bc1, bc2, skip_if_status, nullptr);
-    return check_launch("epilogue_adam_kernel");
+    return check_launch("epilogue_adam_wide_kernel");
 }
 
 extern "C" int cgs_epilogue_adam_dev(const float *acc, int32_t G, int64_t n, double *params, double *m, double *v,
@@ -410,7 +565,12 @@ extern "C" int cgs_epilogue_adam_dev(const float *acc, int32_t G, int64_t n, dou
                                      const double *hyper, const int32_t *skip_if_status, void *stream) {
     if (G <= 0 || n <= 0 || !acc || !params || !m || !v || !hyper || (reinterpret_cast<uintptr_t>(acc) & 7))
         return CGS_ERR_ARG;
-    epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+    if (getenv_flag("CGS_EPI_NARROW")) {
+        epilogue_adam_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            acc, G, n, params, m, v, mode, scale, 0.0, beta1, beta2, eps, 1.0, 1.0, skip_if_status, hyper);
+        return check_launch("epilogue_adam_kernel");
+    }
+    epilogue_adam_wide_kernel<<<(unsigned)((n + kEpiGauss - 1) / kEpiGauss), kEpiThreads, 0, (cudaStream_t)stream>>>(
         acc, G, n, params, m, v, mode, scale, 0.0, beta1, beta2, eps, 1.0, 1.0, skip_if_status, hyper);
-    return check_launch("epilogue_adam_kernel");
+    return check_launch("epilogue_adam_wide_kernel");
 }

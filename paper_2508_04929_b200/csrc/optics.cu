@@ -1086,9 +1086,11 @@ __global__ void __launch_bounds__(SpecLf<D>::NT, 2) obs_spectrum_lf_kernel(const
     lfft::init_twiddles<D>(twt, threadIdx.x, G::NT);
     lf_load_pairs<D, false>(X, obs + (int64_t)b * D * D, 1.f);
     __syncthreads();
+#if !defined(CGS_SPEC_EXP) || !(CGS_SPEC_EXP & 1)
     lf_rows_forward<D>(X, twt);
     __syncthreads();
     lf_cols<D, -1>(X, twt);
+#endif
     __syncthreads();
     // record: F(obs) [D][P] natural (the packed column in kx = 0, kx = D/2 zero), then H_sym / D^2 [D][P]
     float2 *dst = spec + (int64_t)b * (3 * D * P / 2);
@@ -1096,7 +1098,9 @@ __global__ void __launch_bounds__(SpecLf<D>::NT, 2) obs_spectrum_lf_kernel(const
     for (int i = threadIdx.x; i < D * P; i += G::NT) {
         const int ky = i / P, kx = i - ky * P;
         dst[i] = kx == D / 2 ? make_float2(0.f, 0.f) : X[ky * S + kx];
+#if !defined(CGS_SPEC_EXP) || !(CGS_SPEC_EXP & 4)  // 4: no H table (timing experiment)
         hd[i] = ctf_sym(cc, D, ky, kx) * (1.f / ((float)D * (float)D));
+#endif
     }
 }
 
@@ -1120,9 +1124,11 @@ __global__ void __launch_bounds__(SpecLf<D>::NT, 2) ctf_mse_spec_lf_kernel(
     lfft::init_twiddles<D>(twt, threadIdx.x, G::NT);
     lf_load_pairs<D, kFixed>(X, render + (int64_t)b * D * D, kFixed ? 1.f / __ldg(render_scale) : 1.f);
     __syncthreads();
+#if !defined(CGS_SPEC_EXP) || !(CGS_SPEC_EXP & 1)  // timing experiments only: 1 skips the forward, 2 the inverse
     lf_rows_forward<D>(X, twt);
     __syncthreads();
     lf_cols<D, -1>(X, twt);
+#endif
     __syncthreads();
     // F(r) = H F(render) - O (H = Hh D^2, exact: D^2 is a power of two); loss by
     // Parseval (weight 2 on kx = 1..D/2-1, 1 on the packed column); then CTF^T
@@ -1169,9 +1175,15 @@ __global__ void __launch_bounds__(SpecLf<D>::NT, 2) ctf_mse_spec_lf_kernel(
         loss[b] = l;
         if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
     }
+#if !defined(CGS_SPEC_EXP) || !(CGS_SPEC_EXP & 2)
     lf_cols<D, 1>(X, twt);
     __syncthreads();
     lf_rows_inverse<D, kRowPair>(X, twt, upstream + (int64_t)b * D * D);
+#else
+    __syncthreads();
+    for (int i = threadIdx.x; i < D * D / 2; i += G::NT)
+        reinterpret_cast<float2 *>(upstream + (int64_t)b * D * D)[i] = X[(i / D) * 2 * S + (i % D)];
+#endif
 }
 
 template <int R>
