@@ -508,7 +508,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "units_per_launch": bwd_pairs_per_launch,
                      "units": (f"(image, Gaussian, pixel) pairs K5 evaluates: q < {bwd_cut:.3f} (e >= 1e-7 of the "
                                f"peak; the reference's q < 42.25 pairs are {pairs_per_launch:.4g} per launch)"),
-                     "launch_ms": stage_ms["bwd"]},
+                     "launch_ms": stage_ms["bwd"],
+                     # the same launch counted in the reference's q < 6.5^2 pairs (round 1's unit)
+                     "frac_reference_pairs": pairs_per_launch / (stage_ms["bwd"] / 1e3) / 1e9 / bwd_peak},
         "roofline_step": {"achieved": step_achieved, "peak": step_peak, "unit": "Gpair/s",
                           "frac": step_achieved / step_peak,
                           "peak_basis": "0.164 SM-clk per in-ellipse pair (fwd+bwd issue), SURVEY.md 8(d)"},
