@@ -246,7 +246,14 @@ __global__ void epilogue_adam_kernel(const float *__restrict__ part, int G, int6
 //  (3) the chain's algebra, one thread per Gaussian;
 //  (4) Adam, one thread per element of the block's 64 x 11 contiguous
 //      parameters (coalesced p, m, v).
-constexpr int kEpiThreads = 256, kEpiGauss = 64;
+#ifndef CGS_EPI_GAUSS
+#define CGS_EPI_GAUSS 64
+#endif
+#ifndef CGS_EPI_UNROLL
+#define CGS_EPI_UNROLL 4
+#endif
+constexpr int kEpiThreads = 256, kEpiGauss = CGS_EPI_GAUSS, kEpiUnroll = CGS_EPI_UNROLL;
+static_assert(4 * kEpiGauss <= kEpiThreads, "phase (1): four threads per Gaussian");
 #ifndef CGS_EPI_MINB
 #define CGS_EPI_MINB 4
 #endif
@@ -268,8 +275,8 @@ __global__ void __launch_bounds__(kEpiThreads, CGS_EPI_MINB) epilogue_adam_wide_
     const int64_t g0 = (int64_t)blockIdx.x * kEpiGauss;
     const int ng = (int)min((int64_t)kEpiGauss, n - g0);
     {  // (1)
-        const int j = tid >> 6, i = tid & (kEpiGauss - 1);
-        if (i < ng) {
+        const int j = tid / kEpiGauss, i = tid - j * kEpiGauss;
+        if (j < 4 && i < ng) {
             const double *raw = params + (g0 + i) * 11;
             if (j < 3) {
                 chain_pre_scale(raw, j, ss[j][i], ssig[j][i]);
@@ -285,39 +292,38 @@ __global__ void __launch_bounds__(kEpiThreads, CGS_EPI_MINB) epilogue_adam_wide_
             }
         }
     }
-    {  // (2): up to three floats per thread, three independent chains
+    {  // (2): kFpt accumulator floats per thread, independent chains, kEpiUnroll groups of loads in flight
+        constexpr int kFpt = (kEpiGauss * 10 + kEpiThreads - 1) / kEpiThreads;
         const int nf = ng * 10;
         const float *base = part + g0 * 10;
         const int64_t gs = n * 10;
-        const int f0 = tid, f1 = tid + kEpiThreads, f2 = tid + 2 * kEpiThreads;
-        const bool u0 = f0 < nf, u1 = f1 < nf, u2 = f2 < nf;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        double a[kFpt];
+        bool u[kFpt];
+#pragma unroll
+        for (int q = 0; q < kFpt; ++q) {
+            a[q] = 0.0;
+            u[q] = tid + q * kEpiThreads < nf;
+        }
         int k = 0;
-        for (; k + 4 <= G; k += 4) {
-            float x0[4], x1[4], x2[4];
+        for (; k + kEpiUnroll <= G; k += kEpiUnroll) {
+            float x[kEpiUnroll][kFpt];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float *p = base + (k + q) * gs;
-                x0[q] = u0 ? __ldg(p + f0) : 0.f;
-                x1[q] = u1 ? __ldg(p + f1) : 0.f;
-                x2[q] = u2 ? __ldg(p + f2) : 0.f;
-            }
+            for (int r = 0; r < kEpiUnroll; ++r)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                a0 += (double)x0[q];
-                a1 += (double)x1[q];
-                a2 += (double)x2[q];
-            }
+                for (int q = 0; q < kFpt; ++q)
+                    x[r][q] = u[q] ? __ldg(base + (k + r) * gs + tid + q * kEpiThreads) : 0.f;
+#pragma unroll
+            for (int r = 0; r < kEpiUnroll; ++r)
+#pragma unroll
+                for (int q = 0; q < kFpt; ++q) a[q] += (double)x[r][q];
         }
-        for (; k < G; ++k) {
-            const float *p = base + k * gs;
-            a0 += (double)(u0 ? __ldg(p + f0) : 0.f);
-            a1 += (double)(u1 ? __ldg(p + f1) : 0.f);
-            a2 += (double)(u2 ? __ldg(p + f2) : 0.f);
-        }
-        if (u0) sacc[f0] = a0;
-        if (u1) sacc[f1] = a1;
-        if (u2) sacc[f2] = a2;
+        for (; k < G; ++k)
+#pragma unroll
+            for (int q = 0; q < kFpt; ++q)
+                a[q] += (double)(u[q] ? __ldg(base + k * gs + tid + q * kEpiThreads) : 0.f);
+#pragma unroll
+        for (int q = 0; q < kFpt; ++q)
+            if (u[q]) sacc[tid + q * kEpiThreads] = a[q];
     }
     __syncthreads();
     if (tid < ng) {  // (3)
