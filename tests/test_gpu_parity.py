@@ -409,6 +409,35 @@ def test_adam_matches_reference_bitwise():
     assert np.array_equal(prm, k["adam_params"])
 
 
+def test_wide_epilogue_bitwise_equals_narrow(monkeypatch):
+    """K6 over 256 threads per 64 Gaussians (epilogue_adam_wide_kernel) runs the same arithmetic
+    in the same order as the one-thread-per-Gaussian kernel (CGS_EPI_NARROW=1): parameters and
+    both Adam moments bitwise equal, anisotropic and isotropic, with a ragged last block
+    (N = 1000 = 15 x 64 + 40), 3 partial groups and three steps (bias corrections change)."""
+    rng = np.random.default_rng(7)
+    n, G = 1000, 3
+    ctx = engine.DeviceContext.get(0)
+    part = torch.as_tensor(rng.standard_normal((G, n, 10)).astype(np.float32) * 1e-3).cuda()
+    p0 = rng.standard_normal((n, 11))
+    p0[:, 3:6] = rng.uniform(-6.0, -3.0, (n, 3))
+    p0[5] = 0.0  # a zero quaternion row: the chain's degenerate branch
+    for mode in ("anisotropic", "isotropic"):
+        out = {}
+        for narrow in ("1", "0"):
+            monkeypatch.setenv("CGS_EPI_NARROW", narrow)
+            prm = torch.as_tensor(p0).cuda()
+            m = torch.zeros_like(prm)
+            v = torch.zeros_like(prm)
+            for t in (1, 2, 3):
+                _lib.call("cgs_epilogue_adam", part.data_ptr(), G, n, prm.data_ptr(), m.data_ptr(), v.data_ptr(),
+                          _lib.CGS_MODE[mode], 1.0 / 256, 1e-3, 0.9, 0.999, 1e-8, 1.0 - 0.9 ** t,
+                          1.0 - 0.999 ** t, None, ctx.stream)
+            torch.cuda.synchronize()
+            out[narrow] = (prm.cpu().numpy(), m.cpu().numpy(), v.cpu().numpy())
+        for a, b in zip(out["1"], out["0"]):
+            assert np.array_equal(a, b, equal_nan=True)
+
+
 def test_train_small_matches_reference():
     t = load_golden("train_small")
     grid = cs.GridSpec(32, 0.5, 3.0)
