@@ -39,7 +39,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "particle images/sec (fwd+bwd step, 128² px, 50k Gaussians)"
-N_GAUSS, D, BATCH_PER_GPU, DATASET = 50000, 128, 256, 2048
+N_GAUSS, D, BATCH_PER_GPU = 50000, 128, 256
+DATASET = int(os.environ.get("CGS_BENCH_DATASET", "2048"))  # particles per rank (A/B experiments only)
 GLOBAL_BATCH_STRONG = 256  # --scaling strong: C3's fixed global batch
 PIXEL_A = 1.5
 WORKLOAD = "C2: 50k init_random Gaussians, 128x128 particles, batch 256/GPU, known poses + CTF, fwd+bwd+Adam"
