@@ -226,6 +226,12 @@ int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, int32_t B, 
 int cgs_ctf_mse_spectral_fixed(const int32_t *render_fixed, const float *render_scale, const float *obs_spec,
                                int32_t B, cgs_grid grid, float *upstream, double *loss, int32_t *status,
                                int32_t upstream_layout, void *stream);
+/* The same with image b's observation record at row rows[b] (int64 [B], device)
+ * of a dataset's resident records obs_spec [R][cgs_obs_spectrum_elems(D, 1)]:
+ * a batch of a resident dataset needs no gathered copy of its records. */
+int cgs_ctf_mse_spectral_fixed_rows(const int32_t *render_fixed, const float *render_scale, const float *obs_spec,
+                                    const int64_t *rows, int32_t B, cgs_grid grid, float *upstream, double *loss,
+                                    int32_t *status, int32_t upstream_layout, void *stream);
 
 /* Batched Fourier filter out = Re ifft2(F fft2(in)), per image F = H_sym (CTF,
  * ctf f64 [B][8], may be NULL) x the sub-pixel shift ramp

@@ -1107,14 +1107,15 @@ __global__ void __launch_bounds__(SpecLf<D>::NT, 2) obs_spectrum_lf_kernel(const
 template <int D, bool kFixed, bool kRowPair>
 __global__ void __launch_bounds__(SpecLf<D>::NT, 2) ctf_mse_spec_lf_kernel(
     const float *__restrict__ render, const float *__restrict__ render_scale, const float2 *__restrict__ obs_spec,
-    float *__restrict__ upstream, double *__restrict__ loss, int32_t *status) {
+    const int64_t *__restrict__ rows, float *__restrict__ upstream, double *__restrict__ loss, int32_t *status) {
     using G = SpecLf<D>;
     constexpr int S = G::S, P = G::P;
     extern __shared__ float2 X[];
     float2 *twt = X + D * S;
     __shared__ double scratch[G::NT / 32];
     const int b = blockIdx.x;
-    const float2 *O = obs_spec + (int64_t)b * (3 * D * P / 2);
+    // image b's record: row b of obs_spec, or row rows[b] of a dataset's resident records
+    const float2 *O = obs_spec + (rows ? __ldg(rows + b) : (int64_t)b) * (3 * D * P / 2);
     const float *Hh = reinterpret_cast<const float *>(O + D * P);  // H_sym / D^2, natural [ky][kx]
     {  // warm L2 with the observation record, read after the forward transform
         const char *ob = reinterpret_cast<const char *>(O);
@@ -1207,13 +1208,15 @@ static int launch_obs_spectrum(const float *obs, const double *ctf, double pix, 
 }
 
 template <int R, bool kFixed, bool kRowPair>
-static int launch_ctf_mse_spec_t(const float *render, const float *render_scale, const float *spec, int B,
-                                 float *upstream, double *loss, int32_t *status, cudaStream_t st) {
+static int launch_ctf_mse_spec_t(const float *render, const float *render_scale, const float *spec,
+                                 const int64_t *rows, int B, float *upstream, double *loss, int32_t *status,
+                                 cudaStream_t st) {
     constexpr int D = 32 * R, P = D / 2 + 1;
     const size_t smem = (size_t)D * P * sizeof(float2);
     const int rc = ensure_smem_limit((const void *)ctf_mse_spec_kernel<R, kFixed, kRowPair>, smem, "ctf_mse_spec_kernel");
     if (rc) return rc;
 #ifdef CGS_SPEC_V1
+    if (rows) return CGS_ERR_UNSUPPORTED;
     ctf_mse_spec_kernel<R, kFixed, kRowPair><<<B, kR2cThreads, smem, st>>>(
         render, render_scale, reinterpret_cast<const float2 *>(spec), upstream, loss, status);
     return check_launch("ctf_mse_spec_kernel");
@@ -1224,18 +1227,20 @@ static int launch_ctf_mse_spec_t(const float *render, const float *render_scale,
                                       "ctf_mse_spec_lf_kernel");
     if (rc2) return rc2;
     ctf_mse_spec_lf_kernel<D, kFixed, kRowPair><<<B, G::NT, G::smem, st>>>(
-        render, render_scale, reinterpret_cast<const float2 *>(spec), upstream, loss, status);
+        render, render_scale, reinterpret_cast<const float2 *>(spec), rows, upstream, loss, status);
     return check_launch("ctf_mse_spec_lf_kernel");
 #endif
 }
 
 template <int R, bool kFixed>
-static int launch_ctf_mse_spec(const float *render, const float *render_scale, const float *spec, int B,
-                               float *upstream, double *loss, int32_t *status, int layout, cudaStream_t st) {
+static int launch_ctf_mse_spec(const float *render, const float *render_scale, const float *spec,
+                               const int64_t *rows, int B, float *upstream, double *loss, int32_t *status,
+                               int layout, cudaStream_t st) {
     if (layout == CGS_LAYOUT_ROWPAIR)
-        return launch_ctf_mse_spec_t<R, kFixed, true>(render, render_scale, spec, B, upstream, loss, status, st);
+        return launch_ctf_mse_spec_t<R, kFixed, true>(render, render_scale, spec, rows, B, upstream, loss, status, st);
     if (layout == CGS_LAYOUT_NATURAL)
-        return launch_ctf_mse_spec_t<R, kFixed, false>(render, render_scale, spec, B, upstream, loss, status, st);
+        return launch_ctf_mse_spec_t<R, kFixed, false>(render, render_scale, spec, rows, B, upstream, loss, status,
+                                                       st);
     return CGS_ERR_ARG;
 }
 
@@ -1408,9 +1413,9 @@ extern "C" int cgs_ctf_mse_spectral(const float *render, const float *obs_spec, 
     if (!render || !obs_spec || !upstream || !loss || B <= 0 || render == upstream) return CGS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     if (grid.size == 128)
-        return launch_ctf_mse_spec<4, false>(render, nullptr, obs_spec, B, upstream, loss, status, upstream_layout, st);
+        return launch_ctf_mse_spec<4, false>(render, nullptr, obs_spec, nullptr, B, upstream, loss, status, upstream_layout, st);
     if (grid.size == 64)
-        return launch_ctf_mse_spec<2, false>(render, nullptr, obs_spec, B, upstream, loss, status, upstream_layout, st);
+        return launch_ctf_mse_spec<2, false>(render, nullptr, obs_spec, nullptr, B, upstream, loss, status, upstream_layout, st);
     set_error_detail("cgs_ctf_mse_spectral", "image size must be 64 or 128");
     return CGS_ERR_UNSUPPORTED;
 }
@@ -1422,10 +1427,28 @@ extern "C" int cgs_ctf_mse_spectral_fixed(const int32_t *render_fixed, const flo
     if (!r || !render_scale || !obs_spec || !upstream || !loss || B <= 0 || r == upstream) return CGS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     if (grid.size == 128)
-        return launch_ctf_mse_spec<4, true>(r, render_scale, obs_spec, B, upstream, loss, status, upstream_layout, st);
+        return launch_ctf_mse_spec<4, true>(r, render_scale, obs_spec, nullptr, B, upstream, loss, status, upstream_layout, st);
     if (grid.size == 64)
-        return launch_ctf_mse_spec<2, true>(r, render_scale, obs_spec, B, upstream, loss, status, upstream_layout, st);
+        return launch_ctf_mse_spec<2, true>(r, render_scale, obs_spec, nullptr, B, upstream, loss, status, upstream_layout, st);
     set_error_detail("cgs_ctf_mse_spectral_fixed", "image size must be 64 or 128");
+    return CGS_ERR_UNSUPPORTED;
+}
+
+extern "C" int cgs_ctf_mse_spectral_fixed_rows(const int32_t *render_fixed, const float *render_scale,
+                                               const float *obs_spec, const int64_t *rows, int32_t B, cgs_grid grid,
+                                               float *upstream, double *loss, int32_t *status,
+                                               int32_t upstream_layout, void *stream) {
+    const float *r = reinterpret_cast<const float *>(render_fixed);
+    if (!r || !render_scale || !obs_spec || !rows || !upstream || !loss || B <= 0 || r == upstream)
+        return CGS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (grid.size == 128)
+        return launch_ctf_mse_spec<4, true>(r, render_scale, obs_spec, rows, B, upstream, loss, status, upstream_layout,
+                                            st);
+    if (grid.size == 64)
+        return launch_ctf_mse_spec<2, true>(r, render_scale, obs_spec, rows, B, upstream, loss, status, upstream_layout,
+                                            st);
+    set_error_detail("cgs_ctf_mse_spectral_fixed_rows", "image size must be 64 or 128");
     return CGS_ERR_UNSUPPORTED;
 }
 

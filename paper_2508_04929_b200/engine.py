@@ -405,8 +405,11 @@ class StepPipeline:
             return self.render
         return self.render.view(torch.int32).to(torch.float32) / self._render_scale()
 
-    def forward_backward(self, params, poses, obs, ctf, events=None, obs_spec=None):
+    def forward_backward(self, params, poses, obs, ctf, events=None, obs_spec=None, obs_rows=None):
         """K0..K5 for a batch; leaves partial accumulators in self.partial.
+
+        ``obs_spec`` (spectral K4): this batch's observation records, or with ``obs_rows``
+        (int64 [B] device) a dataset's resident records and the batch's rows in them.
 
         ``events`` (optional dict of name -> (start, end) torch.cuda.Event
         lists) records CUDA events around the fwd / ctf / bwd stages on the
@@ -441,12 +444,18 @@ class StepPipeline:
         mark("fwd", 1)
         mark("ctf", 0)
         if ctf is not None and self.spectral:
+            if obs_rows is not None and not fixed:  # only the fixed-point K4 reads records by row
+                obs_spec, obs_rows = obs_spec.index_select(0, obs_rows), None
             if obs_spec is None:  # this batch's records (a dataset passes its precomputed ones)
                 _lib.call("cgs_obs_spectrum", _ptr(obs), _ptr(ctf), self.B, self.grid, _ptr(self.obs_spec), s)
                 obs_spec = self.obs_spec
             # the upstream goes out with row pairs interleaved: the backward's region staging is a copy
             up_layout = _lib.CGS_LAYOUT_ROWPAIR
-            if fixed:
+            if fixed and obs_rows is not None:
+                _lib.call("cgs_ctf_mse_spectral_fixed_rows", _ptr(self.render), _ptr(self._render_scale()),
+                          _ptr(obs_spec), _ptr(obs_rows), self.B, self.grid, _ptr(self.upstream), _ptr(self.loss),
+                          _ptr(self.status), up_layout, s)
+            elif fixed:
                 _lib.call("cgs_ctf_mse_spectral_fixed", _ptr(self.render), _ptr(self._render_scale()), _ptr(obs_spec),
                           self.B, self.grid, _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), up_layout, s)
             else:

@@ -469,9 +469,10 @@ class Reconstructor:
 
         def local():
             if pipe is not None:
-                o, p, c, s = inputs()
+                o, p, c, s, *rows = inputs()
                 pipe.clear_status()
-                pipe.forward_backward(self.params, p, o, c, events=events, obs_spec=s)
+                pipe.forward_backward(self.params, p, o, c, events=events, obs_spec=s,
+                                      obs_rows=rows[0] if rows else None)
             if xch is not None:
                 _lib.call("cgs_reduce_partials_sliced", ptr(pipe.partial) if pipe else 0, pipe.G if pipe else 0,
                           self.n, xch.per, ptr(pipe.status) if pipe else 0, ptr(xch.acc), self.ctx.stream)
@@ -554,21 +555,21 @@ class Reconstructor:
             sl = self._idx_slots[key] = {
                 "idx": torch.zeros(max(b, 1), dtype=torch.int64, device=dev),
                 "o": None if spec or b == 0 else torch.empty((b, D, D), dtype=torch.float32, device=dev),
-                "s": torch.empty((b, self.obs_spec.shape[1]), dtype=torch.float32, device=dev) if spec and b else None,
                 "p": torch.empty((max(b, 1), 12), dtype=torch.float64, device=dev),
-                "c": None if self.ctfs is None else torch.empty((max(b, 1), 8), dtype=torch.float64, device=dev),
+                # the spectral K4 takes H from the records: the CTF rows are not gathered then
+                "c": None if self.ctfs is None or spec else torch.empty((max(b, 1), 8), dtype=torch.float64,
+                                                                         device=dev),
                 "hyper": torch.empty(4, dtype=torch.float64, device=dev)}
 
-            def inputs(sl=sl):
+            def inputs(sl=sl, spec=spec):
                 i = sl["idx"]
-                if sl["s"] is not None:
-                    torch.index_select(self.obs_spec, 0, i, out=sl["s"])
-                else:
-                    torch.index_select(self.obs, 0, i, out=sl["o"])
                 torch.index_select(self.poses, 0, i, out=sl["p"])
+                if spec:  # K4 reads the batch's records in place, by row (no gathered copy)
+                    return None, sl["p"], self.ctfs, self.obs_spec, i[:b]
+                torch.index_select(self.obs, 0, i, out=sl["o"])
                 if sl["c"] is not None:
                     torch.index_select(self.ctfs, 0, i, out=sl["c"])
-                return sl["o"], sl["p"], sl["c"], sl["s"]
+                return sl["o"], sl["p"], sl["c"], None
 
             segs, pipe = self._segments(b, len(indices), inputs, sl["hyper"])
             sl["runner"] = _StepRunner(segs, self.use_graphs, self._whole_graph)

@@ -367,6 +367,50 @@ def test_spectral_ctf_mse_matches_oracle(oracle, D):
     assert ctx.lib.cgs_obs_spectrum(o.data_ptr(), None, B, gs, spec.data_ptr(), None) == 1
 
 
+@pytest.mark.parametrize("D", [64, 128])
+def test_spectral_rows_equal_gathered_records(D):
+    """cgs_ctf_mse_spectral_fixed_rows (K4 reading image b's record at row rows[b] of a resident
+    set, Reconstructor.step's path) is bitwise cgs_ctf_mse_spectral_fixed on the gathered records:
+    5 records, a batch of 4 rows with a repeat, out of order."""
+    R, B = 5, 4
+    rng = np.random.default_rng(90 + D)
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(D, 0.5, 1.5)
+    obs = torch.as_tensor(rng.standard_normal((R, D, D)).astype(np.float32)).cuda()
+    ctf = np.zeros((R, 8))
+    ctf[:, 0] = rng.uniform(1e4, 2.5e4, R)
+    ctf[:, 1] = ctf[:, 0] - 500.0
+    ctf[:, 2] = rng.uniform(0.0, np.pi, R)
+    ctf[:, 3:6] = [300.0, 2.7, 0.1]
+    c = torch.as_tensor(ctf).cuda()
+    per = int(ctx.lib.cgs_obs_spectrum_elems(D, 1))
+    spec = torch.empty((R, per), dtype=torch.float32, device="cuda")
+    _lib.call("cgs_obs_spectrum", obs.data_ptr(), c.data_ptr(), R, gs, spec.data_ptr(), ctx.stream)
+    rows = torch.tensor([3, 0, 3, 1], dtype=torch.int64, device="cuda")
+    gathered = spec.index_select(0, rows).contiguous()
+    render = torch.randint(0, 1 << 20, (B, D, D), dtype=torch.int32, device="cuda")
+    scale = torch.tensor([2.0 ** 20], dtype=torch.float32, device="cuda")
+    out = {}
+    for name in ("gathered", "rows"):
+        up = torch.empty((B, D, D), dtype=torch.float32, device="cuda")
+        loss = torch.empty(B, dtype=torch.float64, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        if name == "rows":
+            _lib.call("cgs_ctf_mse_spectral_fixed_rows", render.data_ptr(), scale.data_ptr(), spec.data_ptr(),
+                      rows.data_ptr(), B, gs, up.data_ptr(), loss.data_ptr(), status.data_ptr(),
+                      _lib.CGS_LAYOUT_ROWPAIR, ctx.stream)
+        else:
+            _lib.call("cgs_ctf_mse_spectral_fixed", render.data_ptr(), scale.data_ptr(), gathered.data_ptr(), B, gs,
+                      up.data_ptr(), loss.data_ptr(), status.data_ptr(), _lib.CGS_LAYOUT_ROWPAIR, ctx.stream)
+        torch.cuda.synchronize()
+        out[name] = (up.cpu(), loss.cpu())
+        assert status.item() == 0
+    assert torch.equal(out["rows"][0], out["gathered"][0])
+    assert torch.equal(out["rows"][1], out["gathered"][1])
+    assert ctx.lib.cgs_ctf_mse_spectral_fixed_rows(render.data_ptr(), scale.data_ptr(), spec.data_ptr(), None, B,
+                                                   gs, render.data_ptr() + 4, None, None, 0, None) == 1
+
+
 def _full_step_device(params, poses, grid, obs, ctfs, render="direct"):
     """Run the engine's fused K0..K5 + epilogue grads for a batch; return (losses, grads)."""
     ctx = engine.DeviceContext.get()
