@@ -340,7 +340,25 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     const float scale = cscale[blockIdx.x];
     int nclamp = 0;
     __syncthreads();
+    // Row bands (D beyond one 64 KB band, e.g. 256^2 in 4 bands): bands past the first skip a
+    // Gaussian whose footprint cannot reach their rows before projecting it, from its projected
+    // centre row and a bound on its y extent (the projected y variance is at most
+    // max(s_max / h, 0.1 px)^2, eigenvalue floor included).  Band 0 projects every Gaussian, so
+    // each (image, Gaussian) clamp is still counted once.
+    const bool cull = blockIdx.z > 0;
+    const float ylo_band = (float)r0, yhi_band = (float)(r1 - 1);
     for (int64_t i = i_begin + threadIdx.x; i < i_end; i += kRThreads) {
+        if (cull) {
+            const float *rec = splat + g * CGS_SPLAT_STRIDE;
+            const float4 m = __ldg(reinterpret_cast<const float4 *>(rec));
+            const float yc = (P.w1[0] * m.x + P.w1[1] * m.y + P.w1[2] * m.z + P.ty) * G.inv_h + G.c0;
+            const float ry = 6.5f * 1.001f * fmaxf(__ldg(rec + 13) * G.inv_h, 0.1f) + 1.f;
+            if (yc + ry < ylo_band || yc - ry > yhi_band) {
+                g += stepA;
+                if (g >= n) g -= n;
+                continue;
+            }
+        }
         const Splat2 s = project2(load_splat(splat, g), P, G);
         g += stepA;
         if (g >= n) g -= n;

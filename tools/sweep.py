@@ -65,8 +65,16 @@ def point(name, n, D, B, ctf, steps):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
     p = sum(pairs[k % nbatch] for k in range(steps)) / steps
+    # one more step with per-stage CUDA events (fwd = weight bound + render; ctf = K4, with the
+    # per-step observation records; bwd = K5; epi = epilogue + Adam)
+    ev = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for s in ("fwd", "ctf", "bwd", "epi")}
+    rec.step_batch(*batches[steps % nbatch], 1e-3, global_batch=B, events=ev)
+    torch.cuda.synchronize()
+    stage = {s: round(e[0].elapsed_time(e[1]), 4) for s, e in ev.items()}
     return {"config": name, "n_gaussians": n, "image_px": D, "batch": B, "ctf": ctf, "ms_per_step": ms,
-            "images_per_s": B / (ms / 1e3), "pairs_per_image": p / B, "gpairs_per_s": p / (ms / 1e3) / 1e9}
+            "images_per_s": B / (ms / 1e3), "pairs_per_image": p / B, "gpairs_per_s": p / (ms / 1e3) / 1e9,
+            "stage_ms": stage}
 
 
 def main():
