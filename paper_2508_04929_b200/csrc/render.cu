@@ -64,6 +64,10 @@ constexpr int kRChunkMin = 512;
 #define CGS_FWD_BAND_KB 64
 #endif
 constexpr int kRBandBytes = CGS_FWD_BAND_KB * 1024;  // int32 accumulator rows per CTA
+#ifndef CGS_FWD_BAND_MULTI_KB
+#define CGS_FWD_BAND_MULTI_KB 100
+#endif
+constexpr int kRBandMultiBytes = CGS_FWD_BAND_MULTI_KB * 1024;  // band budget when an image needs several
 constexpr int kWbThreads = 256;  // weight-bound pass: CTA = 256 logical indices (one wave over the SMs at C2)
 constexpr double kFixedRange = 1073741824.0;  // 2^30
 constexpr double kContribRange = 4194304.0;   // 2^22
@@ -340,50 +344,86 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     const float scale = cscale[blockIdx.x];
     int nclamp = 0;
     __syncthreads();
-    // Row bands (D beyond one 64 KB band, e.g. 256^2 in 4 bands): bands past the first skip a
-    // Gaussian whose footprint cannot reach their rows before projecting it, from its projected
-    // centre row and a bound on its y extent (the projected y variance is at most
-    // max(s_max / h, 0.1 px)^2, eigenvalue floor included).  Band 0 projects every Gaussian, so
-    // each (image, Gaussian) clamp is still counted once.
-    const bool cull = blockIdx.z > 0;
-    const float ylo_band = (float)r0, yhi_band = (float)(r1 - 1);
-    for (int64_t i = i_begin + threadIdx.x; i < i_end; i += kRThreads) {
-        if (cull) {
-            const float *rec = splat + g * CGS_SPLAT_STRIDE;
-            const float4 m = __ldg(reinterpret_cast<const float4 *>(rec));
-            const float yc = (P.w1[0] * m.x + P.w1[1] * m.y + P.w1[2] * m.z + P.ty) * G.inv_h + G.c0;
-            const float ry = 6.5f * 1.001f * fmaxf(__ldg(rec + 13) * G.inv_h, 0.1f) + 1.f;
-            if (yc + ry < ylo_band || yc - ry > yhi_band) {
-                g += stepA;
-                if (g >= n) g -= n;
-                continue;
-            }
-        }
-        const Splat2 s = project2(load_splat(splat, g), P, G);
-        g += stepA;
-        if (g >= n) g -= n;
-        nclamp += s.clamped;
-        if (!(s.w > 0.f)) continue;
-        // Walk q < cut: e(cut) is the larger of kTailFrac (the precision cut,
-        // see the header) and 0.4995 / (w scale), below which a pixel rounds
-        // to 0 units anyway (the 1e-3 margin keeps every pixel that can round
-        // to >= 1 unit), and q < 6.5^2 (splat.py:49).
+    // One projected Gaussian into the band: walk q < cut, where e(cut) is the larger of kTailFrac
+    // (the precision cut, see the header) and 0.4995 / (w scale), below which a pixel rounds to 0
+    // units anyway (the 1e-3 margin keeps every pixel that can round to >= 1 unit), and
+    // q < 6.5^2 (splat.py:49).
+    auto walk = [&](const Splat2 &s) {
+        if (!(s.w > 0.f)) return;
         const float thr = fmaxf(0.4995f * rcp_approx(s.w * scale), kTailFrac);
-        if (!(thr < 1.f)) continue;
+        if (!(thr < 1.f)) return;
         const float cut = fminf(kCutoffSq, -2.f * kLn2 * lg2_approx(thr));
         const float hy = s.hy * sqrt_approx(cut * (1.f / kCutoffSq));
         const int ylo = max(max((int)ceilf(s.mpy - hy), 0), r0);
         const int yhi = min(min((int)floorf(s.mpy + hy), D - 1), r1 - 1);
-        if (ylo > yhi) continue;
+        if (ylo > yhi) return;
 #if defined(CGS_FWD_EXP) && CGS_FWD_EXP == 5
         if (ylo + yhi == -12345 || cut == 1.2345f) band[0] += 1;  // projection only (timing experiment)
-        continue;
+        return;
 #endif
         // widest row = 2 sqrt(cut / p00) = 2 * 6.5 sqrt(cut / 6.5^2) / sqrt(p00)
         if (13.f * sqrt_approx(cut * (1.f / kCutoffSq)) * s.inv_sqrt_p00 < 31.f)
             fwd_rows_band<true>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
         else
             fwd_rows_band<false>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
+    };
+    if (gridDim.z == 1) {  // the whole image in one band: every lane walks its own Gaussians
+        for (int64_t i = i_begin + threadIdx.x; i < i_end; i += kRThreads) {
+            const Splat2 s = project2(load_splat(splat, g), P, G);
+            g += stepA;
+            if (g >= n) g -= n;
+            nclamp += s.clamped;
+            walk(s);
+        }
+    } else {
+        // Row bands (D beyond one 64 KB band, e.g. 256^2 in 4 bands): most of a chunk's Gaussians
+        // miss a band's rows, and lanes skipping them idled while the others walked (half the
+        // lanes of a warp active at C4).  So a warp first sifts candidates, one per lane, and
+        // stacks the survivors in shared memory; then every lane walks one stacked Gaussian.
+        // Band 0 projects every candidate (each (image, Gaussian) clamp counted once) and keeps
+        // those whose footprint box reaches its rows; later bands test the projected centre row
+        // against a bound on the y extent (projected y variance <= max(s_max / h, 0.1 px)^2,
+        // eigenvalue floor included) before any projection.  The render is bitwise the same:
+        // which lane walks a Gaussian does not change the integer sums.
+        int(*stk)[64] = reinterpret_cast<int(*)[64]>(band + HB * D);  // after the band (dynamic smem)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const unsigned below = (1u << lane) - 1u;
+        const float ylo_band = (float)r0, yhi_band = (float)(r1 - 1);
+        int64_t i = i_begin + threadIdx.x;
+        bool more = __any_sync(0xffffffffu, i < i_end);
+        int depth = 0;  // warp-uniform
+        while (more || depth > 0) {
+            while (more && depth < 32) {
+                bool keep = false;
+                const int gi = (int)g;
+                if (i < i_end) {
+                    if (blockIdx.z == 0) {
+                        const Splat2 s0 = project2(load_splat(splat, g), P, G);
+                        nclamp += s0.clamped;
+                        keep = s0.w > 0.f && s0.mpy - s0.hy <= yhi_band && s0.mpy + s0.hy >= ylo_band;
+                    } else {
+                        const float *rec = splat + g * CGS_SPLAT_STRIDE;
+                        const float4 m = __ldg(reinterpret_cast<const float4 *>(rec));
+                        const float yc = (P.w1[0] * m.x + P.w1[1] * m.y + P.w1[2] * m.z + P.ty) * G.inv_h + G.c0;
+                        const float ry = 6.5f * 1.001f * fmaxf(__ldg(rec + 13) * G.inv_h, 0.1f) + 1.f;
+                        keep = yc + ry >= ylo_band && yc - ry <= yhi_band;
+                    }
+                    i += kRThreads;
+                    g += stepA;
+                    if (g >= n) g -= n;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) stk[warp][depth + __popc(bal & below)] = gi;
+                depth += __popc(bal);
+                more = __any_sync(0xffffffffu, i < i_end);
+            }
+            __syncwarp();
+            const int take = min(depth, 32);
+            const int gq = lane < take ? stk[warp][depth - take + lane] : -1;
+            depth -= take;
+            __syncwarp();
+            if (gq >= 0) walk(project2(load_splat(splat, gq), P, G));
+        }
     }
     if (clamp_count && blockIdx.z == 0) {  // every (image, Gaussian) projection counted once
         nclamp = __reduce_add_sync(0xffffffffu, nclamp);
@@ -470,8 +510,18 @@ static int render_impl(const double *params, int32_t *status, float *splat, int6
     int HB = kRBandBytes / (D * (int)sizeof(int));
     if (HB < 1) return CGS_ERR_UNSUPPORTED;
     HB = HB > D ? D : HB;
+    if (HB < D) {
+        // Several bands: as few as a larger band allows at two CTAs per SM (kRBandMultiBytes),
+        // rows split evenly.  A Gaussian cut by a band edge walks only its rows inside the band, so
+        // fewer edges leave fewer lanes of a warp with short walks (C4, 256^2: 3 bands of 86 rows).
+        const int hb_max = max(HB, kRBandMultiBytes / (D * (int)sizeof(int)));
+        const int nb = (D + hb_max - 1) / hb_max;
+        HB = (D + nb - 1) / nb;
+    }
     const int bands = (D + HB - 1) / HB;
-    const size_t smem = (size_t)HB * D * sizeof(int);
+    if (bands > 1 && n > 0x7fffffff) return CGS_ERR_UNSUPPORTED;  // the banded render stacks int indices
+    // banded launches also stack candidate indices per warp (64 ints per warp) after the band
+    const size_t smem = (size_t)HB * D * sizeof(int) + (bands > 1 ? (size_t)kRThreads / 32 * 64 * sizeof(int) : 0);
     int rc = ensure_smem_limit((const void *)raster_fwd_atomic_kernel, smem, "raster_fwd_atomic_kernel");
     if (rc) return rc;
     int slots = 0;
