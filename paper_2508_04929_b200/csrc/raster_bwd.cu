@@ -473,12 +473,26 @@ constexpr int kMaxPoseImages = 64;  // image groups up to this size keep fp32 po
 #define CGS_BWD_REG_FLOATS 6144
 #endif
 constexpr int kRegFloats = CGS_BWD_REG_FLOATS;  // 24 KB per band (measured 8..32 KB)
+#ifndef CGS_BWD_REG_FLOATS_LARGE
+#define CGS_BWD_REG_FLOATS_LARGE 10240
+#endif
+// Images beyond 128^2: a larger region band (40 KB, still 4 CTAs per SM), so a CTA's union box
+// splits into fewer bands; a lane whose footprint misses the current band idles through it
+// (C4, 256^2: K5 1.79 -> see DESIGN.md).
+constexpr int kRegFloatsLarge = CGS_BWD_REG_FLOATS_LARGE;
 
-template <bool kPoseSmem, bool kRowPair>  // kRowPair: upstream in CGS_LAYOUT_ROWPAIR (a straight float2 copy)
+// kRowPair: upstream in CGS_LAYOUT_ROWPAIR (a straight float2 copy); kRegF: the region band in
+// static shared memory of kRegF floats (128^2: the static array measured 0.2% faster), or 0 for a
+// dynamic band of regf_dyn floats (larger images)
+template <bool kPoseSmem, bool kRowPair, int kRegF>
 __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
-    const float *__restrict__ upstream, float *__restrict__ partial, int ipg) {
-    __shared__ __align__(16) float reg[kRegFloats + kRowPad];  // row-pair interleaved (bwd_rowpairs)
+    const float *__restrict__ upstream, float *__restrict__ partial, int ipg, int regf_dyn) {
+    // regf + kRowPad floats, row-pair interleaved (bwd_rowpairs)
+    __shared__ __align__(16) float reg_static[kRegF > 0 ? kRegF + kRowPad : 1];
+    extern __shared__ __align__(16) float reg_dyn[];
+    float *reg = kRegF > 0 ? reg_static : reg_dyn;
+    const int regf = kRegF > 0 ? kRegF : regf_dyn;
     __shared__ int red[2][4][kRegThreads / 32];
     // Register budget: the walk needs ~40 registers, so per-thread state that
     // is touched once per image lives outside the register file: the world
@@ -501,7 +515,7 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
         }
 #pragma unroll
     for (int c = 0; c < CGS_ACC_STRIDE; ++c) accs[c * kRegThreads + threadIdx.x] = 0.f;
-    for (int i = threadIdx.x; i < kRegFloats + kRowPad; i += kRegThreads) reg[i] = 0.f;  // finite reads past spans
+    for (int i = threadIdx.x; i < regf + kRowPad; i += kRegThreads) reg[i] = 0.f;  // finite reads past spans
     __syncthreads();
     auto pose = [&](int b) {
         if (!pose_smem) return load_pose_f(poses, b);
@@ -525,9 +539,9 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
         const Box R = block_union(footprint_box(s, valid, ylo, yhi, D), red, b);
         if (R.x0 > R.x1) continue;  // uniform
         const int W = R.x1 - R.x0 + 1;
-        // rows per band, even so row pairs never straddle bands (W <= kRegFloats / 2);
+        // rows per band, even so row pairs never straddle bands (W <= regf / 2);
         // the division only runs for regions larger than one band
-        const int HBr = ((R.y1 | 1) - (R.y0 & ~1) + 1) * W <= kRegFloats ? D + 2 : (kRegFloats / W) & ~1;
+        const int HBr = ((R.y1 | 1) - (R.y0 & ~1) + 1) * W <= regf ? D + 2 : (regf / W) & ~1;
         const float c2A = ex2_approx(2.f * s.A);
         const float *src = upstream + (int64_t)b * D * D;
         Moments M{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -635,25 +649,37 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
         const char *v = getenv("CGS_BWD_KERNEL");
         variant = (v && v[0] == 'd') ? 1 : (v && v[0] == 'b') ? 2 : 0;
     }
-    if (layout == CGS_LAYOUT_ROWPAIR && ((D & 1) || D > kRegFloats / 2)) return CGS_ERR_UNSUPPORTED;
-    if ((layout == CGS_LAYOUT_NATURAL && variant == 0 && D <= kRegFloats / 2) || layout == CGS_LAYOUT_ROWPAIR) {
+    const int regf = D <= 128 ? kRegFloats : kRegFloatsLarge;
+    if (layout == CGS_LAYOUT_ROWPAIR && ((D & 1) || D > regf / 2)) return CGS_ERR_UNSUPPORTED;
+    if ((layout == CGS_LAYOUT_NATURAL && variant == 0 && D <= regf / 2) || layout == CGS_LAYOUT_ROWPAIR) {
         dim3 g((unsigned)((n + kRegThreads - 1) / kRegThreads), (unsigned)G);
         const GridF gf = make_grid_f(grid);
         const bool ps = images_per_group <= kMaxPoseImages;
-        if (layout == CGS_LAYOUT_ROWPAIR) {
-            if (ps)
-                raster_bwd_region_kernel<true, true><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, gf, upstream,
-                                                                               partial, images_per_group);
-            else
-                raster_bwd_region_kernel<false, true><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, gf, upstream,
-                                                                                partial, images_per_group);
-        } else if (ps) {
-            raster_bwd_region_kernel<true, false><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, gf, upstream,
-                                                                            partial, images_per_group);
-        } else {
-            raster_bwd_region_kernel<false, false><<<g, kRegThreads, 0, st>>>(splat, n, poses, B, gf, upstream,
-                                                                             partial, images_per_group);
-        }
+        const size_t smem = (size_t)(regf + kRowPad) * sizeof(float);
+        auto launch = [&](auto kern) -> int {
+            const size_t dyn = regf == kRegFloats ? 0 : smem;
+            // a dynamic band beyond 48 KB with the static arrays needs the opt-in
+            if (dyn) {
+                const int rc = ensure_smem_limit((const void *)kern, dyn + 16 * 1024, "raster_bwd_region_kernel");
+                if (rc) return rc;
+            }
+            kern<<<g, kRegThreads, dyn, st>>>(splat, n, poses, B, gf, upstream, partial, images_per_group, regf);
+            return CGS_OK;
+        };
+        int rc;
+        if (regf == kRegFloats)
+            rc = layout == CGS_LAYOUT_ROWPAIR
+                     ? (ps ? launch(raster_bwd_region_kernel<true, true, kRegFloats>)
+                           : launch(raster_bwd_region_kernel<false, true, kRegFloats>))
+                     : (ps ? launch(raster_bwd_region_kernel<true, false, kRegFloats>)
+                           : launch(raster_bwd_region_kernel<false, false, kRegFloats>));
+        else
+            rc = layout == CGS_LAYOUT_ROWPAIR
+                     ? (ps ? launch(raster_bwd_region_kernel<true, true, 0>)
+                           : launch(raster_bwd_region_kernel<false, true, 0>))
+                     : (ps ? launch(raster_bwd_region_kernel<true, false, 0>)
+                           : launch(raster_bwd_region_kernel<false, false, 0>));
+        if (rc) return rc;
         return check_launch("raster_bwd_region_kernel");
     }
     const size_t db_bytes = (2 * (size_t)D * D + kRowPad) * sizeof(float);
