@@ -41,6 +41,7 @@
 // c = 2^(2A): two FMULs per pixel instead of an MUFU.EX2, restarted every 32
 // pixels so the recurrence error stays below 2e-5.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "common.cuh"
@@ -528,6 +529,12 @@ static int render_impl(const double *params, int32_t *status, float *splat, int6
     rc = resident_slots((const void *)raster_fwd_atomic_kernel, kRThreads, smem, &slots, "raster_fwd_atomic_kernel");
     if (rc) return rc;
     int64_t nchunks = fwd_chunks(n, (int64_t)B * bands, slots);
+    // tests: CGS_FWD_CHUNKS forces the chunk count (clamped to chunks of kRChunkMin..kRChunk), e.g. the
+    // fewest, largest chunks -- the coarsest fixed-point units -- on a batch too small to pick them
+    if (const char *env = getenv("CGS_FWD_CHUNKS")) {
+        const long long v = atoll(env);
+        if (v > 0) nchunks = std::min<int64_t>(std::max<int64_t>(v, (n + kRChunk - 1) / kRChunk), max_chunks(n));
+    }
     const int chunk = (int)((n + nchunks - 1) / nchunks);
     nchunks = (n + chunk - 1) / chunk;
     const int64_t mulA = scramble_multiplier(n);

@@ -1095,6 +1095,26 @@ def test_training_render_and_step_large_configs(oracle, case):
     grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
 
 
+@pytest.mark.parametrize("case", ["c4_200k_256", "c5_1m_128"])
+def test_training_render_coarsest_units(oracle, case, monkeypatch):
+    """The render at the coarsest fixed-point units a step can use: chunks of the maximum 8192
+    Gaussians (CGS_FWD_CHUNKS = ceil(n / 8192)), as the bench batches pick at C4 and C5 but a
+    2-image test batch would not (it spreads the Gaussians over more, smaller chunks to fill the
+    GPU).  Within the round-2 target at C4 (200k, 256^2) and 1M Gaussians."""
+    n, D, _ = LARGE_CASES[case]
+    B = 2
+    monkeypatch.setenv("CGS_FWD_CHUNKS", str(-(-n // 8192)))
+    grid = oracle.Grid(D, 0.5, 1.5)
+    params = oracle.init_random(n, 0, grid)
+    poses = [oracle.sample_pose(np.random.default_rng(5000 + i)) for i in range(B)]
+    rend = cs.rasterize_batch(cs.GaussianMixture(params), np.stack([W for W, _ in poses]),
+                              np.stack([t for _, t in poses]), cs.GridSpec(D, 0.5, 1.5), method="direct")
+    for i, (W, t) in enumerate(poses):
+        ref, _ = oracle.rasterize(params, W, t, grid)
+        err = rel_l2(rend[i], ref)  # logged to $CGS_MARGIN_LOG by conftest
+        assert err < R02_RENDER_TARGET, err
+
+
 def test_training_render_heterogeneous_mixture(oracle):
     """50k Gaussians with amplitudes spread 100x and mixed anisotropic scales (0.3..3 px), 128^2,
     4 images with CTF: render, losses and gradients against the oracle, for the direct render
