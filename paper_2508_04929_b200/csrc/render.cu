@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
             walk(s);
         }
     } else {
-        // Row bands (D beyond one 64 KB band, e.g. 256^2 in 4 bands): most of a chunk's Gaussians
+        // Row bands (D beyond one 64 KB band, e.g. 256^2 in 3 bands): most of a chunk's Gaussians
         // miss a band's rows, and lanes skipping them idled while the others walked (half the
         // lanes of a warp active at C4).  So a warp first sifts candidates, one per lane, and
         // stacks the survivors in shared memory; then every lane walks one stacked Gaussian.
