@@ -512,6 +512,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "launch_ms": stage_ms["bwd"],
                      # the same launch counted in the reference's q < 6.5^2 pairs (round 1's unit)
                      "frac_reference_pairs": pairs_per_launch / (stage_ms["bwd"] / 1e3) / 1e9 / bwd_peak},
+        # the forward stage (K0 + weight bound + K3 render) against SURVEY.md 8(d)'s forward cost, 1 EX2 + 4 FP32
+        # per in-ellipse pair: the SFU bound, 16 EX2 lanes/clk/SM (measured 15.6,
+        # profiles/measured_fp32_sfu_peaks_r01.json).  K3 walks rows by a two-multiply recurrence instead of an
+        # EX2 per pixel; what bounds it is the shared-memory atomic unit and issue
+        "roofline_fwd": {"bound": "sfu", "kernel": "raster_fwd_atomic (+ weight bound)",
+                         "achieved": pairs_per_launch / (stage_ms["fwd"] / 1e3) / 1e9,
+                         "peak": 16.0 * 148 * f_mhz * 1e6 / 1e9, "unit": "Gpair/s",
+                         "frac": (pairs_per_launch / (stage_ms["fwd"] / 1e3)) / (16.0 * 148 * f_mhz * 1e6),
+                         "units": "the reference's in-ellipse (image, Gaussian, pixel) pairs, q < 6.5^2",
+                         "launch_ms": stage_ms["fwd"]},
         "roofline_step": {"achieved": step_achieved, "peak": step_peak, "unit": "Gpair/s",
                           "frac": step_achieved / step_peak,
                           "peak_basis": "0.164 SM-clk per in-ellipse pair (fwd+bwd issue), SURVEY.md 8(d)"},
