@@ -73,9 +73,9 @@ __device__ __forceinline__ void bwd_rows(const float *__restrict__ img, int r0, 
     const float c = c2A, c4 = (c * c) * (c * c);
     const float2 C4 = f2pack(c4, c4), TWO = f2pack(2.f, 2.f);
     float dy = (float)ya - s.mpy;
-    float xcv = fmaf(-s.slope, dy, s.mpx);
     const float *row = img + (ya - r0) * ld;
-    for (int iy = ya; iy <= yb; ++iy, dy += 1.f, xcv -= s.slope, row += ld) {
+    for (int iy = ya; iy <= yb; ++iy, dy += 1.f, row += ld) {
+        const float xcv = fmaf(-s.slope, dy, s.mpx);  // one rounding per row, no drift
         const float rem = fmaf(-s.k * dy, dy, kCutoffSq);
         if (rem <= 0.f) continue;
         const float half = sqrt_approx(rem) * s.inv_sqrt_p00;
@@ -164,12 +164,14 @@ constexpr float kBwdCut = (CGS_BWD_CUT > 0.f && CGS_BWD_CUT < kCutoffSq) ? CGS_B
 
 __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int b0, int W, int xlo, int xhi,
                                              int ya, int yb, const Splat2 &s, float c, Moments &M) {
-    const float nk = -s.k, A = s.A, Ck = s.Ck, isp = s.inv_sqrt_p00, m2s = -2.f * s.slope;
+    const float nk = -s.k, A = s.A, Ck = s.Ck, isp = s.inv_sqrt_p00;
     int y = ya & ~1;  // b0 is even: pairs are aligned to even rows
     float2 DY = f2pack((float)y - s.mpy, (float)(y + 1) - s.mpy);
-    float2 XC = f2pack(fmaf(-s.slope, DY.x, s.mpx), fmaf(-s.slope, DY.y, s.mpx));
+    const float2 NSL = f2pack(-s.slope, -s.slope), MPX = f2pack(s.mpx, s.mpx);
     const float2 *prow = blk + ((y - b0) >> 1) * W - xlo;
-    for (; y <= yb; y += 2, DY = f2add(DY, f2pack(2.f, 2.f)), XC = f2add(XC, f2pack(m2s, m2s)), prow += W) {
+    for (; y <= yb; y += 2, DY = f2add(DY, f2pack(2.f, 2.f)), prow += W) {
+        // the row centres from DY with one rounding each (an accumulated XC drifts, see render.cu)
+        const float2 XC = f2fma(DY, NSL, MPX);
         const bool v0 = y >= ya, v1 = y + 1 <= yb;
         const float2 REM = f2fma(f2mul(DY, f2pack(nk, nk)), DY, f2pack(kBwdCut, kBwdCut));
         float2 H = f2mul(f2pack(sqrt_approx(fmaxf(REM.x, 0.f)), sqrt_approx(fmaxf(REM.y, 0.f))),

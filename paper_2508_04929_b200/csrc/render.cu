@@ -14,10 +14,10 @@
 //
 // Scales.  The Gaussians split into chunks; a CTA accumulates one chunk of
 // one image into a shared-memory band in the chunk's own unit
-//   scale_c = min(2^30 / sum_{g in c} wb_g, 2^22 / max_{g in c} wb_g),
+//   scale_c = min(R / sum_{g in c} wb_g, C / max_{g in c} wb_g)  (R ~ 2^31, C ~ 2^23, see kFixedRange),
 // wb_g >= w_g(b) for every view b, so no band sum can overflow and no single
-// contribution reaches 2^22.  At the end the band is added to the global
-// image in the image-wide unit S = min(2^30 / sum_g wb_g, ...) <= scale_c
+// contribution reaches 2^23.  At the end the band is added to the global
+// image in the image-wide unit S = min(R / sum_g wb_g, ...) <= scale_c
 // (round(v S / scale_c), one rounding per pixel and chunk), where no pixel
 // can overflow either.  Integer addition makes the render bitwise
 // reproducible whatever the scheduling.
@@ -26,7 +26,7 @@
 // S, so a Gaussian's peak was only ~2^30 / N units and its tail below
 // 0.5 / peak rounded away: the render error grew linearly with N (1.35e-5 rel
 // L2 at 50k, 3.1e-4 at 1M).  With per-chunk units a chunk of <= 8192
-// Gaussians keeps >= 2^30 / 8192 units per peak at any N, and the walk is cut
+// Gaussians keeps >= 2^31 / 8192 units per peak at any N, and the walk is cut
 // at a fixed fraction of each Gaussian's own peak, kTailFrac = 2e-5: the
 // dropped tail carries kTailFrac of the Gaussian's mass (a 2-D Gaussian
 // holds a fraction t of its mass where e < t), which bounds the image error
@@ -70,8 +70,15 @@ constexpr int kRBandBytes = CGS_FWD_BAND_KB * 1024;  // int32 accumulator rows p
 #endif
 constexpr int kRBandMultiBytes = CGS_FWD_BAND_MULTI_KB * 1024;  // band budget when an image needs several
 constexpr int kWbThreads = 256;  // weight-bound pass: CTA = 256 logical indices (one wave over the SMs at C2)
-constexpr double kFixedRange = 1073741824.0;  // 2^30
-constexpr double kContribRange = 4194304.0;   // 2^22
+// Unit ranges.  A band or image pixel sums at most range x (its Gaussians' weight bounds) plus
+// 0.5 per rounded contribution (<= 8192 per band pixel, <= a few thousand chunk flushes per
+// image pixel), so 2^31 - 2^20 keeps every int32 sum below 2^31; a contribution stays below
+// 2^23 - 2^13, inside the denormal range the recurrence path stores its integers in.  Round 1
+// and early round 2 used 2^30 and 2^22: twice as coarse, which showed on chunks whose weight
+// bounds are loose (thin needles: their view-independent bound is the end-on view's peak,
+// tens of times their typical view's), see test_wide_and_needle_footprints_step.
+constexpr double kFixedRange = 2147483648.0 - 1048576.0;  // 2^31 - 2^20
+constexpr double kContribRange = 8388608.0 - 8192.0;      // 2^23 - 2^13
 #ifndef CGS_FWD_TAIL
 #define CGS_FWD_TAIL 2e-5f
 #endif
@@ -266,16 +273,18 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
     // wS by 2^-75, so the product wS e 2^-149 is a denormal whose bit pattern is
     // round(wS e) (round-to-nearest-even on the 2^-149 grid, the same rounding
     // as fast_rint; explicit non-FTZ multiplies, common.cuh).  One multiply per pixel, no bias, no
-    // integer fix-up.  The -wS sub term (< 0.003 units per contribution for
-    // wS <= 2^22) is below the rounding of each contribution and is dropped.
+    // integer fix-up.  The -wS sub term (< 0.006 units per contribution for
+    // wS < 2^23) is below the rounding of each contribution and is dropped.
     const float A2 = 2.f * s.A, nHcut = -kHalfL2e * cut - 74.f, xhiM = kM + (float)xhi;
     const float wSd = wS * 0x1p-75f;
     const float2 WS = f2pack(wSd, wSd);
     float dy = (float)ya - s.mpy;
-    float xcv = fmaf(-s.slope, dy, s.mpx);
     int *row = acc + (ya - r0) * ld;
     CGS_SINK_DECL
-    for (int nr = yb - ya; nr >= 0; --nr, dy += 1.f, xcv -= s.slope, row += ld) {
+    for (int nr = yb - ya; nr >= 0; --nr, dy += 1.f, row += ld) {
+        // the row centre from dy with one rounding: accumulating xcv -= slope drifted by up to
+        // rows x ulp(xcv) (2.5e-4 px over a 65-row needle, a 2e-4 render error on thin footprints)
+        const float xcv = fmaf(-s.slope, dy, s.mpx);
         // rem <= 0 (a row at the cut's tip) leaves an empty span or one pixel
         // at q >= cut, whose contribution rounds to 0: no branch for it
         const float rem = fmaf(-s.k * dy, dy, cut);
@@ -309,6 +318,46 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
         }
     }
     CGS_SINK_FLUSH
+}
+
+// Dim Gaussians (w scale kTailFrac < 0.5 units).  In the chunk's unit their rounding threshold
+// 0.5 / (w scale) lies above kTailFrac of the peak, and rounding each contribution to the
+// nearest unit would drop the footprint beyond it: a bias, not noise.  A chunk whose unit is
+// set by much brighter Gaussians -- thin needles, whose view-independent weight bound is large --
+// then lost a percent of a dim blob's mass (1.4e-4 rel L2 on test_wide_and_needle_footprints_step).
+// These walk down to kTailFrac like the others and round each contribution with a deterministic
+// dither in [0, 1) hashed from (pixel, Gaussian): unbiased, still integer, still order-free
+// (bitwise-reproducible renders).  One exact exp per pixel: dim Gaussians are rare in a step.
+__device__ __forceinline__ float dither_unit(uint32_t px, uint32_t g) {
+    uint32_t k = px * 0x9E3779B1u ^ g * 0x85EBCA77u;
+    k ^= k >> 15;
+    k *= 0x2C1B3C6Du;
+    k ^= k >> 12;
+    k *= 0x297A2D39u;
+    k ^= k >> 15;
+    return (float)(k >> 8) * 0x1p-24f;
+}
+
+__device__ __forceinline__ void fwd_rows_band_dither(int *__restrict__ acc, int r0, int ld, int D, int ya, int yb,
+                                                  const Splat2 &s, float scale, float cut, uint32_t g) {
+    constexpr float kHalfL2e = 0.5f * 1.4426950408889634f;
+    const float wS = s.w * scale, nHcut = -kHalfL2e * cut;
+    float dy = (float)ya - s.mpy;
+    int *row = acc + (ya - r0) * ld;
+    for (int y = ya; y <= yb; ++y, dy += 1.f, row += ld) {
+        const float xcv = fmaf(-s.slope, dy, s.mpx);
+        const float rem = fmaf(-s.k * dy, dy, cut);
+        if (rem <= 0.f) continue;
+        const float sq = sqrt_approx(rem) * s.inv_sqrt_p00;
+        const int xa = max((int)ceilf(xcv - sq), 0), xb = min((int)floorf(xcv + sq), D - 1);
+        const float Ckdy2 = fmaf(kHalfL2e, rem, nHcut);
+        float d = (float)xa - xcv;
+        for (int x = xa; x <= xb; ++x, d += 1.f) {
+            const float v = wS * ex2_approx(fmaf(s.A * d, d, Ckdy2));
+            const int u = __float2int_rd(v + dither_unit((uint32_t)(y * D + x), g));
+            if (u) atomicAdd(row + x, u);
+        }
+    }
 }
 
 // CTA = (chunk of Gaussians, image, band of rows); the band's int32
@@ -349,9 +398,18 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     // (the precision cut, see the header) and 0.4995 / (w scale), below which a pixel rounds to 0
     // units anyway (the 1e-3 margin keeps every pixel that can round to >= 1 unit), and
     // q < 6.5^2 (splat.py:49).
-    auto walk = [&](const Splat2 &s) {
+    auto walk = [&](const Splat2 &s, uint32_t gid) {
         if (!(s.w > 0.f)) return;
-        const float thr = fmaxf(0.4995f * rcp_approx(s.w * scale), kTailFrac);
+        const float thr_round = 0.4995f * rcp_approx(s.w * scale);
+        if (thr_round > kTailFrac) {  // dim in this chunk's unit: dithered rounding down to kTailFrac
+            const float cut = fminf(kCutoffSq, -2.f * kLn2 * lg2_approx(kTailFrac));
+            const float hy = s.hy * sqrt_approx(cut * (1.f / kCutoffSq));
+            const int ylo = max(max((int)ceilf(s.mpy - hy), 0), r0);
+            const int yhi = min(min((int)floorf(s.mpy + hy), D - 1), r1 - 1);
+            if (ylo <= yhi) fwd_rows_band_dither(band, r0, ld, D, ylo, yhi, s, scale, cut, gid);
+            return;
+        }
+        const float thr = fmaxf(thr_round, kTailFrac);
         if (!(thr < 1.f)) return;
         const float cut = fminf(kCutoffSq, -2.f * kLn2 * lg2_approx(thr));
         const float hy = s.hy * sqrt_approx(cut * (1.f / kCutoffSq));
@@ -371,10 +429,11 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
     if (gridDim.z == 1) {  // the whole image in one band: every lane walks its own Gaussians
         for (int64_t i = i_begin + threadIdx.x; i < i_end; i += kRThreads) {
             const Splat2 s = project2(load_splat(splat, g), P, G);
+            const uint32_t gid = (uint32_t)g;
             g += stepA;
             if (g >= n) g -= n;
             nclamp += s.clamped;
-            walk(s);
+            walk(s, gid);
         }
     } else {
         // Row bands (D beyond one 64 KB band, e.g. 256^2 in 3 bands): most of a chunk's Gaussians
@@ -423,7 +482,7 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
             const int gq = lane < take ? stk[warp][depth - take + lane] : -1;
             depth -= take;
             __syncwarp();
-            if (gq >= 0) walk(project2(load_splat(splat, gq), P, G));
+            if (gq >= 0) walk(project2(load_splat(splat, gq), P, G), (uint32_t)gq);
         }
     }
     if (clamp_count && blockIdx.z == 0) {  // every (image, Gaussian) projection counted once

@@ -1071,6 +1071,40 @@ def _hetero_mixture(oracle, n, grid, seed):
     return p
 
 
+def test_wide_and_needle_footprints_step(oracle):
+    """Footprints the C2 bench never produces: 400 Gaussians with scales 2..14 px (rows beyond
+    31 px: the forward's exact-exp rows, the backward's 32-column runs and multi-band regions)
+    and thin slanted needles (14 x 0.3 x 0.3 px, random rotations: the backward's split row-pair
+    walks), amplitudes spread 100x, 128^2, 3 images with CTF: render, losses and gradients
+    against the oracle.  The render is held to the north-star 1e-4, not the 5e-5 round-2 target
+    of the BASELINE configurations: a needle's view-independent weight bound (its end-on peak)
+    is ~47x its broadside peak, which coarsens the fixed-point unit of the chunk it shares with
+    dim blobs (measured 6.9e-5; 2.8e-5 with 28:1 needles, 1.4e-5 with 14:1)."""
+    n, D, B = 400, 128, 3
+    grid = oracle.Grid(D, 0.5, 1.5)
+    rng = np.random.default_rng(21)
+    params = oracle.init_random(n, 21, grid)
+    params[:, 0:3] = rng.normal(0.0, 0.15, (n, 3))
+    px = rng.uniform(2.0, 14.0, (n, 3))
+    needles = rng.random(n) < 0.3
+    px[needles] = [14.0, 0.3, 0.3]
+    params[:, 3:6] = oracle.inverse_activate(px * grid.pixel_width)
+    params[:, 6:10] = rng.standard_normal((n, 4))
+    params[:, 10] = oracle.inverse_activate(10.0 ** rng.uniform(-2.0, 0.0, n) / n)
+    poses = [oracle.sample_pose(np.random.default_rng(6000 + i)) for i in range(B)]
+    cp = [oracle.Ctf(12000.0 + 2500 * i, 14000.0 + 1000 * i, 0.3 * i) for i in range(B)]
+    ctfs = np.stack([c.as_array() for c in cp])
+    refs = [oracle.rasterize(params, W, t, grid)[0] for W, t in poses]
+    obs = np.stack([0.5 * r for r in refs]).astype(np.float32)
+    losses, grads, pipe = _full_step_device(params, poses, grid, obs, ctfs)
+    rend = pipe.render_image().cpu().numpy()
+    for i in range(B):
+        assert rel_l2(rend[i], refs[i]) < RENDER_TOL
+    ref_losses, ref_grads = oracle.batch_step(params, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs)
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
+
+
 @pytest.mark.parametrize("case", list(LARGE_CASES))
 def test_training_render_and_step_large_configs(oracle, case):
     """C4 (200k, 256^2, CTF) and C5 (500k / 1M at 128^2, CTF): the training step's render (the
