@@ -1071,6 +1071,28 @@ def _hetero_mixture(oracle, n, grid, seed):
     return p
 
 
+@pytest.mark.parametrize("D", [33, 96, 256])
+def test_training_step_other_sizes(oracle, D):
+    """The fused step at image sizes outside the spectral K4 (odd, non-power-of-two, and 256^2 with
+    row bands in both raster kernels), where K4 runs through cuFFT: render, losses and gradients
+    against the oracle (300 Gaussians, 3 images, astigmatic CTFs)."""
+    n, B = 300, 3
+    grid = oracle.Grid(D, 0.5, 1.5)
+    params = oracle.init_random(n, 3, grid)
+    poses = [oracle.sample_pose(np.random.default_rng(8000 + i)) for i in range(B)]
+    cp = [oracle.Ctf(12000.0 + 3000 * i, 14000.0, 0.2 * i) for i in range(B)]
+    ctfs = np.stack([c.as_array() for c in cp])
+    refs = [oracle.rasterize(params, W, t, grid)[0] for W, t in poses]
+    obs = np.stack([0.7 * r for r in refs]).astype(np.float32)
+    losses, grads, pipe = _full_step_device(params, poses, grid, obs, ctfs)
+    rend = pipe.render_image().cpu().numpy()
+    for i in range(B):
+        assert rel_l2(rend[i], refs[i]) < R02_RENDER_TARGET
+    ref_losses, ref_grads = oracle.batch_step(params, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs)
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
+    grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
+
+
 def test_wide_and_needle_footprints_step(oracle):
     """Footprints the C2 bench never produces: 400 Gaussians with scales 2..14 px (rows beyond
     31 px: the forward's exact-exp rows, the backward's 32-column runs and multi-band regions)
