@@ -1093,6 +1093,26 @@ def test_training_step_other_sizes(oracle, D):
     grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
 
 
+@pytest.mark.parametrize("n", [8192, 100000])
+def test_fixed_point_range_worst_case(oracle, n):
+    """The case the fixed-point ranges are sized for: n identical isotropic Gaussians stacked on one
+    point (every weight bound tight, every peak on one pixel), so a chunk band and the image reach
+    (2^31 - 2^20) units at the peak pixel.  No overflow: the render equals n x the single
+    Gaussian's oracle image."""
+    D = 64
+    grid = oracle.Grid(D, 0.5, 1.5)
+    W, t = oracle.sample_pose(np.random.default_rng(1))
+    p = oracle.init_random(n, 0, grid)
+    p[:, 0:3] = 0.0
+    p[:, 3:6] = oracle.inverse_activate(np.full((n, 3), 0.8 * grid.pixel_width))
+    p[:, 6:10] = [1.0, 0.0, 0.0, 0.0]
+    p[:, 10] = oracle.inverse_activate(1.0 / n)
+    rend = cs.rasterize_batch(cs.GaussianMixture(p), W[None], t[None], cs.GridSpec(D, 0.5, 1.5), method="direct")[0]
+    ref = oracle.rasterize(p[:1], W, t, grid)[0] * n
+    assert rend.min() >= 0.0
+    assert rel_l2(rend, ref) < R02_RENDER_TARGET
+
+
 def test_wide_and_needle_footprints_step(oracle):
     """Footprints the C2 bench never produces: 400 Gaussians with scales 2..14 px (rows beyond
     31 px: the forward's exact-exp rows, the backward's 32-column runs and multi-band regions)
