@@ -10,7 +10,7 @@ from paper_2508_04929_b200 import engine, _lib
 D = 128
 grid = oracle.Grid(D, 0.5, 1.5)
 poses = [oracle.sample_pose(np.random.default_rng(7000 + i)) for i in range(2)]
-for sig in ((30, 30, 30), (60, 60, 60), (60, 2, 2), (100, 0.5, 0.5)):
+for sig in ((30, 30, 30), (60, 60, 60), (60, 2, 2), (100, 0.5, 0.5), (30, 0.3, 0.3), (14, 0.3, 0.3)):
     rng = np.random.default_rng(5)
     n = 12
     p = oracle.init_random(n, 5, grid)
@@ -33,5 +33,8 @@ for sig in ((30, 30, 30), (60, 60, 60), (60, 2, 2), (100, 0.5, 0.5)):
     pipe.forward_backward(pt, P, torch.as_tensor(obs).cuda(), torch.as_tensor(ctfs).cuda())
     grads = engine.epilogue_grads(ctx, pipe.partial, pipe.G, pt, 0, 1.0 / len(poses)).cpu().numpy()
     ref_l, ref_g = oracle.batch_step(p, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs)
-    ge = max(np.linalg.norm(grads[:, j] - ref_g[:, j]) / max(np.linalg.norm(ref_g[:, j]), 1e-6 * np.linalg.norm(ref_g)) for j in range(11))
+    cols = [np.linalg.norm(grads[:, j] - ref_g[:, j]) / max(np.linalg.norm(ref_g[:, j]), 1e-6 * np.linalg.norm(ref_g)) for j in range(11)]
+    ge = max(cols)
+    if os.environ.get("DIAG_COLS"):
+        print("   cols", ["%.1e" % c for c in cols])
     print("sigma", sig, "render", ["%.2e" % e for e in errs], "grad col max %.2e" % ge, "loss rel %.2e" % float(np.max(np.abs(pipe.loss.cpu().numpy() - ref_l) / np.abs(ref_l))), flush=True)
