@@ -78,7 +78,8 @@ constexpr int kWbThreads = 256;  // weight-bound pass: CTA = 256 logical indices
 // bounds are loose (thin needles: their view-independent bound is the end-on view's peak,
 // tens of times their typical view's), see test_wide_and_needle_footprints_step.
 constexpr double kFixedRange = 2147483648.0 - 1048576.0;  // 2^31 - 2^20
-constexpr double kContribRange = 8388608.0 - 8192.0;      // 2^23 - 2^13
+constexpr double kContribRange = 2147483648.0 - 1048576.0;  // a single contribution: int32 (see kDen)
+constexpr float kDenormalUnits = 8388608.0f - 8192.0f;      // 2^23 - 2^13: the denormal path's ceiling
 #ifndef CGS_FWD_TAIL
 #define CGS_FWD_TAIL 2e-5f
 #endif
@@ -260,7 +261,11 @@ __device__ int g_sink_dummy;
 #define CGS_SINK_FLUSH
 #endif
 
-template <bool kRecur>
+// kDen: contributions as denormal bit patterns (wS < 2^23, every Gaussian in the BASELINE
+// configurations); otherwise (a Gaussian brighter than 2^23 units in this view, possible since
+// the chunk unit is bounded by the chunk's sum of weight bounds alone) e rides unscaled and each
+// contribution is converted with one rint.
+template <bool kRecur, bool kDen = true>
 __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int ld, int xhi, int ya, int yb,
                                               const Splat2 &s, float scale, float cut) {
     constexpr float kM = 12582912.0f;
@@ -275,8 +280,8 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
     // as fast_rint; explicit non-FTZ multiplies, common.cuh).  One multiply per pixel, no bias, no
     // integer fix-up.  The -wS sub term (< 0.006 units per contribution for
     // wS < 2^23) is below the rounding of each contribution and is dropped.
-    const float A2 = 2.f * s.A, nHcut = -kHalfL2e * cut - 74.f, xhiM = kM + (float)xhi;
-    const float wSd = wS * 0x1p-75f;
+    const float A2 = 2.f * s.A, nHcut = -kHalfL2e * cut - (kDen ? 74.f : 0.f), xhiM = kM + (float)xhi;
+    const float wSd = kDen ? wS * 0x1p-75f : wS;
     const float2 WS = f2pack(wSd, wSd);
     float dy = (float)ya - s.mpy;
     int *row = acc + (ya - r0) * ld;
@@ -304,17 +309,26 @@ __device__ __forceinline__ void fwd_rows_band(int *__restrict__ acc, int r0, int
             int x = xa;
 #pragma unroll 1
             for (; x < xb; x += 2) {
-                const float2 v = f2mul_keep_denorm(WS, E);
-                CGS_BAND_ADD(row + x, __float_as_int(v.x));
-                CGS_BAND_ADD(row + x + 1, __float_as_int(v.y));
+                if (kDen) {
+                    const float2 v = f2mul_keep_denorm(WS, E);
+                    CGS_BAND_ADD(row + x, __float_as_int(v.x));
+                    CGS_BAND_ADD(row + x + 1, __float_as_int(v.y));
+                } else {
+                    const float2 v = f2mul(WS, E);
+                    CGS_BAND_ADD(row + x, __float2int_rn(v.x));
+                    CGS_BAND_ADD(row + x + 1, __float2int_rn(v.y));
+                }
                 f2scale(E, R);
                 f2scale(R, C4);
             }
-            if (x == xb) CGS_BAND_ADD(row + x, __float_as_int(fmul_keep_denorm(wSd, E.x)));
+            if (x == xb)
+                CGS_BAND_ADD(row + x, kDen ? __float_as_int(fmul_keep_denorm(wSd, E.x)) : __float2int_rn(wSd * E.x));
         } else {
             float d = dx;
-            for (int x = xa; x <= xb; ++x, d += 1.f)
-                atomicAdd(row + x, __float_as_int(fmul_keep_denorm(wSd, ex2_approx(fmaf(s.A * d, d, Ckdy2)))));
+            for (int x = xa; x <= xb; ++x, d += 1.f) {
+                const float e = ex2_approx(fmaf(s.A * d, d, Ckdy2));
+                atomicAdd(row + x, kDen ? __float_as_int(fmul_keep_denorm(wSd, e)) : __float2int_rn(wSd * e));
+            }
         }
     }
     CGS_SINK_FLUSH
@@ -421,10 +435,17 @@ __global__ void __launch_bounds__(kRThreads, CGS_FWD_MINB) raster_fwd_atomic_ker
         return;
 #endif
         // widest row = 2 sqrt(cut / p00) = 2 * 6.5 sqrt(cut / 6.5^2) / sqrt(p00)
-        if (13.f * sqrt_approx(cut * (1.f / kCutoffSq)) * s.inv_sqrt_p00 < 31.f)
-            fwd_rows_band<true>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
-        else
-            fwd_rows_band<false>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
+        const bool recur = 13.f * sqrt_approx(cut * (1.f / kCutoffSq)) * s.inv_sqrt_p00 < 31.f;
+        if (s.w * scale < kDenormalUnits) {
+            if (recur)
+                fwd_rows_band<true>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
+            else
+                fwd_rows_band<false>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
+        } else if (recur) {
+            fwd_rows_band<true, false>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
+        } else {
+            fwd_rows_band<false, false>(band, r0, ld, D - 1, ylo, yhi, s, scale, cut);
+        }
     };
     if (gridDim.z == 1) {  // the whole image in one band: every lane walks its own Gaussians
         for (int64_t i = i_begin + threadIdx.x; i < i_end; i += kRThreads) {

@@ -1118,10 +1118,10 @@ def test_wide_and_needle_footprints_step(oracle):
     31 px: the forward's exact-exp rows, the backward's 32-column runs and multi-band regions)
     and thin slanted needles (14 x 0.3 x 0.3 px, random rotations: the backward's split row-pair
     walks), amplitudes spread 100x, 128^2, 3 images with CTF: render, losses and gradients
-    against the oracle.  The render is held to the north-star 1e-4, not the 5e-5 round-2 target
-    of the BASELINE configurations: a needle's view-independent weight bound (its end-on peak)
-    is ~47x its broadside peak, which coarsens the fixed-point unit of the chunk it shares with
-    dim blobs (measured 6.9e-5; 2.8e-5 with 28:1 needles, 1.4e-5 with 14:1)."""
+    against the oracle, within the round-2 target.  A needle's view-independent weight bound (its
+    end-on peak) is ~47x its broadside peak, which coarsened the fixed-point unit of the chunk it
+    shares with dim blobs (1.4e-4 before the unit was bounded by the chunk's sum of bounds alone,
+    with a non-denormal path for Gaussians brighter than 2^23 units in view)."""
     n, D, B = 400, 128, 3
     grid = oracle.Grid(D, 0.5, 1.5)
     rng = np.random.default_rng(21)
@@ -1141,7 +1141,7 @@ def test_wide_and_needle_footprints_step(oracle):
     losses, grads, pipe = _full_step_device(params, poses, grid, obs, ctfs)
     rend = pipe.render_image().cpu().numpy()
     for i in range(B):
-        assert rel_l2(rend[i], refs[i]) < RENDER_TOL
+        assert rel_l2(rend[i], refs[i]) < R02_RENDER_TARGET
     ref_losses, ref_grads = oracle.batch_step(params, poses, grid, [oracle.ctf_evaluate(c, grid) for c in cp], obs)
     np.testing.assert_allclose(losses, ref_losses, rtol=1e-4)
     grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
