@@ -14,9 +14,11 @@
 //
 // Scales.  The Gaussians split into chunks; a CTA accumulates one chunk of
 // one image into a shared-memory band in the chunk's own unit
-//   scale_c = min(R / sum_{g in c} wb_g, C / max_{g in c} wb_g)  (R ~ 2^31, C ~ 2^23, see kFixedRange),
-// wb_g >= w_g(b) for every view b, so no band sum can overflow and no single
-// contribution reaches 2^23.  At the end the band is added to the global
+//   scale_c = R / sum_{g in c} wb_g  (R = 2^31 - 2^20, see kFixedRange),
+// wb_g >= w_g(b) for every view b, so no band sum can overflow.  A Gaussian
+// brighter than 2^23 units in its view takes the rint path instead of the
+// denormal one (fwd_rows_band kDen), one dimmer than 0.5 / kTailFrac units the
+// dithered one (fwd_rows_band_dither).  At the end the band is added to the global
 // image in the image-wide unit S = min(R / sum_g wb_g, ...) <= scale_c
 // (round(v S / scale_c), one rounding per pixel and chunk), where no pixel
 // can overflow either.  Integer addition makes the render bitwise
@@ -71,12 +73,12 @@ constexpr int kRBandBytes = CGS_FWD_BAND_KB * 1024;  // int32 accumulator rows p
 constexpr int kRBandMultiBytes = CGS_FWD_BAND_MULTI_KB * 1024;  // band budget when an image needs several
 constexpr int kWbThreads = 256;  // weight-bound pass: CTA = 256 logical indices (one wave over the SMs at C2)
 // Unit ranges.  A band or image pixel sums at most range x (its Gaussians' weight bounds) plus
-// 0.5 per rounded contribution (<= 8192 per band pixel, <= a few thousand chunk flushes per
-// image pixel), so 2^31 - 2^20 keeps every int32 sum below 2^31; a contribution stays below
-// 2^23 - 2^13, inside the denormal range the recurrence path stores its integers in.  Round 1
-// and early round 2 used 2^30 and 2^22: twice as coarse, which showed on chunks whose weight
-// bounds are loose (thin needles: their view-independent bound is the end-on view's peak,
-// tens of times their typical view's), see test_wide_and_needle_footprints_step.
+// up to one unit per rounded contribution (<= 8192 per band pixel, <= a few thousand chunk
+// flushes per image pixel), so 2^31 - 2^20 keeps every int32 sum below 2^31.  Contributions
+// below 2^23 - 2^13 units take the denormal path.  Until late round 2 the unit was also capped
+// at 2^22 / max wb (and the range was 2^30), which coarsened chunks whose weight bounds are
+// loose (thin needles: their view-independent bound is the end-on view's peak, tens of times
+// their typical view's), see test_wide_and_needle_footprints_step.
 constexpr double kFixedRange = 2147483648.0 - 1048576.0;  // 2^31 - 2^20
 constexpr double kContribRange = 2147483648.0 - 1048576.0;  // a single contribution: int32 (see kDen)
 constexpr float kDenormalUnits = 8388608.0f - 8192.0f;      // 2^23 - 2^13: the denormal path's ceiling
