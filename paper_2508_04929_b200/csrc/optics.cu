@@ -1280,6 +1280,119 @@ static int cufft_check(cufftResult r, const char *what) {
     return CGS_ERR_CUFFT;
 }
 
+
+// ---- spectral K4 through cuFFT, for the sizes without a one-CTA line-FFT
+// kernel (C4: a 256^2 half spectrum is 264 KB, more than one CTA's shared
+// memory).  Same records and loss as the line-FFT path, natural [ky][kx] half
+// spectrum: F(obs) then H_sym / D^2.  Per step: int32 render -> float (scale),
+// R2C, one filter/loss kernel over the half spectrum, C2R -- one transform
+// pair instead of cgs_ctf_mse's two, and H from the records.
+constexpr int kSpecFftThreads = 256, kSpecFftElems = 8 * kSpecFftThreads;  // half-spectrum elements per CTA
+
+__host__ __device__ inline int spec_fft_ctas(int D) { return (D * (D / 2 + 1) + kSpecFftElems - 1) / kSpecFftElems; }
+// record stride in float2: F (n complex) + H (n floats), padded to an even float count (odd D: n odd)
+__host__ __device__ inline int64_t spec_fft_record_f2(int D) {
+    const int64_t n = (int64_t)D * (D / 2 + 1);
+    return (3 * n + (n & 1)) / 2;
+}
+
+// out = in / scale (the fixed-point render as floats, the R2C's input)
+__global__ void __launch_bounds__(256) fixed_scale_kernel(const int *__restrict__ in, float *__restrict__ out,
+                                                          int64_t count, const float *__restrict__ scale_ptr) {
+    const float inv = 1.f / __ldg(scale_ptr);
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
+    if (i + 3 < count) {
+        const int4 v = __ldg(reinterpret_cast<const int4 *>(in + i));
+        *reinterpret_cast<float4 *>(out + i) = make_float4((float)v.x * inv, (float)v.y * inv, (float)v.z * inv,
+                                                           (float)v.w * inv);
+    } else {
+        for (int64_t j = i; j < count; ++j) out[j] = (float)in[j] * inv;
+    }
+}
+
+// record b: F(obs) as cuFFT left it, then H_sym / D^2 (grid: CTAs per image x B)
+__global__ void __launch_bounds__(kSpecFftThreads) obs_record_fft_kernel(const float2 *__restrict__ spectrum,
+                                                                         const double *__restrict__ ctf, int D,
+                                                                         double pix, float2 *__restrict__ rec) {
+    const int b = blockIdx.y, P = D / 2 + 1, n = D * P;
+    __shared__ CtfConst cc;
+    if (threadIdx.x == 0) {
+        CtfConst c = load_ctf(ctf + 8 * (int64_t)b, D, pix);
+        c.inv_dA = 1.0 / c.dA;
+        c.pl = kPiD * c.lam;
+        c.cs3 = 0.5 * kPiD * c.cs * c.lam * c.lam * c.lam;
+        cc = c;
+    }
+    __syncthreads();
+    const float2 *src = spectrum + (int64_t)b * n;
+    float2 *dst = rec + (int64_t)b * spec_fft_record_f2(D);
+    float *hd = reinterpret_cast<float *>(dst + n);
+    const float inv_d2 = 1.f / ((float)D * (float)D);
+    const int end = min(n, (int)(blockIdx.x + 1) * kSpecFftElems);
+    for (int i = blockIdx.x * kSpecFftElems + threadIdx.x; i < end; i += kSpecFftThreads) {
+        const int ky = i / P, kx = i - ky * P;
+        dst[i] = src[i];
+        hd[i] = ctf_sym(cc, D, ky, kx) * inv_d2;
+    }
+}
+
+// r = H F(render) - F(obs) over the half spectrum in place of F(render), then
+// CTF^T and the 2/D^2 residual scale (C2R is unnormalised: Hh = H / D^2 gives
+// the 1/D^2).  Loss by Parseval, weight 1 on the self-conjugate columns kx = 0
+// and D/2 (even D), 2 elsewhere; per-CTA fp64 sums, the image's last CTA adds
+// them in CTA order (deterministic) and resets its counter.
+__global__ void __launch_bounds__(kSpecFftThreads) ctf_mse_spec_fft_kernel(
+    float2 *__restrict__ spectrum, const float2 *__restrict__ obs_spec, const int64_t *__restrict__ rows, int D,
+    double *__restrict__ part, unsigned *__restrict__ count, double *__restrict__ loss, int32_t *status) {
+    const int b = blockIdx.y, P = D / 2 + 1, n = D * P, K = gridDim.x;
+    const float2 *O = obs_spec + (rows ? __ldg(rows + b) : (int64_t)b) * spec_fft_record_f2(D);
+    const float *Hh = reinterpret_cast<const float *>(O + n);
+    float2 *Z = spectrum + (int64_t)b * n;
+    const float d2 = (float)D * (float)D, sc = 2.f / d2;
+    double acc = 0.0;
+    const int end = min(n, (int)(blockIdx.x + 1) * kSpecFftElems);
+    for (int i = blockIdx.x * kSpecFftElems + threadIdx.x; i < end; i += kSpecFftThreads) {
+        const int kx = i % P;
+        const float h = __ldg(Hh + i);
+        const float2 z = Z[i], o = __ldg(O + i);
+        const float hd = h * d2;
+        const float rx = fmaf(hd, z.x, -o.x), ry = fmaf(hd, z.y, -o.y);
+        const double w = (kx == 0 || (!(D & 1) && kx == D / 2)) ? 1.0 : 2.0;
+        acc += w * ((double)rx * rx + (double)ry * ry);
+        const float hs = h * sc;
+        Z[i] = make_float2(hs * rx, hs * ry);
+    }
+    __shared__ double scratch[kSpecFftThreads / 32];
+    __shared__ bool last;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kSpecFftThreads / 32; ++w) t += scratch[w];
+        part[(int64_t)b * K + blockIdx.x] = t;
+        __threadfence();
+        last = atomicAdd(count + b, 1u) == (unsigned)(K - 1);
+        if (last) {
+            __threadfence();
+            double s = 0.0;
+            for (int k = 0; k < K; ++k) s += *(volatile const double *)(part + (int64_t)b * K + k);
+            const double l = poison_loss(s / ((double)d2 * (double)d2), status);
+            loss[b] = l;
+            if (status && !isfinite(l)) atomicOr(status, CGS_STATUS_NONFINITE_LOSS);
+            count[b] = 0;
+        }
+    }
+}
+
+static int spec_fft_setup(FftPlan *p, int32_t B, cgs_grid grid, cudaStream_t st) {
+    if (!p || p->D != grid.size || p->B != B) return CGS_ERR_ARG;
+    int rc = cufft_check(cufftSetStream(p->r2c, st), "cufftSetStream");
+    if (rc) return rc;
+    return cufft_check(cufftSetStream(p->c2r, st), "cufftSetStream");
+}
+
 }  // namespace cgs
 
 using namespace cgs;
@@ -1450,6 +1563,59 @@ extern "C" int cgs_ctf_mse_spectral_fixed_rows(const int32_t *render_fixed, cons
                                             st);
     set_error_detail("cgs_ctf_mse_spectral_fixed_rows", "image size must be 64 or 128");
     return CGS_ERR_UNSUPPORTED;
+}
+
+extern "C" int64_t cgs_obs_spectrum_fft_elems(int32_t size, int32_t B) {
+    if (size < 2 || B < 0) return 0;
+    return (int64_t)B * 2 * spec_fft_record_f2(size);
+}
+
+extern "C" size_t cgs_spectral_fft_workspace_bytes(int32_t size, int32_t B) {
+    if (size < 2 || B <= 0) return 0;
+    return (size_t)B * spec_fft_ctas(size) * sizeof(double) + (size_t)B * sizeof(unsigned);
+}
+
+extern "C" int cgs_obs_spectrum_fft(void *plan, const float *obs, const double *ctf, int32_t B, cgs_grid grid,
+                                    void *spectrum, float *spec, void *stream) {
+    if (!obs || !ctf || !spec || !spectrum || B <= 0 || !(grid.pixel_size > 0)) return CGS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = spec_fft_setup((FftPlan *)plan, B, grid, st);
+    if (rc) return rc;
+    FftPlan *p = (FftPlan *)plan;
+    rc = cufft_check(cufftExecR2C(p->r2c, (cufftReal *)obs, (cufftComplex *)spectrum), "cufftExecR2C");
+    if (rc) return rc;
+    const int D = grid.size;
+    obs_record_fft_kernel<<<dim3(spec_fft_ctas(D), B), kSpecFftThreads, 0, st>>>(
+        (const float2 *)spectrum, ctf, D, grid.pixel_size, (float2 *)spec);
+    return check_launch("obs_record_fft_kernel");
+}
+
+extern "C" int cgs_ctf_mse_spectral_fft(void *plan, const int32_t *render_fixed, const float *render_scale,
+                                        const float *obs_spec, const int64_t *rows, int32_t B, cgs_grid grid,
+                                        void *spectrum, void *workspace, float *upstream, double *loss,
+                                        int32_t *status, void *stream) {
+    if (!render_fixed || !render_scale || !obs_spec || !spectrum || !workspace || !upstream || !loss || B <= 0 ||
+        (const void *)render_fixed == (const void *)upstream)
+        return CGS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = spec_fft_setup((FftPlan *)plan, B, grid, st);
+    if (rc) return rc;
+    FftPlan *p = (FftPlan *)plan;
+    const int D = grid.size, K = spec_fft_ctas(D);
+    const int64_t count = (int64_t)B * D * D;
+    fixed_scale_kernel<<<(unsigned)(((count + 3) / 4 + 255) / 256), 256, 0, st>>>(render_fixed, upstream, count,
+                                                                                 render_scale);
+    rc = check_launch("fixed_scale_kernel");
+    if (rc) return rc;
+    rc = cufft_check(cufftExecR2C(p->r2c, (cufftReal *)upstream, (cufftComplex *)spectrum), "cufftExecR2C");
+    if (rc) return rc;
+    double *part = (double *)workspace;
+    unsigned *cnt = (unsigned *)(part + (int64_t)B * K);
+    ctf_mse_spec_fft_kernel<<<dim3(K, B), kSpecFftThreads, 0, st>>>((float2 *)spectrum, (const float2 *)obs_spec,
+                                                                   rows, D, part, cnt, loss, status);
+    rc = check_launch("ctf_mse_spec_fft_kernel");
+    if (rc) return rc;
+    return cufft_check(cufftExecC2R(p->c2r, (cufftComplex *)spectrum, (cufftReal *)upstream), "cufftExecC2R");
 }
 
 extern "C" int cgs_fourier_filter(const float *in, float *out, int32_t B, cgs_grid grid, const double *ctf,

@@ -113,8 +113,10 @@ class DeviceContext:
             self._bufs[name] = t
         return t[: max(int(numel), 1)]
 
-    def plan(self, size: int, batch: int) -> int:
-        key = (int(size), int(batch))
+    def plan(self, size: int, batch: int, tag: str = "") -> int:
+        """A cuFFT plan for (size, batch), cached; ``tag`` keeps separate plans (and cuFFT work
+        areas) for users that may run on different streams."""
+        key = (int(size), int(batch), tag)
         if key not in self._plans:
             h = ctypes.c_void_p()
             _lib.call("cgs_fft_plan_create", int(size), int(batch), ctypes.byref(h))
@@ -245,19 +247,54 @@ def loss_residual(ctx, model, obs, resid=None):
     return loss
 
 
+def spectral_kind(ctx, D: int, render: str = "direct"):
+    """Which spectral K4 a training step at image size D takes: "lf" (one CTA per image on line
+    FFTs, D = 64 / 128), "fft" (cuFFT R2C, one filter/loss kernel, C2R: the other sizes, for the
+    direct fixed-point render) or None (the real-space K4: D = 32, whose fused kernel is one
+    launch; CGS_CTF_SPATIAL=1, or CGS_SPEC_FFT=0 for the cuFFT form, A/B)."""
+    if os.environ.get("CGS_CTF_SPATIAL", "0") == "1":
+        return None
+    if int(ctx.lib.cgs_obs_spectrum_elems(D, 1)):
+        return "lf"
+    if render == "direct" and D >= 2 and D != 32 and os.environ.get("CGS_SPEC_FFT", "1") != "0":
+        return "fft"
+    return None
+
+
+def obs_record_elems(ctx, D: int) -> int:
+    """Floats per observation record of the spectral K4 at size D (0: no spectral K4)."""
+    kind = spectral_kind(ctx, D)
+    if kind == "lf":
+        return int(ctx.lib.cgs_obs_spectrum_elems(D, 1))
+    if kind == "fft":
+        return int(ctx.lib.cgs_obs_spectrum_fft_elems(D, 1))
+    return 0
+
+
 def obs_spectra(ctx, obs, ctfs, grid_s, chunk: int = 4096, out=None):
     """Spectral-K4 records of a device stack (obs f32 [R][D][D], ctfs f64 [R][8]): F(obs) and
-    H_sym / D^2 per observation, f32 [R][3 D (D/2+1)] (cgs_obs_spectrum), or None when the size
-    has no spectral path.  ``out``: an existing [R][per] buffer to fill."""
+    H_sym / D^2 per observation, f32 [R][3 D (D/2+1)] (cgs_obs_spectrum, or cgs_obs_spectrum_fft
+    with its own cuFFT plan and scratch), or None when the size has no spectral path.  ``out``:
+    an existing [R][per] buffer to fill."""
     R, D = obs.shape[0], grid_s.size
-    per = int(ctx.lib.cgs_obs_spectrum_elems(D, 1))
-    if per == 0 or os.environ.get("CGS_CTF_SPATIAL", "0") == "1":
+    kind = spectral_kind(ctx, D)
+    if kind is None:
         return None
+    per = obs_record_elems(ctx, D)
     if out is None:
         out = torch.empty((R, per), dtype=torch.float32, device=ctx.device)
+    if kind == "fft":  # cuFFT scratch of at most 256 MB per chunk
+        chunk = max(1, min(chunk, (256 << 20) // (8 * D * (D // 2 + 1))))
+        spectrum = torch.empty(2 * int(ctx.lib.cgs_fft_spectrum_elems(D, min(chunk, R))), dtype=torch.float32,
+                               device=ctx.device)
     for a in range(0, R, chunk):
         b = min(R, a + chunk)
-        _lib.call("cgs_obs_spectrum", _ptr(obs[a:b]), _ptr(ctfs[a:b]), b - a, grid_s, _ptr(out[a:b]), ctx.stream)
+        if kind == "fft":
+            _lib.call("cgs_obs_spectrum_fft", ctx.plan(D, b - a, tag="records"), _ptr(obs[a:b]), _ptr(ctfs[a:b]),
+                      b - a, grid_s, _ptr(spectrum), _ptr(out[a:b]), ctx.stream)
+        else:
+            _lib.call("cgs_obs_spectrum", _ptr(obs[a:b]), _ptr(ctfs[a:b]), b - a, grid_s, _ptr(out[a:b]),
+                      ctx.stream)
     return out
 
 
@@ -321,10 +358,14 @@ class StepPipeline:
         self.plan = ctx.plan(D, self.B)
         # zeroed once: the render's weight-bound pass keeps a self-resetting counter in it
         self.render_ws = torch.zeros(ctx.lib.cgs_render_workspace_bytes(n) // 4 + 1, dtype=torch.float32, device=dev)
-        spec_elems = int(ctx.lib.cgs_obs_spectrum_elems(D, self.B))
-        self.obs_spec = None  # per-step observation records of the spectral K4 (None: real-space K4)
-        if spec_elems and os.environ.get("CGS_CTF_SPATIAL", "0") != "1":
-            self.obs_spec = torch.empty(spec_elems, dtype=torch.float32, device=dev)
+        # per-step observation records of the spectral K4 (None: real-space K4)
+        self.spectral_kind = spectral_kind(ctx, D, render)
+        self.obs_spec = self.spec_ws = None
+        if self.spectral_kind is not None:
+            self.obs_spec = torch.empty(obs_record_elems(ctx, D) * self.B, dtype=torch.float32, device=dev)
+        if self.spectral_kind == "fft":  # per-CTA loss sums + self-resetting counters, zeroed once
+            self.spec_ws = torch.zeros(int(ctx.lib.cgs_spectral_fft_workspace_bytes(D, self.B)) // 8 + 1,
+                                       dtype=torch.float64, device=dev)
         self.T = int(ctx.lib.cgs_bin_tiles(D, tile))
         self.S = int(ctx.lib.cgs_bin_segments(n))
         if render == "tiles":
@@ -382,6 +423,8 @@ class StepPipeline:
         n = 2 + (0 if spectral else 2) + 1 + 1
         if not ctf:
             return n + 1
+        if spectral and self.spectral_kind == "fft":  # fixed_scale + the filter kernel around cuFFT's own
+            return n + (2 if obs_spectrum else 3)
         if spectral:
             return n + (1 if obs_spectrum else 2)
         fused = self.D in (32, 64, 128) and os.environ.get("CGS_CTF_CUFFT", "0") != "1"
@@ -389,8 +432,9 @@ class StepPipeline:
 
     @property
     def spectral(self) -> bool:
-        """K4 runs in the Fourier domain (cgs_ctf_mse_spectral) for D = 64 / 128 with a CTF;
-        CGS_CTF_SPATIAL=1 keeps the real-space kernel (A/B)."""
+        """K4 runs in the Fourier domain with a CTF: cgs_ctf_mse_spectral* for D = 64 / 128,
+        cgs_ctf_mse_spectral_fft for the other sizes but 32 (``spectral_kind``); CGS_CTF_SPATIAL=1
+        keeps the real-space K4 (A/B)."""
         return self.obs_spec is not None
 
     def _render_scale(self):
@@ -446,12 +490,22 @@ class StepPipeline:
         if ctf is not None and self.spectral:
             if obs_rows is not None and not fixed:  # only the fixed-point K4 reads records by row
                 obs_spec, obs_rows = obs_spec.index_select(0, obs_rows), None
+            fft = self.spectral_kind == "fft"
             if obs_spec is None:  # this batch's records (a dataset passes its precomputed ones)
-                _lib.call("cgs_obs_spectrum", _ptr(obs), _ptr(ctf), self.B, self.grid, _ptr(self.obs_spec), s)
+                if fft:
+                    _lib.call("cgs_obs_spectrum_fft", self.plan, _ptr(obs), _ptr(ctf), self.B, self.grid,
+                              _ptr(self.spectrum), _ptr(self.obs_spec), s)
+                else:
+                    _lib.call("cgs_obs_spectrum", _ptr(obs), _ptr(ctf), self.B, self.grid, _ptr(self.obs_spec), s)
                 obs_spec = self.obs_spec
             # the upstream goes out with row pairs interleaved: the backward's region staging is a copy
-            up_layout = _lib.CGS_LAYOUT_ROWPAIR
-            if fixed and obs_rows is not None:
+            # (cuFFT's C2R writes it in natural order)
+            up_layout = _lib.CGS_LAYOUT_NATURAL if fft else _lib.CGS_LAYOUT_ROWPAIR
+            if fft:
+                _lib.call("cgs_ctf_mse_spectral_fft", self.plan, _ptr(self.render), _ptr(self._render_scale()),
+                          _ptr(obs_spec), _ptr(obs_rows), self.B, self.grid, _ptr(self.spectrum),
+                          _ptr(self.spec_ws), _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
+            elif fixed and obs_rows is not None:
                 _lib.call("cgs_ctf_mse_spectral_fixed_rows", _ptr(self.render), _ptr(self._render_scale()),
                           _ptr(obs_spec), _ptr(obs_rows), self.B, self.grid, _ptr(self.upstream), _ptr(self.loss),
                           _ptr(self.status), up_layout, s)

@@ -402,8 +402,8 @@ class Reconstructor:
             out["idx"] = torch.empty(r, dtype=torch.int64, device=dev)
             out["idx_host"] = torch.empty(r, dtype=torch.int64).pin_memory()
             out["spec"] = None
-            per = int(self.ctx.lib.cgs_obs_spectrum_elems(D, 1))
-            if out["ctfs"] is not None and per and os.environ.get("CGS_CTF_SPATIAL", "0") != "1":
+            per = engine.obs_record_elems(self.ctx, D)
+            if out["ctfs"] is not None and per:
                 out["spec"] = torch.empty((r, per), dtype=torch.float32, device=dev)
         with torch.cuda.stream(stream):
             if out.get("event") is not None:  # the pinned index buffer is reused: its last copy must be done

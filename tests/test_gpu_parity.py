@@ -367,6 +367,68 @@ def test_spectral_ctf_mse_matches_oracle(oracle, D):
     assert ctx.lib.cgs_obs_spectrum(o.data_ptr(), None, B, gs, spec.data_ptr(), None) == 1
 
 
+@pytest.mark.parametrize("D", [33, 96, 256])
+def test_spectral_fft_ctf_mse_matches_oracle(oracle, D):
+    """The spectral K4 through cuFFT (cgs_obs_spectrum_fft + cgs_ctf_mse_spectral_fft, the sizes
+    without a line-FFT kernel: C4's 256^2, an odd size) against the reference's centred FFTs:
+    loss by Parseval (weight 1 on the self-conjugate columns), CTF^T upstream; a cgs_render_fixed
+    image in; records read by row (a repeat, out of order) bitwise equal to row b; a second call
+    bitwise equal to the first (the per-image counters reset themselves)."""
+    B = 3
+    grid = oracle.Grid(D, 0.5, 1.5)
+    rng = np.random.default_rng(70 + D)
+    fixed = (rng.standard_normal((B, D, D)) * 2.0 ** 20).astype(np.int32)
+    render = fixed.astype(np.float64) / 2.0 ** 20
+    obs = rng.standard_normal((B, D, D)).astype(np.float32)
+    ctfs = [oracle.Ctf(12000.0, 15000.0, 0.7), oracle.Ctf(20000.0, 18000.0, -0.3, phase_shift=0.4),
+            oracle.Ctf(9000.0, 9500.0, 1.2, b_factor=40.0)]
+    ctx = engine.DeviceContext.get()
+    gs = _lib.grid_struct(D, grid.extent, grid.pixel_size)
+    rf, o = _dev(fixed, torch.int32), _dev(obs, torch.float32)
+    c = _dev(np.stack([x.as_array() for x in ctfs]), torch.float64)
+    scale = torch.tensor([2.0 ** 20], dtype=torch.float32, device=o.device)
+    per = int(ctx.lib.cgs_obs_spectrum_fft_elems(D, 1))
+    n = D * (D // 2 + 1)
+    assert per == 3 * n + n % 2  # padded to an even float count (float2 alignment of the next record)
+    spec = torch.empty((B, per), dtype=torch.float32, device=o.device)
+    wspec = torch.empty(2 * int(ctx.lib.cgs_fft_spectrum_elems(D, B)), dtype=torch.float32, device=o.device)
+    ws = torch.zeros(int(ctx.lib.cgs_spectral_fft_workspace_bytes(D, B)), dtype=torch.uint8, device=o.device)
+    plan = ctx.plan(D, B)
+    _lib.call("cgs_obs_spectrum_fft", plan, o.data_ptr(), c.data_ptr(), B, gs, wspec.data_ptr(), spec.data_ptr(),
+              ctx.stream)
+    status = torch.zeros(1, dtype=torch.int32, device=o.device)
+
+    def k4(rows=None, src=rf):
+        up = torch.empty((B, D, D), dtype=torch.float32, device=o.device)
+        loss = torch.empty(B, dtype=torch.float64, device=o.device)
+        _lib.call("cgs_ctf_mse_spectral_fft", plan, src.data_ptr(), scale.data_ptr(), spec.data_ptr(),
+                  0 if rows is None else rows.data_ptr(), B, gs, wspec.data_ptr(), ws.data_ptr(), up.data_ptr(),
+                  loss.data_ptr(), status.data_ptr(), ctx.stream)
+        return up, loss
+
+    up, loss = k4()
+    up_again, loss_again = k4()
+    rows = torch.tensor([2, 0, 2], dtype=torch.int64, device=o.device)
+    up_rows, loss_rows = k4(rows, rf.index_select(0, rows).contiguous())
+    torch.cuda.synchronize()
+    for b in range(B):
+        H = oracle.ctf_evaluate(ctfs[b], grid)
+        m_ref = oracle.apply_ctf(render[b], H)
+        u_ref = oracle.apply_ctf((2.0 / (D * D)) * (m_ref - obs[b]), H)
+        l_ref = oracle.loss_mse(m_ref, obs[b])
+        assert rel_l2(up[b].cpu().numpy(), u_ref) < 1e-5
+        assert abs(loss[b].item() - l_ref) <= 1e-5 * l_ref
+    assert torch.equal(up, up_again) and torch.equal(loss, loss_again)
+    assert torch.equal(up_rows, up.index_select(0, rows)) and torch.equal(loss_rows, loss.index_select(0, rows))
+    assert status.item() == 0
+    # wrong plan batch, missing workspace
+    assert ctx.lib.cgs_ctf_mse_spectral_fft(ctx.plan(D, B + 1), rf.data_ptr(), scale.data_ptr(), spec.data_ptr(),
+                                            None, B, gs, wspec.data_ptr(), ws.data_ptr(), up.data_ptr(),
+                                            loss.data_ptr(), None, None) == 1
+    assert ctx.lib.cgs_ctf_mse_spectral_fft(plan, rf.data_ptr(), scale.data_ptr(), spec.data_ptr(), None, B, gs,
+                                            wspec.data_ptr(), None, up.data_ptr(), loss.data_ptr(), None, None) == 1
+
+
 @pytest.mark.parametrize("D", [64, 128])
 def test_spectral_rows_equal_gathered_records(D):
     """cgs_ctf_mse_spectral_fixed_rows (K4 reading image b's record at row rows[b] of a resident
