@@ -241,15 +241,17 @@ int cgs_ctf_mse_spectral_fixed_rows(const int32_t *render_fixed, const float *re
  * cgs_spectral_fft_workspace_bytes(D, B) bytes, zero-initialised once (per-CTA
  * loss sums and self-resetting counters).  cgs_ctf_mse_spectral_fft takes a
  * cgs_render_fixed image, rows as cgs_ctf_mse_spectral_fixed_rows (NULL: row
- * b), and writes the upstream in CGS_LAYOUT_NATURAL: one R2C, one filter/loss
- * kernel, one C2R per batch (cgs_ctf_mse takes two transform pairs). */
+ * b): one R2C, one filter/loss kernel, one C2R per batch (cgs_ctf_mse takes two
+ * transform pairs).  upstream_layout CGS_LAYOUT_NATURAL, or CGS_LAYOUT_ROWPAIR
+ * (even D; an in-place interleave after the C2R, else CGS_ERR_UNSUPPORTED). */
 int64_t cgs_obs_spectrum_fft_elems(int32_t size, int32_t B);
 size_t cgs_spectral_fft_workspace_bytes(int32_t size, int32_t B);
 int cgs_obs_spectrum_fft(void *plan, const float *obs, const double *ctf, int32_t B, cgs_grid grid, void *spectrum,
                          float *spec, void *stream);
 int cgs_ctf_mse_spectral_fft(void *plan, const int32_t *render_fixed, const float *render_scale, const float *obs_spec,
                              const int64_t *rows, int32_t B, cgs_grid grid, void *spectrum, void *workspace,
-                             float *upstream, double *loss, int32_t *status, void *stream);
+                             float *upstream, double *loss, int32_t *status, int32_t upstream_layout,
+                             void *stream);
 
 /* Batched Fourier filter out = Re ifft2(F fft2(in)), per image F = H_sym (CTF,
  * ctf f64 [B][8], may be NULL) x the sub-pixel shift ramp

@@ -86,7 +86,7 @@ PROTOTYPES = {
     "cgs_obs_spectrum_fft_elems": (I64, [I32, I32]),
     "cgs_spectral_fft_workspace_bytes": (ctypes.c_size_t, [I32, I32]),
     "cgs_obs_spectrum_fft": (ctypes.c_int, [P, P, P, I32, G, P, P, P]),
-    "cgs_ctf_mse_spectral_fft": (ctypes.c_int, [P, P, P, P, P, I32, G, P, P, P, P, P, P]),
+    "cgs_ctf_mse_spectral_fft": (ctypes.c_int, [P, P, P, P, P, I32, G, P, P, P, P, P, I32, P]),
     "cgs_voxelize_workspace_bytes": (ctypes.c_size_t, [I64]),
     "cgs_voxelize": (ctypes.c_int, [P, I64, G, P, P, P, P]),
     "cgs_bwd_groups": (I64, [I32, I32]),

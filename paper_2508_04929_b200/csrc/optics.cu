@@ -1349,18 +1349,33 @@ __global__ void __launch_bounds__(kSpecFftThreads) ctf_mse_spec_fft_kernel(
     const float *Hh = reinterpret_cast<const float *>(O + n);
     float2 *Z = spectrum + (int64_t)b * n;
     const float d2 = (float)D * (float)D, sc = 2.f / d2;
+    constexpr int kPer = kSpecFftElems / kSpecFftThreads;
+    const int i0 = blockIdx.x * kSpecFftElems + threadIdx.x;
+    // all loads of the thread's elements first: one DRAM round trip, not kPer
+    float2 z[kPer], o[kPer];
+    float h[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int i = i0 + j * kSpecFftThreads;
+        if (i < n) {
+            z[j] = Z[i];
+            o[j] = __ldg(O + i);
+            h[j] = __ldg(Hh + i);
+        }
+    }
     double acc = 0.0;
-    const int end = min(n, (int)(blockIdx.x + 1) * kSpecFftElems);
-    for (int i = blockIdx.x * kSpecFftElems + threadIdx.x; i < end; i += kSpecFftThreads) {
-        const int kx = i % P;
-        const float h = __ldg(Hh + i);
-        const float2 z = Z[i], o = __ldg(O + i);
-        const float hd = h * d2;
-        const float rx = fmaf(hd, z.x, -o.x), ry = fmaf(hd, z.y, -o.y);
-        const double w = (kx == 0 || (!(D & 1) && kx == D / 2)) ? 1.0 : 2.0;
-        acc += w * ((double)rx * rx + (double)ry * ry);
-        const float hs = h * sc;
-        Z[i] = make_float2(hs * rx, hs * ry);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int i = i0 + j * kSpecFftThreads;
+        if (i < n) {
+            const int kx = i % P;
+            const float hd = h[j] * d2;
+            const float rx = fmaf(hd, z[j].x, -o[j].x), ry = fmaf(hd, z[j].y, -o[j].y);
+            const double w = (kx == 0 || (!(D & 1) && kx == D / 2)) ? 1.0 : 2.0;
+            acc += w * ((double)rx * rx + (double)ry * ry);
+            const float hs = h[j] * sc;
+            Z[i] = make_float2(hs * rx, hs * ry);
+        }
     }
     __shared__ double scratch[kSpecFftThreads / 32];
     __shared__ bool last;
@@ -1384,6 +1399,18 @@ __global__ void __launch_bounds__(kSpecFftThreads) ctf_mse_spec_fft_kernel(
             count[b] = 0;
         }
     }
+}
+
+// natural -> CGS_LAYOUT_ROWPAIR in place, one CTA per row pair (even D): the
+// backward's region staging then copies float2 pairs (2% of K5 at 256^2)
+constexpr int kInterleaveThreads = 128;
+__global__ void __launch_bounds__(kInterleaveThreads) rowpair_interleave_kernel(float *__restrict__ buf, int D) {
+    extern __shared__ float rows[];  // [2][D]
+    float *p = buf + (int64_t)blockIdx.x * 2 * D;
+    for (int x = threadIdx.x; x < 2 * D; x += kInterleaveThreads) rows[x] = p[x];
+    __syncthreads();
+    float2 *q = reinterpret_cast<float2 *>(p);
+    for (int x = threadIdx.x; x < D; x += kInterleaveThreads) q[x] = make_float2(rows[x], rows[D + x]);
 }
 
 static int spec_fft_setup(FftPlan *p, int32_t B, cgs_grid grid, cudaStream_t st) {
@@ -1593,10 +1620,12 @@ extern "C" int cgs_obs_spectrum_fft(void *plan, const float *obs, const double *
 extern "C" int cgs_ctf_mse_spectral_fft(void *plan, const int32_t *render_fixed, const float *render_scale,
                                         const float *obs_spec, const int64_t *rows, int32_t B, cgs_grid grid,
                                         void *spectrum, void *workspace, float *upstream, double *loss,
-                                        int32_t *status, void *stream) {
+                                        int32_t *status, int32_t upstream_layout, void *stream) {
     if (!render_fixed || !render_scale || !obs_spec || !spectrum || !workspace || !upstream || !loss || B <= 0 ||
         (const void *)render_fixed == (const void *)upstream)
         return CGS_ERR_ARG;
+    if (upstream_layout != CGS_LAYOUT_NATURAL && upstream_layout != CGS_LAYOUT_ROWPAIR) return CGS_ERR_ARG;
+    if (upstream_layout == CGS_LAYOUT_ROWPAIR && (grid.size & 1)) return CGS_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     int rc = spec_fft_setup((FftPlan *)plan, B, grid, st);
     if (rc) return rc;
@@ -1615,7 +1644,11 @@ extern "C" int cgs_ctf_mse_spectral_fft(void *plan, const int32_t *render_fixed,
                                                                    rows, D, part, cnt, loss, status);
     rc = check_launch("ctf_mse_spec_fft_kernel");
     if (rc) return rc;
-    return cufft_check(cufftExecC2R(p->c2r, (cufftComplex *)spectrum, (cufftReal *)upstream), "cufftExecC2R");
+    rc = cufft_check(cufftExecC2R(p->c2r, (cufftComplex *)spectrum, (cufftReal *)upstream), "cufftExecC2R");
+    if (rc || upstream_layout == CGS_LAYOUT_NATURAL) return rc;
+    rowpair_interleave_kernel<<<(unsigned)((int64_t)B * D / 2), kInterleaveThreads, 2 * D * sizeof(float), st>>>(
+        upstream, D);
+    return check_launch("rowpair_interleave_kernel");
 }
 
 extern "C" int cgs_fourier_filter(const float *in, float *out, int32_t B, cgs_grid grid, const double *ctf,

@@ -423,8 +423,9 @@ class StepPipeline:
         n = 2 + (0 if spectral else 2) + 1 + 1
         if not ctf:
             return n + 1
-        if spectral and self.spectral_kind == "fft":  # fixed_scale + the filter kernel around cuFFT's own
-            return n + (2 if obs_spectrum else 3)
+        if spectral and self.spectral_kind == "fft":  # fixed_scale, filter (+ interleave) around cuFFT's own
+            k = 2 + (self.D % 2 == 0)
+            return n + (k if obs_spectrum else k + 1)
         if spectral:
             return n + (1 if obs_spectrum else 2)
         fused = self.D in (32, 64, 128) and os.environ.get("CGS_CTF_CUFFT", "0") != "1"
@@ -499,12 +500,12 @@ class StepPipeline:
                     _lib.call("cgs_obs_spectrum", _ptr(obs), _ptr(ctf), self.B, self.grid, _ptr(self.obs_spec), s)
                 obs_spec = self.obs_spec
             # the upstream goes out with row pairs interleaved: the backward's region staging is a copy
-            # (cuFFT's C2R writes it in natural order)
-            up_layout = _lib.CGS_LAYOUT_NATURAL if fft else _lib.CGS_LAYOUT_ROWPAIR
+            # (after cuFFT's C2R an in-place interleave; odd sizes stay natural)
+            up_layout = _lib.CGS_LAYOUT_NATURAL if fft and self.D % 2 else _lib.CGS_LAYOUT_ROWPAIR
             if fft:
                 _lib.call("cgs_ctf_mse_spectral_fft", self.plan, _ptr(self.render), _ptr(self._render_scale()),
                           _ptr(obs_spec), _ptr(obs_rows), self.B, self.grid, _ptr(self.spectrum),
-                          _ptr(self.spec_ws), _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), s)
+                          _ptr(self.spec_ws), _ptr(self.upstream), _ptr(self.loss), _ptr(self.status), up_layout, s)
             elif fixed and obs_rows is not None:
                 _lib.call("cgs_ctf_mse_spectral_fixed_rows", _ptr(self.render), _ptr(self._render_scale()),
                           _ptr(obs_spec), _ptr(obs_rows), self.B, self.grid, _ptr(self.upstream), _ptr(self.loss),

@@ -398,18 +398,26 @@ def test_spectral_fft_ctf_mse_matches_oracle(oracle, D):
               ctx.stream)
     status = torch.zeros(1, dtype=torch.int32, device=o.device)
 
-    def k4(rows=None, src=rf):
+    def k4(rows=None, src=rf, layout=_lib.CGS_LAYOUT_NATURAL):
         up = torch.empty((B, D, D), dtype=torch.float32, device=o.device)
         loss = torch.empty(B, dtype=torch.float64, device=o.device)
         _lib.call("cgs_ctf_mse_spectral_fft", plan, src.data_ptr(), scale.data_ptr(), spec.data_ptr(),
                   0 if rows is None else rows.data_ptr(), B, gs, wspec.data_ptr(), ws.data_ptr(), up.data_ptr(),
-                  loss.data_ptr(), status.data_ptr(), ctx.stream)
+                  loss.data_ptr(), status.data_ptr(), layout, ctx.stream)
         return up, loss
 
     up, loss = k4()
     up_again, loss_again = k4()
     rows = torch.tensor([2, 0, 2], dtype=torch.int64, device=o.device)
     up_rows, loss_rows = k4(rows, rf.index_select(0, rows).contiguous())
+    if D % 2 == 0:  # the step's layout: row pairs interleaved after the C2R
+        up_rp, loss_rp = k4(layout=_lib.CGS_LAYOUT_ROWPAIR)
+        assert torch.equal(up_rp, up.view(B, D // 2, 2, D).transpose(2, 3).reshape(B, D, D))
+        assert torch.equal(loss_rp, loss)
+    else:
+        assert ctx.lib.cgs_ctf_mse_spectral_fft(plan, rf.data_ptr(), scale.data_ptr(), spec.data_ptr(), None, B, gs,
+                                                wspec.data_ptr(), ws.data_ptr(), up.data_ptr(), loss.data_ptr(),
+                                                None, _lib.CGS_LAYOUT_ROWPAIR, None) == 4
     torch.cuda.synchronize()
     for b in range(B):
         H = oracle.ctf_evaluate(ctfs[b], grid)
@@ -424,9 +432,10 @@ def test_spectral_fft_ctf_mse_matches_oracle(oracle, D):
     # wrong plan batch, missing workspace
     assert ctx.lib.cgs_ctf_mse_spectral_fft(ctx.plan(D, B + 1), rf.data_ptr(), scale.data_ptr(), spec.data_ptr(),
                                             None, B, gs, wspec.data_ptr(), ws.data_ptr(), up.data_ptr(),
-                                            loss.data_ptr(), None, None) == 1
+                                            loss.data_ptr(), None, _lib.CGS_LAYOUT_NATURAL, None) == 1
     assert ctx.lib.cgs_ctf_mse_spectral_fft(plan, rf.data_ptr(), scale.data_ptr(), spec.data_ptr(), None, B, gs,
-                                            wspec.data_ptr(), None, up.data_ptr(), loss.data_ptr(), None, None) == 1
+                                            wspec.data_ptr(), None, up.data_ptr(), loss.data_ptr(), None,
+                                            _lib.CGS_LAYOUT_NATURAL, None) == 1
 
 
 @pytest.mark.parametrize("D", [64, 128])

@@ -2,8 +2,9 @@
 
     CGS_B200_LIB=... python tools/k4_probe.py [--D 128] [--B 256] [--iters 30]
 
-Times cgs_obs_spectrum (per-step observation records, the e2e path) and
-cgs_ctf_mse_spectral_fixed (the training step's K4) on random images and bench-like
+Times cgs_obs_spectrum (per-step observation records, the e2e path),
+cgs_ctf_mse_spectral_fixed (the training step's K4; the _fft forms at sizes without
+line-FFT kernels) and the real-space cgs_ctf_mse on random images and bench-like
 CTFs; prints ms per launch (CUDA events, median of 5 blocks of `iters` launches)
 and checksums of the loss and upstream so variants can be compared.
 """
@@ -45,20 +46,39 @@ def main():
     # a fixed-point render as cgs_render_fixed leaves it: int32 values in unit `scale`
     scale = torch.tensor([2.0 ** 20], dtype=torch.float32, device="cuda")
     render = (torch.rand((a.B, a.D, a.D), generator=g, device="cuda") * 2.0 ** 20).to(torch.int32)
-    spec = torch.empty(int(ctx.lib.cgs_obs_spectrum_elems(a.D, a.B)), dtype=torch.float32, device="cuda")
+    fft = int(ctx.lib.cgs_obs_spectrum_elems(a.D, a.B)) == 0  # sizes without line-FFT kernels: the cuFFT form
+    elems = ctx.lib.cgs_obs_spectrum_fft_elems(a.D, a.B) if fft else ctx.lib.cgs_obs_spectrum_elems(a.D, a.B)
+    spec = torch.empty(int(elems), dtype=torch.float32, device="cuda")
+    plan = ctx.plan(a.D, a.B)
+    wspec = torch.empty(2 * int(ctx.lib.cgs_fft_spectrum_elems(a.D, a.B)), dtype=torch.float32, device="cuda")
+    ws = torch.zeros(int(ctx.lib.cgs_spectral_fft_workspace_bytes(a.D, a.B)) + 8, dtype=torch.uint8, device="cuda")
     up = torch.empty((a.B, a.D, a.D), dtype=torch.float32, device="cuda")
     loss = torch.empty(a.B, dtype=torch.float64, device="cuda")
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
 
     def obs_rec():
-        _lib.call("cgs_obs_spectrum", obs.data_ptr(), ctf_t.data_ptr(), a.B, gs, spec.data_ptr(), s)
+        if fft:
+            _lib.call("cgs_obs_spectrum_fft", plan, obs.data_ptr(), ctf_t.data_ptr(), a.B, gs, wspec.data_ptr(),
+                      spec.data_ptr(), s)
+        else:
+            _lib.call("cgs_obs_spectrum", obs.data_ptr(), ctf_t.data_ptr(), a.B, gs, spec.data_ptr(), s)
 
     def k4():
-        _lib.call("cgs_ctf_mse_spectral_fixed", render.data_ptr(), scale.data_ptr(), spec.data_ptr(), a.B, gs,
-                  up.data_ptr(), loss.data_ptr(), status.data_ptr(), _lib.CGS_LAYOUT_ROWPAIR, s)
+        if fft:
+            _lib.call("cgs_ctf_mse_spectral_fft", plan, render.data_ptr(), scale.data_ptr(), spec.data_ptr(), 0,
+                      a.B, gs, wspec.data_ptr(), ws.data_ptr(), up.data_ptr(), loss.data_ptr(), status.data_ptr(),
+                      _lib.CGS_LAYOUT_ROWPAIR, s)
+        else:
+            _lib.call("cgs_ctf_mse_spectral_fixed", render.data_ptr(), scale.data_ptr(), spec.data_ptr(), a.B, gs,
+                      up.data_ptr(), loss.data_ptr(), status.data_ptr(), _lib.CGS_LAYOUT_ROWPAIR, s)
+
+    def k4_spatial():  # the real-space K4 (cgs_ctf_mse: two cuFFT transform pairs at sizes without fused kernels)
+        _lib.call("cgs_ctf_mse", plan, up.data_ptr(), obs.data_ptr(), a.B, gs, ctf_t.data_ptr(), wspec.data_ptr(),
+                  0, up2.data_ptr(), loss.data_ptr(), status.data_ptr(), _lib.CGS_LAYOUT_NATURAL, s)
 
     res = {"tag": os.path.basename(a.tag), "D": a.D, "B": a.B}
-    for name, fn in (("obs_spectrum", obs_rec), ("k4", k4)):
+    up2 = torch.empty_like(up)
+    for name, fn in (("obs_spectrum", obs_rec), ("k4", k4), ("k4_spatial", k4_spatial)):
         for _ in range(3):
             fn()
         blocks = []

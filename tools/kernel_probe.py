@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--D", type=int, default=128)
     ap.add_argument("--B", type=int, default=256)
     ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--layout", choices=("rowpair", "natural"), default="rowpair",
+                    help="upstream layout K5 reads (the spectral K4 writes row pairs at 64/128, cuFFT natural)")
     ap.add_argument("--tag", default=os.environ.get("CGS_B200_LIB", "base"))
     a = ap.parse_args()
     grid = cs.GridSpec(a.D, 0.5, 1.5)
@@ -49,6 +51,7 @@ def main():
     G = int(ctx.lib.cgs_bwd_groups(a.B, engine.images_per_group_auto(a.n, a.B)))
     part = torch.empty(G * a.n * 10, dtype=torch.float32, device="cuda")
     s = ctx.stream
+    layout = _lib.CGS_LAYOUT_ROWPAIR if a.layout == "rowpair" else _lib.CGS_LAYOUT_NATURAL
 
     def fwd():
         _lib.call("cgs_render_fixed", splat.data_ptr(), a.n, P.data_ptr(), a.B, gs, out.data_ptr(), None,
@@ -56,9 +59,9 @@ def main():
 
     def bwd():
         _lib.call("cgs_raster_bwd", splat.data_ptr(), a.n, P.data_ptr(), a.B, gs, up.data_ptr(),
-                  _lib.CGS_LAYOUT_ROWPAIR, part.data_ptr(), engine.images_per_group_auto(a.n, a.B), s)
+                  layout, part.data_ptr(), engine.images_per_group_auto(a.n, a.B), s)
 
-    res = {"tag": os.path.basename(a.tag), "n": a.n, "D": a.D, "B": a.B}
+    res = {"tag": os.path.basename(a.tag), "n": a.n, "D": a.D, "B": a.B, "layout": a.layout}
     for name, fn in (("fwd", fwd), ("bwd", bwd)):
         for _ in range(3):
             fn()
