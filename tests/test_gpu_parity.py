@@ -823,6 +823,46 @@ def test_indexed_step_graph_matches_eager_across_reorder():
     assert np.array_equal(a.params_host(), b.params_host())
 
 
+def test_indexed_step_cufft_spectral_graph_vs_eager_and_real_space(monkeypatch):
+    """At a size without line-FFT kernels (96^2) Reconstructor.step runs the cuFFT spectral K4 on
+    the dataset's resident records by row: the graph-replayed step (cuFFT captured) must equal the
+    eager one bitwise, and both must agree with the real-space K4 (CGS_CTF_SPATIAL=1: two cuFFT
+    transform pairs per step, no records) to fp32 rounding."""
+    from paper_2508_04929_b200.optimize import Reconstructor
+
+    D, R = 96, 20
+    grid = cs.GridSpec(D, 0.5, 1.5)
+    rng = np.random.default_rng(29)
+    rot = np.stack([cs.sample_pose(np.random.default_rng(700 + i)).rotation for i in range(R)])
+    obs = (rng.standard_normal((R, D, D)) * 1e-3).astype(np.float32)
+    ctfs = engine.ctf_array([cs.CtfParams(float(d), float(d) + 300.0, 0.4) for d in rng.uniform(1e4, 2e4, R)])
+    mix = cs.init_random(2000, 0, grid)
+    order = rng.permutation(R)
+    batches = [order[i:i + 8] for i in range(0, R, 8)]  # 8, 8, 4
+
+    def run(graphs):
+        r = Reconstructor(grid, mix.params, obs, engine.pose_array(rot), ctfs, batch_size=8)
+        r.use_graphs = graphs
+        losses = [r.step(bi, 2e-3).clone() for bi in batches]
+        torch.cuda.synchronize()
+        return r, torch.cat(losses)
+
+    a, la = run(True)
+    assert a.obs_spec is not None and a.pipeline(8).spectral_kind == "fft"
+    b, lb = run(False)
+    assert torch.equal(la, lb) and torch.equal(a.params, b.params) and torch.equal(a.m, b.m)
+    monkeypatch.setenv("CGS_CTF_SPATIAL", "1")
+    c, lc = run(False)
+    assert c.obs_spec is None and not c.pipeline(8).spectral
+    np.testing.assert_allclose(la.cpu().numpy(), lc.cpu().numpy(), rtol=2e-5)
+    # Adam turns a near-zero gradient's rounding into a full +-lr step, so the updates are compared
+    # norm-wise per parameter column (an element-wise bound would test Adam's sign, not K4)
+    p0 = cs.init_random(2000, 0, grid).params
+    da, dc = a.params_host() - p0, c.params_host() - p0
+    for col in range(da.shape[1]):
+        assert np.linalg.norm(da[:, col] - dc[:, col]) <= 1e-2 * np.linalg.norm(da[:, col]) + 1e-12
+
+
 def test_full_size_c2_properties(oracle):
     """BASELINE configs[1] at full size (50k Gaussians, 128^2, B = 256) through properties that hold
     at any size.  (1) A batch render equals the renders of its images alone to fixed-point
