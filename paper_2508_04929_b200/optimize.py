@@ -585,8 +585,10 @@ class Reconstructor:
     def step_host(self, obs, poses, ctfs, lr: float, *, global_batch: int, loss_out=None):
         """Public end-to-end step from (pinned) HOST buffers of this rank's batch.
 
-        Copies the batch host->device on a dedicated copy stream, runs the step
-        on the current stream once the copy has landed, and copies the per-image
+        Copies the batch host->device on a dedicated copy stream (with a spectral
+        K4 the batch's observation records are made there too, overlapping the
+        previous step), runs the step on the current stream once the copy has
+        landed, and copies the per-image
         losses device->host into ``loss_out`` (pinned).  Nothing synchronises the
         host, so back-to-back calls overlap the next batch's H2D (PCIe) with
         this batch's kernels; the caller synchronises when it needs the numbers.
@@ -602,13 +604,24 @@ class Reconstructor:
         key = (tuple(obs.shape), ctfs is None, int(global_batch))
         slots = self._h2d_slots.get(key)
         if slots is None:
+            # with a spectral K4 the batch's observation records are made on the copy stream right
+            # after its H2D, so they overlap the previous step's kernels instead of running inside
+            # this step; the step then reads them like a resident dataset's
+            per = engine.obs_record_elems(self.ctx, self.grid.size) if ctfs is not None and obs.shape[0] else 0
+
             def slot():
                 sl = {"o": torch.empty(obs.shape, dtype=obs.dtype, device=dev),
                       "p": torch.empty(poses.shape, dtype=poses.dtype, device=dev),
                       "c": None if ctfs is None else torch.empty(ctfs.shape, dtype=ctfs.dtype, device=dev),
+                      "spec": torch.empty((obs.shape[0], per), dtype=torch.float32, device=dev) if per else None,
                       "hyper": torch.empty(4, dtype=torch.float64, device=dev), "done": None}
-                segs, pipe = self._segments(obs.shape[0], global_batch,
-                                            lambda: (sl["o"], sl["p"], sl["c"], None), sl["hyper"])
+                if sl["spec"] is not None:
+                    def inputs():
+                        return None, sl["p"], sl["c"], sl["spec"]
+                else:
+                    def inputs():
+                        return sl["o"], sl["p"], sl["c"], None
+                segs, pipe = self._segments(obs.shape[0], global_batch, inputs, sl["hyper"])
                 sl["runner"], sl["pipe"] = _StepRunner(segs, self.use_graphs, self._whole_graph), pipe
                 return sl
             slots = self._h2d_slots[key] = [slot(), slot(), 0]
@@ -625,6 +638,8 @@ class Reconstructor:
             sl["p"].copy_(poses, non_blocking=True)
             if ctfs is not None:
                 sl["c"].copy_(ctfs, non_blocking=True)
+            if sl["spec"] is not None:
+                engine.obs_spectra(self.ctx, sl["o"], sl["c"], self.gs, out=sl["spec"])
         compute.wait_stream(cs)
         sl["runner"].run()
         self.t = t
