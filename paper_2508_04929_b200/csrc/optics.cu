@@ -1415,6 +1415,10 @@ __global__ void __launch_bounds__(kInterleaveThreads) rowpair_interleave_kernel(
 
 static int spec_fft_setup(FftPlan *p, int32_t B, cgs_grid grid, cudaStream_t st) {
     if (!p || p->D != grid.size || p->B != B) return CGS_ERR_ARG;
+    if (B > 65535) {  // images on the grid's y dimension
+        set_error_detail("cgs spectral fft", "batch above 65535 images");
+        return CGS_ERR_UNSUPPORTED;
+    }
     int rc = cufft_check(cufftSetStream(p->r2c, st), "cufftSetStream");
     if (rc) return rc;
     return cufft_check(cufftSetStream(p->c2r, st), "cufftSetStream");
