@@ -232,7 +232,8 @@ int cgs_ctf_mse_spectral_fixed(const int32_t *render_fixed, const float *render_
 int cgs_ctf_mse_spectral_fixed_rows(const int32_t *render_fixed, const float *render_scale, const float *obs_spec,
                                     const int64_t *rows, int32_t B, cgs_grid grid, float *upstream, double *loss,
                                     int32_t *status, int32_t upstream_layout, void *stream);
-/* The spectral K4 through cuFFT, for the other sizes (C4's 256^2 half spectrum
+/* The spectral K4 through cuFFT (the apply_ctf -> loss_mse -> apply_ctf chain of
+ * train.py:151-155, optics.py:124-141), for the other sizes (C4's 256^2 half spectrum
  * does not fit one CTA).  Records: F(obs) then H_sym / D^2, natural [ky][kx]
  * half spectrum, n = D (D/2+1): 3n floats per record, padded to an even count
  * (cgs_obs_spectrum_fft_elems(D, B) floats in all, any D >= 2); they are
