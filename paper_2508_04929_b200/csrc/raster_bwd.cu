@@ -162,6 +162,10 @@ constexpr float kMinSeedLog2 = -100.f;  // joint row-pair walks need every live 
 #endif
 constexpr float kBwdCut = (CGS_BWD_CUT > 0.f && CGS_BWD_CUT < kCutoffSq) ? CGS_BWD_CUT : kCutoffSq;
 
+// kUnroll4: four columns per loop trip instead of two (the large-image kernel: rows at 256^2 are
+// wide enough for the shorter loop control to pay, K5 1.686 -> 1.670 ms at C4; at 128^2 the
+// longer remainder peel costs more, 0.698 -> 0.705 ms).  Same operations in the same order.
+template <bool kUnroll4>
 __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int b0, int W, int xlo, int xhi,
                                              int ya, int yb, const Splat2 &s, float c, Moments &M) {
     const float nk = -s.k, A = s.A, Ck = s.Ck, isp = s.inv_sqrt_p00;
@@ -218,13 +222,32 @@ __device__ __forceinline__ void bwd_rowpairs(const float2 *__restrict__ blk, int
             // two columns per trip, both loaded at the top of the trip (no value
             // carried across trips: a software-pipelined load costs register
             // moves in the loop); an odd column count peels one column first
-            const float2 *qe = q + (n - 1);
-            if (n & 1) column(*q++);
+            if constexpr (kUnroll4) {  // four columns per trip; n mod 4 columns peeled first
+                const float2 *qe = q + n;
+                if (n & 1) column(*q++);
+                if (n & 2) {
+                    const float2 V0 = q[0], V1 = q[1];
+                    column(V0);
+                    column(V1);
+                    q += 2;
+                }
 #pragma unroll 1
-            for (; q < qe; q += 2) {
-                const float2 V0 = q[0], V1 = q[1];
-                column(V0);
-                column(V1);
+                for (; q < qe; q += 4) {
+                    const float2 V0 = q[0], V1 = q[1], V2 = q[2], V3 = q[3];
+                    column(V0);
+                    column(V1);
+                    column(V2);
+                    column(V3);
+                }
+            } else {
+                const float2 *qe = q + (n - 1);
+                if (n & 1) column(*q++);
+#pragma unroll 1
+                for (; q < qe; q += 2) {
+                    const float2 V0 = q[0], V1 = q[1];
+                    column(V0);
+                    column(V1);
+                }
             }
             const float nf = (float)n;
             const float2 Dn = f2add(DX, f2pack(nf, nf));
@@ -579,7 +602,8 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
             __syncthreads();
             const int ya = max(ylo, by0), yb = min(yhi, by1);
             if (ya <= yb)
-                bwd_rowpairs(reinterpret_cast<const float2 *>(reg), by0, W, R.x0, R.x1, ya, yb, s, c2A, M);
+                bwd_rowpairs<kRegF == 0>(reinterpret_cast<const float2 *>(reg), by0, W, R.x0, R.x1, ya, yb, s, c2A,
+                                         M);
         }
         if (ylo <= yhi) {
             float acc[CGS_ACC_STRIDE];
