@@ -23,7 +23,8 @@
 //  * raster_bwd_region_kernel (default, natural layout): per image the CTA
 //    stages only the union of its Gaussians' footprint boxes (Morton order
 //    keeps it small), row-pair interleaved, and walks two rows per packed step
-//    (bwd_rowpairs); 256 threads, 64 registers, 4 CTAs per SM.
+//    (bwd_rowpairs); up to 128^2 128 threads, 70 registers, 6 CTAs per SM,
+//    beyond it 256 threads, 64 registers, 4 CTAs per SM (RegShape).
 //  * raster_bwd_db_kernel (CGS_BWD_KERNEL=db, D <= 160): whole upstream images
 //    double-buffered with 1-D bulk async copies (TMA engine, mbarrier), one row
 //    per step (bwd_rows).
@@ -492,7 +493,23 @@ __global__ void __launch_bounds__(kBwdThreadsBand, 3) raster_bwd_band_kernel(
 #ifndef CGS_BWD_MINB
 #define CGS_BWD_MINB 4
 #endif
+#ifndef CGS_BWD_REG_THREADS_SMALL
+#define CGS_BWD_REG_THREADS_SMALL 128
+#endif
+#ifndef CGS_BWD_MINB_SMALL
+#define CGS_BWD_MINB_SMALL 7
+#endif
 constexpr int kRegThreads = CGS_BWD_REG_THREADS;
+// CTA shape per band kind.  The static 24 KB band (D <= 128) runs 128 threads at up to 7 CTAs
+// per SM: 70 registers and no spills (256 threads at 4 per SM allow 64 and spill), 6 CTAs per SM
+// by shared memory; C2 K5 0.698 -> 0.690 ms, bitwise the same partials.  The 40 KB dynamic band
+// (larger images) keeps 256 threads at 4 per SM: at 128 threads its band per thread doubles and
+// C4's K5 went 1.67 -> 1.88 ms.
+template <int kRegF>
+struct RegShape {
+    static constexpr int kT = kRegF > 0 ? CGS_BWD_REG_THREADS_SMALL : kRegThreads;
+    static constexpr int kMinB = kRegF > 0 ? CGS_BWD_MINB_SMALL : CGS_BWD_MINB;
+};
 constexpr int kMaxPoseImages = 64;  // image groups up to this size keep fp32 poses in shared memory
 #ifndef CGS_BWD_REG_FLOATS
 #define CGS_BWD_REG_FLOATS 6144
@@ -510,23 +527,24 @@ constexpr int kRegFloatsLarge = CGS_BWD_REG_FLOATS_LARGE;
 // static shared memory of kRegF floats (128^2: the static array measured 0.2% faster), or 0 for a
 // dynamic band of regf_dyn floats (larger images)
 template <bool kPoseSmem, bool kRowPair, int kRegF>
-__global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_kernel(
+__global__ void __launch_bounds__(RegShape<kRegF>::kT, RegShape<kRegF>::kMinB) raster_bwd_region_kernel(
     const float *__restrict__ splat, int64_t n, const double *__restrict__ poses, int B, GridF G,
     const float *__restrict__ upstream, float *__restrict__ partial, int ipg, int regf_dyn) {
+    constexpr int kT = RegShape<kRegF>::kT;
     // regf + kRowPad floats, row-pair interleaved (bwd_rowpairs)
     __shared__ __align__(16) float reg_static[kRegF > 0 ? kRegF + kRowPad : 1];
     extern __shared__ __align__(16) float reg_dyn[];
     float *reg = kRegF > 0 ? reg_static : reg_dyn;
     const int regf = kRegF > 0 ? kRegF : regf_dyn;
-    __shared__ int red[2][4][kRegThreads / 32];
+    __shared__ int red[2][4][kT / 32];
     // Register budget: the walk needs ~40 registers, so per-thread state that
     // is touched once per image lives outside the register file: the world
     // accumulator in shared memory (column-major: conflict-free), poses as fp32
     // in shared memory, and the splat record re-read from L1 each image.
-    __shared__ float accs[CGS_ACC_STRIDE * kRegThreads];
+    __shared__ float accs[CGS_ACC_STRIDE * kT];
     __shared__ float poses_f[kMaxPoseImages * 8];
     const int D = G.D;
-    const int64_t g = (int64_t)blockIdx.x * kRegThreads + threadIdx.x;
+    const int64_t g = (int64_t)blockIdx.x * kT + threadIdx.x;
     const bool valid = g < n;
     const int grp = blockIdx.y;
     const int b_begin = grp * ipg, b_end = min(B, b_begin + ipg);
@@ -534,13 +552,13 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
     const float ext = kBwdCut < kCutoffSq ? 1.0001f * sqrtf(kBwdCut / kCutoffSq) : 1.f;
     constexpr bool pose_smem = kPoseSmem;  // host guarantees ipg <= kMaxPoseImages when set
     if (pose_smem)
-        for (int i = threadIdx.x; i < (b_end - b_begin) * 8; i += kRegThreads) {
+        for (int i = threadIdx.x; i < (b_end - b_begin) * 8; i += kT) {
             const int k = i & 7;
             poses_f[i] = (float)poses[12 * (int64_t)(b_begin + (i >> 3)) + (k < 6 ? k : k + 3)];
         }
 #pragma unroll
-    for (int c = 0; c < CGS_ACC_STRIDE; ++c) accs[c * kRegThreads + threadIdx.x] = 0.f;
-    for (int i = threadIdx.x; i < regf + kRowPad; i += kRegThreads) reg[i] = 0.f;  // finite reads past spans
+    for (int c = 0; c < CGS_ACC_STRIDE; ++c) accs[c * kT + threadIdx.x] = 0.f;
+    for (int i = threadIdx.x; i < regf + kRowPad; i += kT) reg[i] = 0.f;  // finite reads past spans
     __syncthreads();
     auto pose = [&](int b) {
         if (!pose_smem) return load_pose_f(poses, b);
@@ -586,13 +604,13 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
                 float fi = (float)threadIdx.x + 0.5f;
                 if (kRowPair) {  // the pair rows are already interleaved in HBM (even D)
                     const float2 *sb2 = reinterpret_cast<const float2 *>(src) + (by0 >> 1) * D + R.x0;
-                    for (int i = threadIdx.x; i < nel; i += kRegThreads, fi += (float)kRegThreads) {
+                    for (int i = threadIdx.x; i < nel; i += kT, fi += (float)kT) {
                         const int j = __float_as_int(__fmaf_rd(fi, invW, 12582912.0f)) - 0x4B400000;
                         reg2[i] = __ldg(sb2 + j * D + (i - j * W));
                     }
                 } else {
                     const float *sb = src + by0 * D + R.x0;
-                    for (int i = threadIdx.x; i < nel; i += kRegThreads, fi += (float)kRegThreads) {
+                    for (int i = threadIdx.x; i < nel; i += kT, fi += (float)kT) {
                         const int j = __float_as_int(__fmaf_rd(fi, invW, 12582912.0f)) - 0x4B400000;
                         const float *p = sb + j * (2 * D) + (i - j * W);
                         reg2[i] = f2pack(__ldg(p), by0 + 2 * j + 1 < D ? __ldg(p + D) : 0.f);
@@ -608,16 +626,16 @@ __global__ void __launch_bounds__(kRegThreads, CGS_BWD_MINB) raster_bwd_region_k
         if (ylo <= yhi) {
             float acc[CGS_ACC_STRIDE];
 #pragma unroll
-            for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = accs[c * kRegThreads + threadIdx.x];
+            for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = accs[c * kT + threadIdx.x];
             accumulate_world(M, s, pose(b), G.inv_h, acc);
 #pragma unroll
-            for (int c = 0; c < CGS_ACC_STRIDE; ++c) accs[c * kRegThreads + threadIdx.x] = acc[c];
+            for (int c = 0; c < CGS_ACC_STRIDE; ++c) accs[c * kT + threadIdx.x] = acc[c];
         }
     }
     if (valid) {
         float acc[CGS_ACC_STRIDE];
 #pragma unroll
-        for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = accs[c * kRegThreads + threadIdx.x];
+        for (int c = 0; c < CGS_ACC_STRIDE; ++c) acc[c] = accs[c * kT + threadIdx.x];
         store_partial(partial, grp, n, g, acc);
     }
 }
@@ -678,7 +696,8 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
     const int regf = D <= 128 ? kRegFloats : kRegFloatsLarge;
     if (layout == CGS_LAYOUT_ROWPAIR && ((D & 1) || D > regf / 2)) return CGS_ERR_UNSUPPORTED;
     if ((layout == CGS_LAYOUT_NATURAL && variant == 0 && D <= regf / 2) || layout == CGS_LAYOUT_ROWPAIR) {
-        dim3 g((unsigned)((n + kRegThreads - 1) / kRegThreads), (unsigned)G);
+        const int threads = regf == kRegFloats ? RegShape<kRegFloats>::kT : RegShape<0>::kT;
+        dim3 g((unsigned)((n + threads - 1) / threads), (unsigned)G);
         const GridF gf = make_grid_f(grid);
         const bool ps = images_per_group <= kMaxPoseImages;
         const size_t smem = (size_t)(regf + kRowPad) * sizeof(float);
@@ -689,7 +708,7 @@ extern "C" int cgs_raster_bwd(const float *splat, int64_t n, const double *poses
                 const int rc = ensure_smem_limit((const void *)kern, dyn + 16 * 1024, "raster_bwd_region_kernel");
                 if (rc) return rc;
             }
-            kern<<<g, kRegThreads, dyn, st>>>(splat, n, poses, B, gf, upstream, partial, images_per_group, regf);
+            kern<<<g, threads, dyn, st>>>(splat, n, poses, B, gf, upstream, partial, images_per_group, regf);
             return CGS_OK;
         };
         int rc;
