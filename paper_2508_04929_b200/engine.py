@@ -35,7 +35,7 @@ DEFAULT_TILE = 32
 # overrides for A/B).  Large mixtures take more images per group (images_per_group()).
 DEFAULT_IMAGES_PER_GROUP = int(os.environ.get("CGS_IMAGES_PER_GROUP", "10"))
 # image-group heuristic in units of 256-Gaussian blocks at 4 per SM (raster_bwd.cu kRegThreads; the
-# 128^2 kernel runs 128-thread CTAs, twice the blocks, at up to 6 per SM: the same ~8 waves)
+# 128^2 kernel runs 128-thread CTAs, twice the blocks at up to 6 per SM: ~11 waves instead of 8)
 _BWD_THREADS = 256
 _BWD_TARGET_CTAS = 4736   # 8 waves of 148 SMs x 4 resident CTAs
 _MAX_POSE_IMAGES = 64     # groups up to this size keep their poses in shared memory
