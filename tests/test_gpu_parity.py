@@ -763,17 +763,20 @@ def test_full_step_large_footprints_d256(oracle):
     grads_close(grads, ref_grads, GRAD_TOL, 1e-6)
 
 
-def test_step_host_graph_replay_matches_eager():
+@pytest.mark.parametrize("D", [64, 96])
+def test_step_host_graph_replay_matches_eager(D):
     """step_host replays each input slot's step as a CUDA graph (Adam's lr / bias corrections
-    read from device memory); four steps must leave exactly the parameters and losses of the
-    eager step_batch path (the kernels are deterministic)."""
+    read from device memory) and makes the batch's spectral-K4 records on its copy stream (line
+    FFTs at 64^2, cuFFT with its own plan at 96^2); four steps must leave exactly the parameters
+    and losses of the eager step_batch path, which makes them inside the step (the kernels are
+    deterministic)."""
     from paper_2508_04929_b200.optimize import Reconstructor
 
-    grid = cs.GridSpec(64, 0.5, 1.5)
+    grid = cs.GridSpec(D, 0.5, 1.5)
     rng = np.random.default_rng(9)
     R = 24
     rot = np.stack([cs.sample_pose(np.random.default_rng(300 + i)).rotation for i in range(R)])
-    obs = (rng.standard_normal((R, 64, 64)) * 1e-3).astype(np.float32)
+    obs = (rng.standard_normal((R, D, D)) * 1e-3).astype(np.float32)
     ctfs = engine.ctf_array([cs.CtfParams(float(d), float(d)) for d in rng.uniform(1e4, 2e4, R)])
     mix = cs.init_random(3000, 0, grid)
     a = Reconstructor(grid, mix.params, obs, engine.pose_array(rot), ctfs, batch_size=8)
